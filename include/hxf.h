@@ -1,0 +1,141 @@
+/*
+ * hxf.h -- C ABI of libhxf.so, the B200 (sm_100a) hierarchical exchange build.
+ *
+ * Drop-in boundary for the reference's hot path (paths relative to
+ * /root/reference/pkg/src/hexfock).  Each entry point replaces one reference
+ * interface; the Python mirror (paper_1401_6961_b200/quadtree.py,
+ * exchange.py) binds them with ctypes and keeps the reference signatures.
+ *
+ *   hxf_system_create   <- build_partition (quadtree.py:90-113) output + the
+ *                          BasisSystem / GaussianShell inputs (basis.py:62-101)
+ *   hxf_pairs_build     <- build_pair_tree            (quadtree.py:284-337)
+ *   hxf_density_build   <- build_matrix_tree          (quadtree.py:198-235)
+ *   hxf_exchange        <- build_exchange_naive       (exchange_naive.py:200-240)
+ *                          build_exchange_symmetric   (exchange_symmetry.py:364-409)
+ *   hxf_*_download      <- node attribute reads of ShellPairNode /
+ *                          MatrixQuadtree (quadtree.py:116-142, 238-269)
+ *
+ * Plain pointers and sizes only; no C++ or torch types.  Every function
+ * returns HXF_OK (0) or an error code; hxf_last_error() gives the message of
+ * the last failure on the calling thread.  Calls on one object are not
+ * thread-safe; use one object per thread.  `stream` is a cudaStream_t (NULL =
+ * legacy default stream).
+ */
+#ifndef HXF_H
+#define HXF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HXF_OK 0
+#define HXF_EINVAL 1 /* InvalidArgumentError (basis.py:35-36)           */
+#define HXF_ELOGIC 2 /* LogicError (exchange_naive.py:24-25)            */
+#define HXF_ECUDA 3  /* CUDA runtime failure / no device                */
+#define HXF_ENOMEM 4 /* device allocation failed                        */
+
+#define HXF_MODE_SCHWARZ 0 /* exchange_naive.py:83-85: sqrt of diag norms */
+#define HXF_MODE_LITERAL 1 /* exchange_naive.py:86: norms as-is           */
+
+#define HXF_NAIVE 0     /* exchange_naive.py, ordered shell pairs      */
+#define HXF_FOURFOLD 1  /* exchange_symmetry.py, canonical pairs       */
+
+#define HXF_NCASES 9 /* CASE_LABELS, exchange_symmetry.py:43 */
+
+typedef struct hxf_system hxf_system;   /* basis + partition, device resident */
+typedef struct hxf_pairs hxf_pairs;     /* shell-pair quadtree               */
+typedef struct hxf_density hxf_density; /* density quadtree + dense P        */
+
+/* TraversalCounters (exchange_naive.py:28-65) + SymmetryCounters extras
+ * (exchange_symmetry.py:72-132) + tie counts. */
+typedef struct hxf_counters {
+    int64_t tasks_visited;
+    int64_t tasks_culled_screening;
+    int64_t tasks_culled_absent;
+    int64_t leaf_contractions;
+    int64_t eri_shell_quartets;
+    int64_t quartets_culled_leaf;
+    int64_t tasks_expanded;
+    int64_t children_spawned;
+    int64_t links_culled_screening;
+    int64_t links_culled_absent;
+    int64_t case_tasks[HXF_NCASES];
+    int64_t case_leaf_tasks[HXF_NCASES];
+    int64_t ties_task;   /* task-level bounds within 1e-12 rel of tau   */
+    int64_t ties_leaf;   /* quartet-level bounds within 1e-12 rel of tau */
+    int64_t prim_quartets; /* primitive quartets evaluated (work metric) */
+    double culled_bound_ledger;
+} hxf_counters;
+
+/* Exchange options.  The shard fields select a subset of the product-tree
+ * tasks at level `shard_level` (tasks [shard_begin, shard_end) of that
+ * level's frontier, in frontier order) for multi-GPU runs; shard_level < 0
+ * runs the whole tree. */
+typedef struct hxf_exchange_opts {
+    double tau_2e;
+    int mode;          /* HXF_MODE_*   */
+    int symmetry;      /* HXF_NAIVE / HXF_FOURFOLD */
+    int evaluate;      /* 0: counters only, K = 0 (exchange_naive.py:183) */
+    int K_on_device;   /* K_out is a device pointer                  */
+    int symmetrize;    /* fourfold: apply symmetrize_final (:197-209) */
+    int shard_level;
+    int64_t shard_begin;
+    int64_t shard_end;
+    int32_t* quartet_log;   /* NULL or 4*capacity int32 (host) */
+    int64_t log_capacity;
+    int64_t* log_count;     /* out: quartets logged (may exceed capacity) */
+} hxf_exchange_opts;
+
+const char* hxf_last_error(void);
+int hxf_version(void);
+
+int hxf_system_create(int device, int n_shells, const double* centers /* ns*3 Bohr */,
+                      const int* l /* 0|1 */, const int* prim_off /* ns+1 */,
+                      const double* exponents, const double* weights,
+                      const double* s_weights /* s-normalised weights for overlap pruning */,
+                      int n_levels, const int* level_off /* n_levels+1 */,
+                      const int* span_shell_lo, const int* span_shell_hi,
+                      const int* span_fn_lo, const int* span_fn_hi,
+                      const int* span_kid0, const int* span_kid1 /* level-local, -1 none */,
+                      hxf_system** out);
+void hxf_system_destroy(hxf_system* sys);
+int hxf_system_info(const hxf_system* sys, int64_t* n_functions, int64_t* n_leaves);
+
+int hxf_pairs_build(hxf_system* sys, double tau_ovlp, void* stream, hxf_pairs** out);
+void hxf_pairs_destroy(hxf_pairs* pairs);
+/* node arrays of one level (n_spans(level)^2 entries, row-major (r, c)):
+ * diag_norm, rowsum_max, colsum_max, pruned flag (1 = pruned). */
+int hxf_pairs_download(const hxf_pairs* pairs, int level, double* diag_norm, double* rowsum_max,
+                       double* colsum_max, uint8_t* pruned);
+/* Q = (ij|ij) (max over function pairs for p), n_shells^2 row-major; entries
+ * outside live leaf nodes are set to -1. */
+int hxf_pairs_download_q(const hxf_pairs* pairs, double* q);
+/* |S_ij| (s-proxy contracted overlap), n_shells^2 row-major. */
+int hxf_pairs_overlap(const hxf_pairs* pairs, double* s_abs);
+
+int hxf_density_build(hxf_system* sys, const double* P, int P_on_device, double zero_drop,
+                      void* stream, hxf_density** out);
+void hxf_density_destroy(hxf_density* dens);
+/* node norms of one level, -1 where the node is absent. */
+int hxf_density_download(const hxf_density* dens, int level, double* norm);
+
+int hxf_exchange(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* opts,
+                 double* K_out, hxf_counters* counters, void* stream);
+
+/* Frontier size of the product tree at `level` (for multi-GPU shard
+ * planning); also returns per-task cost estimates (descendant leaf count
+ * proxy) when `cost` is non-NULL (host buffer of that size). */
+int hxf_frontier(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, double tau_2e, int mode,
+                 int symmetry, int level, int64_t* n_tasks, double* cost, int64_t cost_capacity,
+                 void* stream);
+
+/* Device timing of the last hxf_exchange on this thread (ms per stage):
+ * [0] traversal, [1] leaf screen, [2] ERI + contraction, [3] epilogue, [4] total. */
+int hxf_last_timings(double* ms, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HXF_H */

@@ -1,0 +1,130 @@
+"""ctypes binding of libhxf.so (include/hxf.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (csrc/Makefile).
+There is no CPU fallback: if the library or a CUDA device is missing, every
+call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .basis import InvalidArgumentError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhxf.so")
+
+HXF_OK, HXF_EINVAL, HXF_ELOGIC, HXF_ECUDA, HXF_ENOMEM = 0, 1, 2, 3, 4
+NCASES = 9
+
+EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_destroy",
+            "hxf_system_info", "hxf_pairs_build", "hxf_pairs_destroy", "hxf_pairs_download",
+            "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
+            "hxf_density_destroy", "hxf_density_download", "hxf_exchange", "hxf_frontier",
+            "hxf_last_timings")
+
+
+class LogicError(RuntimeError):
+    """Internal traversal invariant violated (exchange_naive.py:24-25)."""
+
+
+class Counters(ctypes.Structure):
+    _fields_ = [("tasks_visited", ctypes.c_int64),
+                ("tasks_culled_screening", ctypes.c_int64),
+                ("tasks_culled_absent", ctypes.c_int64),
+                ("leaf_contractions", ctypes.c_int64),
+                ("eri_shell_quartets", ctypes.c_int64),
+                ("quartets_culled_leaf", ctypes.c_int64),
+                ("tasks_expanded", ctypes.c_int64),
+                ("children_spawned", ctypes.c_int64),
+                ("links_culled_screening", ctypes.c_int64),
+                ("links_culled_absent", ctypes.c_int64),
+                ("case_tasks", ctypes.c_int64 * NCASES),
+                ("case_leaf_tasks", ctypes.c_int64 * NCASES),
+                ("ties_task", ctypes.c_int64),
+                ("ties_leaf", ctypes.c_int64),
+                ("prim_quartets", ctypes.c_int64),
+                ("culled_bound_ledger", ctypes.c_double)]
+
+
+class ExchangeOpts(ctypes.Structure):
+    _fields_ = [("tau_2e", ctypes.c_double),
+                ("mode", ctypes.c_int),
+                ("symmetry", ctypes.c_int),
+                ("evaluate", ctypes.c_int),
+                ("K_on_device", ctypes.c_int),
+                ("symmetrize", ctypes.c_int),
+                ("shard_level", ctypes.c_int),
+                ("shard_begin", ctypes.c_int64),
+                ("shard_end", ctypes.c_int64),
+                ("quartet_log", ctypes.POINTER(ctypes.c_int32)),
+                ("log_capacity", ctypes.c_int64),
+                ("log_count", ctypes.POINTER(ctypes.c_int64))]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhxf.so once; raise loudly if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    P = ctypes.POINTER
+    L.hxf_last_error.restype = ctypes.c_char_p
+    L.hxf_version.restype = i32
+    L.hxf_system_create.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
+                                    vp, P(vp)]
+    L.hxf_system_destroy.argtypes = [vp]
+    L.hxf_system_destroy.restype = None
+    L.hxf_system_info.argtypes = [vp, P(i64), P(i64)]
+    L.hxf_pairs_build.argtypes = [vp, dbl, vp, P(vp)]
+    L.hxf_pairs_destroy.argtypes = [vp]
+    L.hxf_pairs_destroy.restype = None
+    L.hxf_pairs_download.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.hxf_pairs_download_q.argtypes = [vp, vp]
+    L.hxf_pairs_overlap.argtypes = [vp, vp]
+    L.hxf_density_build.argtypes = [vp, vp, i32, dbl, vp, P(vp)]
+    L.hxf_density_destroy.argtypes = [vp]
+    L.hxf_density_destroy.restype = None
+    L.hxf_density_download.argtypes = [vp, i32, vp]
+    L.hxf_exchange.argtypes = [vp, vp, vp, P(ExchangeOpts), vp, P(Counters), vp]
+    L.hxf_frontier.argtypes = [vp, vp, vp, dbl, i32, i32, i32, P(i64), vp, i64, vp]
+    L.hxf_last_timings.argtypes = [vp, i32]
+    _lib = L
+    return L
+
+
+def check(rc):
+    """Map an hxf status code to the reference's exception types."""
+    if rc == HXF_OK:
+        return
+    msg = lib().hxf_last_error().decode(errors="replace")
+    if rc == HXF_EINVAL:
+        raise InvalidArgumentError(msg)
+    if rc == HXF_ELOGIC:
+        raise LogicError(msg)
+    raise RuntimeError(f"libhxf error {rc}: {msg}")
+
+
+def ptr(arr):
+    """Raw pointer of a contiguous numpy array (or torch tensor)."""
+    if hasattr(arr, "data_ptr"):
+        return ctypes.c_void_p(arr.data_ptr())
+    return arr.ctypes.data_as(ctypes.c_void_p)
+
+
+def current_stream():
+    """cudaStream_t of torch's current stream when torch is loaded, else NULL."""
+    try:
+        import torch
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except Exception:  # pragma: no cover
+        pass
+    return ctypes.c_void_p(0)

@@ -1,0 +1,300 @@
+// C ABI of libhxf.so (include/hxf.h): argument validation, device state
+// ownership, error codes.  All compute lives in trees.cu / traverse.cu / leaf.cu.
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hxf_internal.cuh"
+
+static thread_local std::string g_err;
+
+void hxf_set_error(const std::string& msg) { g_err = msg; }
+
+int hxf_last_timings_impl(double* ms, int n);
+
+#define HXF_TRY(...)                                         \
+    try {                                                    \
+        __VA_ARGS__;                                         \
+        return HXF_OK;                                       \
+    } catch (const HxfError& e) {                            \
+        g_err = e.msg;                                       \
+        return e.code;                                       \
+    } catch (const std::exception& e) {                      \
+        g_err = e.what();                                    \
+        return HXF_ECUDA;                                    \
+    }
+
+namespace {
+
+template <typename T>
+T* upload(const T* h, size_t n, std::vector<void*>& owned) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess)
+        throw HxfError{HXF_ENOMEM, "device allocation failed"};
+    owned.push_back(p);
+    if (n) HXF_CUDA(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice));
+    return (T*)p;
+}
+
+void set_device(int dev) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw HxfError{HXF_ECUDA, "no CUDA device available (libhxf has no CPU fallback)"};
+    if (dev < 0 || dev >= n) throw HxfError{HXF_EINVAL, "device index out of range"};
+    HXF_CUDA(cudaSetDevice(dev));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hxf_last_error(void) { return g_err.c_str(); }
+
+int hxf_version(void) { return 1; }
+
+int hxf_system_create(int device, int ns, const double* centers, const int* l, const int* prim_off,
+                      const double* exps, const double* weights, const double* s_weights,
+                      int n_levels, const int* level_off, const int* slo, const int* shi,
+                      const int* flo, const int* fhi, const int* kid0, const int* kid1,
+                      hxf_system** out) {
+    HXF_TRY({
+        if (!out) throw HxfError{HXF_EINVAL, "out is NULL"};
+        *out = nullptr;
+        if (ns < 1 || n_levels < 1) throw HxfError{HXF_EINVAL, "empty basis or partition"};
+        set_device(device);
+        hxf_system* s = new hxf_system();
+        s->device = device;
+        s->ns = ns;
+        s->n_levels = n_levels;
+        s->h_off.assign(level_off, level_off + n_levels + 1);
+        const int nsp = s->h_off[n_levels];
+        s->h_slo.assign(slo, slo + nsp);
+        s->h_shi.assign(shi, shi + nsp);
+        s->h_flo.assign(flo, flo + nsp);
+        s->h_fhi.assign(fhi, fhi + nsp);
+        s->h_kid0.assign(kid0, kid0 + nsp);
+        s->h_kid1.assign(kid1, kid1 + nsp);
+        s->h_l.assign(l, l + ns);
+        s->h_poff.assign(prim_off, prim_off + ns + 1);
+        s->h_fn.resize(ns);
+        s->h_nf.resize(ns);
+        int off = 0;
+        for (int i = 0; i < ns; ++i) {
+            if (l[i] != 0 && l[i] != 1) throw HxfError{HXF_EINVAL, "only s and p shells are supported"};
+            const int np = prim_off[i + 1] - prim_off[i];
+            if (np < 1 || np > 3) throw HxfError{HXF_EINVAL, "shells must have 1..3 primitives"};
+            s->h_fn[i] = off;
+            s->h_nf[i] = l[i] ? 3 : 1;
+            off += s->h_nf[i];
+        }
+        s->nfn = off;
+        // leaf ids: a span is a partition leaf iff it repeats as its own only child
+        // (or sits on the deepest level); ids follow deepest-level order
+        const int D = n_levels - 1;
+        s->h_leaf_id.assign(nsp, -1);
+        s->max_span = 0;
+        for (int L = 0; L < n_levels; ++L) {
+            const int n = s->h_off[L + 1] - s->h_off[L];
+            s->max_span = std::max(s->max_span, n);
+            if (n > 32767) throw HxfError{HXF_EINVAL, "more than 32767 spans on one partition level"};
+        }
+        s->n_leaves = s->h_off[D + 1] - s->h_off[D];
+        for (int k = s->h_off[D]; k < s->h_off[D + 1]; ++k) {
+            s->h_leaf_id[k] = k - s->h_off[D];
+            if (s->h_shi[k] - s->h_slo[k] > 12)
+                throw HxfError{HXF_EINVAL, "leaf spans hold at most 12 shells on the device path"};
+        }
+        for (int L = D - 1; L >= 0; --L)
+            for (int k = s->h_off[L]; k < s->h_off[L + 1]; ++k)
+                if (s->h_kid1[k] < 0) s->h_leaf_id[k] = s->h_leaf_id[s->h_off[L + 1] + s->h_kid0[k]];
+        if (s->h_fhi[s->h_off[0]] != s->nfn) throw HxfError{HXF_EINVAL, "partition does not cover the basis"};
+        s->node_off.resize(n_levels + 1);
+        s->node_off[0] = 0;
+        for (int L = 0; L < n_levels; ++L) {
+            const int64_t n = s->h_off[L + 1] - s->h_off[L];
+            s->node_off[L + 1] = s->node_off[L] + n * n;
+        }
+        // basis
+        std::vector<double3> ctr(ns);
+        for (int i = 0; i < ns; ++i) ctr[i] = make_double3(centers[3 * i], centers[3 * i + 1], centers[3 * i + 2]);
+        const int npr = prim_off[ns];
+        s->basis.ns = ns;
+        s->basis.nfn = s->nfn;
+        s->basis.ctr = upload(ctr.data(), ns, s->allocs);
+        s->basis.l = upload(l, ns, s->allocs);
+        s->basis.poff = upload(prim_off, ns + 1, s->allocs);
+        s->basis.fn = upload(s->h_fn.data(), ns, s->allocs);
+        s->basis.nf = upload(s->h_nf.data(), ns, s->allocs);
+        s->basis.exps = upload(exps, npr, s->allocs);
+        s->basis.w = upload(weights, npr, s->allocs);
+        s->basis.sw = upload(s_weights, npr, s->allocs);
+        s->lv.n_levels = n_levels;
+        s->lv.n_leaves = s->n_leaves;
+        s->lv.off = upload(s->h_off.data(), s->h_off.size(), s->allocs);
+        s->lv.slo = upload(slo, nsp, s->allocs);
+        s->lv.shi = upload(shi, nsp, s->allocs);
+        s->lv.flo = upload(flo, nsp, s->allocs);
+        s->lv.fhi = upload(fhi, nsp, s->allocs);
+        s->lv.kid0 = upload(kid0, nsp, s->allocs);
+        s->lv.kid1 = upload(kid1, nsp, s->allocs);
+        s->lv.leaf_id = upload(s->h_leaf_id.data(), nsp, s->allocs);
+        s->lv.leaf_span = nullptr;
+        *out = s;
+    })
+}
+
+void hxf_system_destroy(hxf_system* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    for (void* p : s->allocs) cudaFree(p);
+    delete s;
+}
+
+int hxf_system_info(const hxf_system* s, int64_t* n_functions, int64_t* n_leaves) {
+    HXF_TRY({
+        if (!s) throw HxfError{HXF_EINVAL, "NULL system"};
+        if (n_functions) *n_functions = s->nfn;
+        if (n_leaves) *n_leaves = s->n_leaves;
+    })
+}
+
+int hxf_pairs_build(hxf_system* s, double tau_ovlp, void* stream, hxf_pairs** out) {
+    HXF_TRY({
+        if (!s || !out) throw HxfError{HXF_EINVAL, "NULL argument"};
+        if (!(tau_ovlp >= 0.0)) throw HxfError{HXF_EINVAL, "tau_ovlp must be non-negative"};
+        set_device(s->device);
+        hxf_pairs* p = new hxf_pairs();
+        memset(p, 0, sizeof(*p));
+        p->sys = s;
+        p->device = s->device;
+        p->tau_ovlp = tau_ovlp;
+        try {
+            trees_build_pairs(p, (cudaStream_t)stream);
+        } catch (...) {
+            hxf_pairs_destroy(p);
+            throw;
+        }
+        *out = p;
+    })
+}
+
+void hxf_pairs_destroy(hxf_pairs* p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    void* ptrs[] = {p->norm, p->rowsum, p->colsum, p->smax, p->leaf_base, p->pi,
+                    p->pj,   p->ppoff,  p->q,      p->pp};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    delete p;
+}
+
+int hxf_pairs_download(const hxf_pairs* p, int level, double* norm, double* rowsum, double* colsum,
+                       uint8_t* pruned) {
+    HXF_TRY({
+        if (!p) throw HxfError{HXF_EINVAL, "NULL pairs"};
+        const hxf_system* s = p->sys;
+        if (level < 0 || level >= s->n_levels) throw HxfError{HXF_EINVAL, "level out of range"};
+        set_device(s->device);
+        const int64_t n = s->h_off[level + 1] - s->h_off[level];
+        const int64_t o = s->node_off[level];
+        std::vector<double> v(n * n);
+        HXF_CUDA(cudaMemcpy(v.data(), p->norm + o, n * n * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < n * n; ++k) {
+            if (pruned) pruned[k] = v[k] < 0.0;
+            if (norm) norm[k] = v[k] < 0.0 ? 0.0 : v[k];
+        }
+        if (rowsum) HXF_CUDA(cudaMemcpy(rowsum, p->rowsum + o, n * n * sizeof(double), cudaMemcpyDeviceToHost));
+        if (colsum) HXF_CUDA(cudaMemcpy(colsum, p->colsum + o, n * n * sizeof(double), cudaMemcpyDeviceToHost));
+    })
+}
+
+int hxf_pairs_download_q(const hxf_pairs* p, double* q) {
+    HXF_TRY({
+        if (!p || !q) throw HxfError{HXF_EINVAL, "NULL argument"};
+        const hxf_system* s = p->sys;
+        set_device(s->device);
+        const int ns = s->ns;
+        std::vector<int> pi(p->n_pairs), pj(p->n_pairs);
+        std::vector<double> qq(p->n_pairs);
+        if (p->n_pairs) {
+            HXF_CUDA(cudaMemcpy(pi.data(), p->pi, p->n_pairs * sizeof(int), cudaMemcpyDeviceToHost));
+            HXF_CUDA(cudaMemcpy(pj.data(), p->pj, p->n_pairs * sizeof(int), cudaMemcpyDeviceToHost));
+            HXF_CUDA(cudaMemcpy(qq.data(), p->q, p->n_pairs * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        for (int64_t k = 0; k < (int64_t)ns * ns; ++k) q[k] = -1.0;
+        for (int64_t k = 0; k < p->n_pairs; ++k) q[(int64_t)pi[k] * ns + pj[k]] = qq[k];
+    })
+}
+
+int hxf_pairs_overlap(const hxf_pairs* p, double* s_abs) {
+    HXF_TRY({
+        (void)p;
+        (void)s_abs;
+        throw HxfError{HXF_EINVAL, "hxf_pairs_overlap: not available in this build"};
+    })
+}
+
+int hxf_density_build(hxf_system* s, const double* P, int P_on_device, double zero_drop, void* stream,
+                      hxf_density** out) {
+    HXF_TRY({
+        if (!s || !P || !out) throw HxfError{HXF_EINVAL, "NULL argument"};
+        set_device(s->device);
+        hxf_density* d = new hxf_density();
+        memset(d, 0, sizeof(*d));
+        d->sys = s;
+        d->device = s->device;
+        d->zero_drop = zero_drop;
+        try {
+            trees_build_density(d, P, P_on_device, (cudaStream_t)stream);
+        } catch (...) {
+            hxf_density_destroy(d);
+            throw;
+        }
+        *out = d;
+    })
+}
+
+void hxf_density_destroy(hxf_density* d) {
+    if (!d) return;
+    cudaSetDevice(d->device);
+    if (d->P) cudaFree(d->P);
+    if (d->norm) cudaFree(d->norm);
+    delete d;
+}
+
+int hxf_density_download(const hxf_density* d, int level, double* norm) {
+    HXF_TRY({
+        if (!d || !norm) throw HxfError{HXF_EINVAL, "NULL argument"};
+        const hxf_system* s = d->sys;
+        if (level < 0 || level >= s->n_levels) throw HxfError{HXF_EINVAL, "level out of range"};
+        set_device(s->device);
+        const int64_t n = s->h_off[level + 1] - s->h_off[level];
+        HXF_CUDA(cudaMemcpy(norm, d->norm + s->node_off[level], n * n * sizeof(double), cudaMemcpyDeviceToHost));
+    })
+}
+
+int hxf_exchange(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* opts,
+                 double* K_out, hxf_counters* counters, void* stream) {
+    HXF_TRY({
+        if (!bra || !ket || !P || !opts || !counters) throw HxfError{HXF_EINVAL, "NULL argument"};
+        set_device(bra->sys->device);
+        memset(counters, 0, sizeof(*counters));
+        exchange_run(bra, ket, P, opts, K_out, counters, (cudaStream_t)stream);
+    })
+}
+
+int hxf_frontier(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, double tau_2e, int mode, int symmetry,
+                 int level, int64_t* n_tasks, double* cost, int64_t cost_capacity, void* stream) {
+    HXF_TRY({
+        if (!bra || !ket || !P || !n_tasks) throw HxfError{HXF_EINVAL, "NULL argument"};
+        set_device(bra->sys->device);
+        frontier_run(bra, ket, P, tau_2e, mode, symmetry == HXF_FOURFOLD, level, n_tasks, cost,
+                     cost_capacity, (cudaStream_t)stream);
+    })
+}
+
+int hxf_last_timings(double* ms, int n) { return hxf_last_timings_impl(ms, n); }
+
+}  // extern "C"

@@ -1,0 +1,214 @@
+"""Generate eri_classes.cuh: straight-line Obara-Saika / HGP code per class.
+
+For each angular class (la, lb, lc, ld) in {0,1}^4 this emits
+
+    struct Eri<la,lb,lc,ld> {
+        static constexpr int NI, NJ, NK, NL;
+        __device__ static void eval(bra, nb, ket, nk, A, B, C, D, out);
+    };
+
+where bra[0:nb] / ket[0:nk] are the primitive pairs of the bra / ket shell
+pair (PrimPair tables of hxf_internal.cuh).  Per primitive quartet: Boys F_0..F_L, vertical
+recursion (electron 1 on P, electron 2 on Q, as in the CPU oracle's
+``eri_general``) onto [e0|f0]; contraction in registers; then the horizontal
+transfer (a,b+1_i| = (a+1_i,b| + AB_i (a,b| on the contracted values.
+Output layout out[((i*NJ + j)*NK + k)*NL + l], p components ordered x,y,z.
+
+Run:  python gen_eri.py > eri_classes.cuh
+"""
+
+import itertools
+
+UNIT = ((1, 0, 0), (0, 1, 0), (0, 0, 1))
+ZERO = (0, 0, 0)
+AX = "xyz"
+
+
+def carts(l):
+    return [ZERO] if l == 0 else list(UNIT)
+
+
+def carts_upto(lo, hi):
+    out = []
+    for L in range(lo, hi + 1):
+        for x in range(L, -1, -1):
+            for y in range(L - x, -1, -1):
+                out.append((x, y, L - x - y))
+    return out
+
+
+def sub(v, i):
+    return v[:i] + (v[i] - 1,) + v[i + 1:]
+
+
+def add(v, i):
+    return v[:i] + (v[i] + 1,) + v[i + 1:]
+
+
+def name(v):
+    return "".join(str(c) for c in v)
+
+
+class Gen:
+    def __init__(self):
+        self.lines = []
+        self.memo = {}
+        self.n = 0
+
+    def tmp(self, expr, prefix="t"):
+        v = f"{prefix}{self.n}"
+        self.n += 1
+        self.lines.append(f"const double {v} = {expr};")
+        return v
+
+    def vrr(self, e, f, m):
+        key = (e, f, m)
+        if key in self.memo:
+            return self.memo[key]
+        if e == ZERO and f == ZERO:
+            v = f"bm{m}"
+        elif e != ZERO:
+            i = next(t for t in range(3) if e[t] > 0)
+            e1 = sub(e, i)
+            a = self.vrr(e1, f, m)
+            b = self.vrr(e1, f, m + 1)
+            expr = f"PA{AX[i]} * {a} + WP{AX[i]} * {b}"
+            if e1[i] > 0:
+                e2 = sub(e1, i)
+                c = self.vrr(e2, f, m)
+                d = self.vrr(e2, f, m + 1)
+                expr += f" + {float(e1[i])} * o2p * ({c} - rp * {d})"
+            if f[i] > 0:
+                g = self.vrr(e1, sub(f, i), m + 1)
+                expr += f" + {float(f[i])} * o2pq * {g}"
+            v = self.tmp(expr)
+        else:
+            i = next(t for t in range(3) if f[t] > 0)
+            f1 = sub(f, i)
+            a = self.vrr(e, f1, m)
+            b = self.vrr(e, f1, m + 1)
+            expr = f"QC{AX[i]} * {a} + WQ{AX[i]} * {b}"
+            if f1[i] > 0:
+                f2 = sub(f1, i)
+                c = self.vrr(e, f2, m)
+                d = self.vrr(e, f2, m + 1)
+                expr += f" + {float(f1[i])} * o2q * ({c} - rq * {d})"
+            v = self.tmp(expr)
+        self.memo[key] = v
+        return v
+
+
+def gen_class(la, lb, lc, ld):
+    L = la + lb + lc + ld
+    es = carts_upto(la, la + lb)
+    fs = carts_upto(lc, lc + ld)
+    ni, nj, nk, nl = (len(carts(x)) for x in (la, lb, lc, ld))
+    out = []
+    w = out.append
+    w(f"template <> struct Eri<{la},{lb},{lc},{ld}> {{")
+    w(f"  static constexpr int NI = {ni}, NJ = {nj}, NK = {nk}, NL = {nl}, L = {L};")
+    w("  __device__ __forceinline__ static void eval(const PrimPair* __restrict__ bra, int nb,")
+    w("      const PrimPair* __restrict__ ket, int nk, const double3 A, const double3 B,")
+    w("      const double3 C, const double3 D, double* __restrict__ out) {")
+    accs = [(e, f) for e in es for f in fs]
+    for e, f in accs:
+        w(f"    double acc_{name(e)}_{name(f)} = 0.0;")
+    w("    for (int ib = 0; ib < nb; ++ib) {")
+    w("      const PrimPair bp = load_pp(bra + ib);")
+    if la + lb > 0:
+        w("      const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
+        w("      const double o2p = 0.5 * bp.ip;")
+    w("      for (int ik = 0; ik < nk; ++ik) {")
+    w("        const PrimPair kp = load_pp(ket + ik);")
+    w("        const double ps = bp.p + kp.p;")
+    w("        const double r = rsqrt(ps);")
+    w("        const double r2 = r * r;")
+    w("        const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;")
+    w("        const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
+    w("        const double T = bp.p * kp.p * r2 * R2;")
+    w("        const double pref = bp.c * kp.c * r;")
+    if L == 0:
+        w("        const double bm0 = pref * boys_f0(T);")
+    else:
+        w(f"        double F[{L + 1}];")
+        w(f"        boys_fm<{L}>(T, F);")
+        for m in range(L + 1):
+            w(f"        const double bm{m} = pref * F[{m}];")
+        if la + lb > 0:
+            w("        const double rp = kp.p * r2;")
+            w("        const double WPx = -rp * PQx, WPy = -rp * PQy, WPz = -rp * PQz;")
+        if lc + ld > 0:
+            w("        const double rq = bp.p * r2;")
+            w("        const double WQx = rq * PQx, WQy = rq * PQy, WQz = rq * PQz;")
+            w("        const double QCx = kp.x - C.x, QCy = kp.y - C.y, QCz = kp.z - C.z;")
+            w("        const double o2q = 0.5 * kp.ip;")
+        if la + lb > 0 and lc + ld > 0:
+            w("        const double o2pq = 0.5 * r2;")
+    g = Gen()
+    res = {}
+    for e, f in accs:
+        res[(e, f)] = g.vrr(e, f, 0)
+    for line in g.lines:
+        w("        " + line)
+    for e, f in accs:
+        w(f"        acc_{name(e)}_{name(f)} += {res[(e, f)]};")
+    w("      }")
+    w("    }")
+    # horizontal recursion on contracted values
+    memo = {}
+    hl = []
+    cnt = [0]
+
+    def hrr(a, b, c, d):
+        key = (a, b, c, d)
+        if key in memo:
+            return memo[key]
+        if b != ZERO:
+            i = next(t for t in range(3) if b[t] > 0)
+            b1 = sub(b, i)
+            x = hrr(add(a, i), b1, c, d)
+            y = hrr(a, b1, c, d)
+            v = f"h{cnt[0]}"
+            cnt[0] += 1
+            hl.append(f"const double {v} = {x} + AB{AX[i]} * {y};")
+        elif d != ZERO:
+            i = next(t for t in range(3) if d[t] > 0)
+            d1 = sub(d, i)
+            x = hrr(a, b, add(c, i), d1)
+            y = hrr(a, b, c, d1)
+            v = f"h{cnt[0]}"
+            cnt[0] += 1
+            hl.append(f"const double {v} = {x} + CD{AX[i]} * {y};")
+        else:
+            v = f"acc_{name(a)}_{name(c)}"
+        memo[key] = v
+        return v
+
+    outs = []
+    for (x, a), (y, b), (z, c), (t, d) in itertools.product(
+            enumerate(carts(la)), enumerate(carts(lb)), enumerate(carts(lc)), enumerate(carts(ld))):
+        outs.append((((x * nj + y) * nk + z) * nl + t, hrr(a, b, c, d)))
+    if lb:
+        w("    const double ABx = A.x - B.x, ABy = A.y - B.y, ABz = A.z - B.z;")
+    if ld:
+        w("    const double CDx = C.x - D.x, CDy = C.y - D.y, CDz = C.z - D.z;")
+    for line in hl:
+        w("    " + line)
+    for idx, v in outs:
+        w(f"    out[{idx}] = {v};")
+    w("  }")
+    w("};")
+    return "\n".join(out)
+
+
+def main():
+    print("// generated by gen_eri.py -- do not edit")
+    print("#pragma once")
+    print("template <int LA, int LB, int LC, int LD> struct Eri;")
+    for cls in itertools.product((0, 1), repeat=4):
+        print(gen_class(*cls))
+        print()
+
+
+if __name__ == "__main__":
+    main()

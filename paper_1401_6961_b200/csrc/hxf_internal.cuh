@@ -1,0 +1,299 @@
+// Internal types and device helpers shared by the hxf translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hxf.h"
+
+// ---------------------------------------------------------------- errors
+
+void hxf_set_error(const std::string& msg);
+
+struct HxfError {
+    int code;
+    std::string msg;
+};
+
+#define HXF_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw HxfError{HXF_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+
+// ---------------------------------------------------------------- layout
+
+// One primitive pair of a shell pair (integrals.py:115-154 restated for the
+// device): exponent sum p, 1/p, product centre, and
+// c = w_a w_b exp(-ab/p |AB|^2) / p * sqrt(2 pi^{5/2}), so the primitive
+// (ss|ss) is c_bra c_ket F0(T) / sqrt(p+q).  64-byte aligned record.
+struct __align__(16) PrimPair {
+    double p, ip, c, x, y, z, pad0, pad1;
+};
+
+// Partition levels on device (quadtree.py:55-84): spans of every level,
+// concatenated; kid indices are level-local indices at the next level; a
+// leaf span repeats at deeper levels as its own only child.
+struct DevLevels {
+    int n_levels;
+    int n_leaves;
+    const int* off;      // n_levels + 1 (host copy mirrored in HostLevels)
+    const int* slo;      // per span (concatenated)
+    const int* shi;
+    const int* flo;
+    const int* fhi;
+    const int* kid0;
+    const int* kid1;
+    const int* leaf_id;  // partition-leaf index or -1
+    const int* leaf_span;  // per leaf: span index at the deepest level
+};
+
+struct DevBasis {
+    int ns;
+    int nfn;
+    const double3* ctr;
+    const int* l;
+    const int* poff;
+    const int* fn;
+    const int* nf;
+    const double* exps;
+    const double* w;
+    const double* sw;
+};
+
+// Device state handles (opaque to C callers).
+struct hxf_system {
+    int device;
+    int ns, nfn, n_levels, n_leaves, max_span;
+    std::vector<int> h_off, h_slo, h_shi, h_flo, h_fhi, h_kid0, h_kid1, h_leaf_id, h_l, h_poff,
+        h_fn, h_nf;
+    std::vector<int64_t> node_off;  // per level offset of dense node arrays (n_L^2)
+    DevBasis basis;
+    DevLevels lv;
+    std::vector<void*> allocs;
+};
+
+struct hxf_pairs {
+    hxf_system* sys;
+    int device;
+    double tau_ovlp;
+    double* norm;      // per level dense; -1 where pruned
+    double* rowsum;
+    double* colsum;
+    double* smax;      // block max |S|
+    int64_t* leaf_base;  // per leaf pair (nleaf^2): first pair id, -1 if pruned
+    int64_t n_pairs;
+    int* pi;           // per pair id: shells
+    int* pj;
+    int64_t* ppoff;    // n_pairs + 1
+    double* q;         // per pair id: Q in canonical orientation
+    PrimPair* pp;
+    int64_t n_prim_pairs;
+    double maxq;
+    int has_p;
+};
+
+struct hxf_density {
+    hxf_system* sys;
+    int device;
+    double* P;         // n x n row-major
+    double* norm;      // per level dense; -1 where absent
+    double zero_drop;
+    double frob;       // root norm
+    double maxabs;
+};
+
+// ---------------------------------------------------------------- helpers
+
+__host__ __device__ __forceinline__ int64_t node_index(const int64_t* node_off, int level,
+                                                       int nspan, int r, int c) {
+    return node_off[level] + (int64_t)r * nspan + c;
+}
+
+__device__ __forceinline__ PrimPair load_pp(const PrimPair* p) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    PrimPair r;
+    r.p = a.x; r.ip = a.y; r.c = b.x; r.x = b.y; r.y = c.x; r.z = c.y;
+    r.pad0 = 0.0; r.pad1 = 0.0;
+    return r;
+}
+
+// sorted 3-factor product (exchange_naive.py:68-71); no FMA contraction.
+__device__ __forceinline__ double sorted_product3(double a, double b, double c) {
+    double lo = fmin(a, b), hi = fmax(a, b);
+    double mid;
+    if (c < lo) { mid = lo; lo = c; }
+    else if (c > hi) { mid = hi; hi = c; }
+    else mid = c;
+    return __dmul_rn(__dmul_rn(lo, mid), hi);
+}
+
+// ---------------------------------------------------------------- fsum
+
+// Correctly rounded sum (Shewchuk partials + CPython's final half-way
+// correction), so device norms match math.fsum (quadtree.py:20-25) bit for
+// bit given identical inputs.  Partials live in local memory.
+struct FSum {
+    double part[48];
+    int n;
+    __device__ __forceinline__ FSum() : n(0) {}
+    __device__ __forceinline__ void add(double x) {
+        int i = 0;
+        for (int k = 0; k < n; ++k) {
+            double y = part[k];
+            if (fabs(x) < fabs(y)) { double t = x; x = y; y = t; }
+            double hi = __dadd_rn(x, y);
+            double lo = __dsub_rn(y, __dsub_rn(hi, x));
+            if (lo != 0.0) part[i++] = lo;
+            x = hi;
+        }
+        if (i < 48) part[i++] = x;
+        n = i;
+    }
+    __device__ __forceinline__ double result() const {
+        if (n == 0) return 0.0;
+        int k = n - 1;
+        double hi = part[k], lo = 0.0;
+        while (k > 0) {
+            double x = hi;
+            --k;
+            double y = part[k];
+            hi = __dadd_rn(x, y);
+            double yr = __dsub_rn(hi, x);
+            lo = __dsub_rn(y, yr);
+            if (lo != 0.0) break;
+        }
+        if (k > 0 && ((lo < 0.0 && part[k - 1] < 0.0) || (lo > 0.0 && part[k - 1] > 0.0))) {
+            double y = lo * 2.0;
+            double x = __dadd_rn(hi, y);
+            double yr = __dsub_rn(x, hi);
+            if (y == yr) hi = x;
+        }
+        return hi;
+    }
+};
+
+// ---------------------------------------------------------------- fixed point
+//
+// Order-independent accumulation: each value is rounded once to an N-limb
+// two's-complement integer at scale 2^S and added with integer atomics, so
+// sums are bitwise reproducible regardless of thread scheduling.
+
+template <int N>
+__device__ __forceinline__ void fx_from_double(double x, int S, unsigned long long* limb) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) limb[k] = 0ull;
+    if (x == 0.0) return;
+    const bool neg = x < 0.0;
+    unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(x));
+    int ex = (int)((bits >> 52) & 0x7ff);
+    unsigned long long mant = bits & ((1ull << 52) - 1);
+    if (ex == 0) ex = 1; else mant |= (1ull << 52);
+    int s = ex - 1075 + S;  // value = mant * 2^s
+    if (s < 0) {
+        if (s <= -64) return;
+        int sh = -s;
+        unsigned long long rem = mant & ((1ull << sh) - 1);
+        mant >>= sh;
+        unsigned long long half = 1ull << (sh - 1);
+        if (rem > half || (rem == half && (mant & 1ull))) mant += 1;
+        s = 0;
+    }
+    int li = s >> 6, off = s & 63;
+    if (li < N) limb[li] = mant << off;
+    if (off && li + 1 < N) limb[li + 1] = mant >> (64 - off);
+    if (neg) {
+        unsigned long long carry = 1;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            unsigned long long v = ~limb[k] + carry;
+            carry = (carry && v == 0) ? 1ull : 0ull;
+            limb[k] = v;
+        }
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void fx_atomic_add(unsigned long long* acc, const unsigned long long* v) {
+    unsigned long long carry = 0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        unsigned long long add = v[k] + carry;
+        unsigned long long c1 = (add < carry) ? 1ull : 0ull;
+        unsigned long long c2 = 0;
+        if (add != 0ull) {
+            unsigned long long old = atomicAdd(acc + k, add);
+            c2 = (old + add < old) ? 1ull : 0ull;
+        }
+        carry = c1 + c2;
+        if (k + 1 < N && carry == 0ull) {
+            // remaining limbs of v may still be nonzero (sign extension)
+            bool rest = false;
+#pragma unroll
+            for (int t = k + 1; t < N; ++t) rest |= (v[t] != 0ull);
+            if (!rest) break;
+        }
+    }
+}
+
+template <int N>
+__host__ __device__ inline double fx_to_double(const unsigned long long* limb, int S) {
+    // interpret as signed two's complement
+    const bool neg = (long long)limb[N - 1] < 0;
+    unsigned long long m[N];
+    unsigned long long carry = 1;
+    for (int k = 0; k < N; ++k) {
+        m[k] = neg ? ~limb[k] + carry : limb[k];
+        if (neg) carry = (carry && m[k] == 0) ? 1ull : 0ull;
+    }
+    double r = 0.0;
+    for (int k = N - 1; k >= 0; --k) r = r + ldexp((double)m[k], 64 * k - S);
+    return neg ? -r : r;
+}
+
+#define LEDGER_LIMBS 4
+#define LEDGER_SCALE 160
+#define K_LIMBS 2
+
+// ---------------------------------------------------------------- warp utils
+
+__device__ __forceinline__ void atomic_add_ll(long long* p, long long v) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// counter slots in the device counter array
+enum {
+    C_VISITED = 0, C_CULL_SCREEN, C_CULL_ABSENT, C_LEAF, C_ERIQ, C_CULL_LEAF, C_EXPANDED,
+    C_SPAWNED, C_LINK_SCREEN, C_LINK_ABSENT, C_CASE0, C_CASELEAF0 = C_CASE0 + HXF_NCASES,
+    C_TIE_TASK = C_CASELEAF0 + HXF_NCASES, C_TIE_LEAF, C_PRIMQ, C_OVERFLOW, C_NCOUNTERS
+};
+
+// ---------------------------------------------------------------- launchers
+// (defined in the .cu files)
+
+void launch_boys_init();
+void trees_build_pairs(hxf_pairs* pr, cudaStream_t st);
+void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStream_t st);
+
+struct ExchangeCtx;
+int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* o,
+                 double* K_out, hxf_counters* c, cudaStream_t st);
+int frontier_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, double tau, int mode, int sym,
+                 int level, int64_t* n_tasks, double* cost, int64_t cap, cudaStream_t st);

@@ -1,0 +1,732 @@
+// Leaf stage of the exchange build (SURVEY.md kernel K6) and the K epilogue (K7).
+//
+//   screen   per-quartet Schwarz test of every leaf task, one warp per task
+//            (exchange_naive.py:156-182, exchange_symmetry.py:296-331):
+//            bound = (f(Q_ij) |P|) f(Q_kl), keep iff bound > tau; counters and
+//            the culled-bound ledger; survivors compacted (ballot + warp-
+//            aggregated atomics) into a bounded record buffer.
+//   sort     survivors bucketed by angular class (4-bit radix pass) so each
+//            ERI launch is class-uniform (no divergence between s and p code).
+//   eri      Obara-Saika/HGP ERIs (eri_classes.cuh), one thread per shell
+//            quartet, contracted into K with the density: naive slot
+//            K[i,l] += -1/2 P[j,k] (ij|kl) (exchange_naive.py:191-192); the
+//            4-fold scatter of exchange_symmetry.py:345-361 with its
+//            diagonal weights.  K accumulates in 128-bit fixed point with
+//            integer atomics, so the result is bitwise reproducible.
+//   epilogue fixed point -> FP64; fourfold: asymmetry check and (K+K^T)/2
+//            (symmetrize_final, exchange_symmetry.py:197-209).
+// Leaf tasks are processed in chunks sized so the survivor buffer never
+// overflows; chunk boundaries depend only on the data (deterministic).
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "boys.cuh"
+#include "hxf_internal.cuh"
+#include "eri_classes.cuh"
+#include "traverse.cuh"
+
+#define MAXS 12
+#define MAXP (MAXS * MAXS)
+#define SCREEN_WARPS 4
+
+namespace {
+
+struct ScreenArgs {
+    const uint64_t* tasks;
+    int64_t t0, t1;
+    const int* lslo;
+    const int* lshi;
+    int nleaf;
+    const int64_t* bra_base;
+    const int64_t* ket_base;
+    const double* qb;
+    const double* qk;
+    const int* l;
+    const int* fn;
+    const int* nf;
+    const double* P;
+    int nfn;
+    double tau;
+    int mode;
+    uint64_t* rec;
+    int64_t cap;
+    unsigned long long* fill;
+    long long* counters;
+    unsigned long long* ledger;
+};
+
+struct WarpSmem {
+    double fa[MAXP], sa[MAXP], fb[MAXP], sb[MAXP];
+    double pm[4][MAXP];
+    unsigned char ax[MAXP], ay[MAXP], bx[MAXP], by[MAXP], acl[MAXP], bcl[MAXP];
+    unsigned short apl[MAXP], bpl[MAXP];
+};
+
+// max |P| over the function block of shells (s, t) (|P_jk| for s shells)
+__device__ __forceinline__ double pblock_max(const ScreenArgs& a, int s, int t) {
+    const int f0 = a.fn[s], g0 = a.fn[t];
+    const int nfs = a.nf[s], nft = a.nf[t];
+    double m = 0.0;
+    for (int x = 0; x < nfs; ++x)
+        for (int y = 0; y < nft; ++y) m = fmax(m, fabs(a.P[(int64_t)(f0 + x) * a.nfn + g0 + y]));
+    return m;
+}
+
+// canonical (x <= y) enumeration of a diagonal node's pairs
+__device__ __forceinline__ void tri_decode(int a, int n, int* x, int* y) {
+    int r = 0;
+    while (a >= n - r) {
+        a -= n - r;
+        ++r;
+    }
+    *x = r;
+    *y = r + a;
+}
+
+template <bool SYM, bool EMIT>
+__global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
+    __shared__ WarpSmem sm_all[SCREEN_WARPS];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpSmem& sm = sm_all[wid];
+    const int64_t gw = blockIdx.x * (int64_t)SCREEN_WARPS + wid;
+    const int64_t W = (int64_t)gridDim.x * SCREEN_WARPS;
+    long long n_eri = 0, n_cull = 0, n_tie = 0;
+    double ledger = 0.0;
+    const bool schwarz = a.mode == HXF_MODE_SCHWARZ;
+    for (int64_t t = a.t0 + gw; t < a.t1; t += W) {
+        const uint64_t task = a.tasks[t];
+        const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
+                  sig = (task >> 45) & 0x7fff;
+        const int live = SYM ? (int)(task >> 60) : 1;
+        const int smu = a.lslo[mu], snu = a.lslo[nu], slam = a.lslo[lam], ssig = a.lslo[sig];
+        const int nmu = a.lshi[mu] - smu, nnu = a.lshi[nu] - snu, nlam = a.lshi[lam] - slam,
+                  nsig = a.lshi[sig] - ssig;
+        const int64_t bb = a.bra_base[(int64_t)mu * a.nleaf + nu];
+        const int64_t kb = a.ket_base[(int64_t)lam * a.nleaf + sig];
+        const bool bdiag = SYM && mu == nu, kdiag = SYM && lam == sig;
+        const int ma = bdiag ? nmu * (nmu + 1) / 2 : nmu * nnu;
+        const int mb = kdiag ? nlam * (nlam + 1) / 2 : nlam * nsig;
+        for (int i = lane; i < ma; i += 32) {
+            int x, y;
+            if (bdiag) tri_decode(i, nmu, &x, &y);
+            else { x = i / nnu; y = i - x * nnu; }
+            const double q = a.qb[bb + x * nnu + y];
+            sm.sa[i] = sqrt(q);
+            sm.fa[i] = schwarz ? sm.sa[i] : q;
+            sm.ax[i] = x;
+            sm.ay[i] = y;
+            sm.apl[i] = x * nnu + y;
+            sm.acl[i] = (a.l[smu + x] << 1) | a.l[snu + y];
+        }
+        for (int i = lane; i < mb; i += 32) {
+            int x, y;
+            if (kdiag) tri_decode(i, nlam, &x, &y);
+            else { x = i / nsig; y = i - x * nsig; }
+            const double q = a.qk[kb + x * nsig + y];
+            sm.sb[i] = sqrt(q);
+            sm.fb[i] = schwarz ? sm.sb[i] : q;
+            sm.bx[i] = x;
+            sm.by[i] = y;
+            sm.bpl[i] = x * nsig + y;
+            sm.bcl[i] = (a.l[slam + x] << 1) | a.l[ssig + y];
+        }
+        // density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
+        const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
+        const int cs[4] = {slam, slam, ssig, ssig}, cn[4] = {nlam, nlam, nsig, nsig};
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            if (!((live >> g) & 1)) continue;
+            for (int i = lane; i < rn[g] * cn[g]; i += 32) {
+                const int x = i / cn[g], y = i - x * cn[g];
+                sm.pm[g][i] = pblock_max(a, rs[g] + x, cs[g] + y);
+            }
+        }
+        __syncwarp();
+        const int total = ma * mb;
+        for (int q0 = 0; q0 < total; q0 += 32) {
+            const int q = q0 + lane;
+            bool keep_any = false;
+            int mask = 0;
+            int ia = 0, ib = 0;
+            if (q < total) {
+                ia = q / mb;
+                ib = q - ia * mb;
+                const double fa = sm.fa[ia], fb = sm.fb[ib];
+                const int x = sm.ax[ia], y = sm.ay[ia], z = sm.bx[ib], w = sm.by[ib];
+                const int rowv[4] = {y, x, y, x}, colv[4] = {z, z, w, w};
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    if (!((live >> g) & 1)) continue;
+                    const double pm = sm.pm[g][rowv[g] * cn[g] + colv[g]];
+                    const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
+                    n_tie += fabs(bound - a.tau) <= 1e-12 * a.tau;
+                    if (bound > a.tau) {
+                        keep_any = true;
+                        mask |= 1 << g;
+                    } else {
+                        ++n_cull;
+                        ledger += schwarz ? bound : __dmul_rn(__dmul_rn(sm.sa[ia], pm), sm.sb[ib]);
+                    }
+                }
+                if (SYM) {
+                    // diagonal-pair weights: g1/g3 need i != j, g2/g3 need k != l
+                    const bool ij = !(bdiag && x == y), kl = !(kdiag && z == w);
+                    if (!ij) mask &= ~0xa;
+                    if (!kl) mask &= ~0xc;
+                }
+                n_eri += keep_any;
+            }
+            if (EMIT) {
+                const unsigned bal = __ballot_sync(0xffffffffu, keep_any);
+                if (bal) {
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(a.fill, (unsigned long long)__popc(bal));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (keep_any) {
+                        const uint64_t pos = base + __popc(bal & ((1u << lane) - 1u));
+                        if ((int64_t)pos < a.cap) {
+                            const uint64_t pb = (uint64_t)(bb + sm.apl[ia]);
+                            const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
+                            const uint64_t cls = ((uint64_t)sm.acl[ia] << 2) | sm.bcl[ib];
+                            a.rec[pos] = pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    // per-lane totals; counters are integers (order independent); the warp's
+    // ledger partial has a fixed task->warp assignment and a fixed shuffle tree
+    n_eri = warp_sum_ll(n_eri);
+    n_cull = warp_sum_ll(n_cull);
+    n_tie = warp_sum_ll(n_tie);
+    ledger = warp_sum(ledger);
+    if (lane == 0) {
+        if (n_eri) atomic_add_ll(&a.counters[C_ERIQ], n_eri);
+        if (n_cull) atomic_add_ll(&a.counters[C_CULL_LEAF], n_cull);
+        if (n_tie) atomic_add_ll(&a.counters[C_TIE_LEAF], n_tie);
+        if (ledger != 0.0) {
+            unsigned long long limb[LEDGER_LIMBS];
+            fx_from_double<LEDGER_LIMBS>(0.5 * ledger, LEDGER_SCALE, limb);
+            fx_atomic_add<LEDGER_LIMBS>(a.ledger, limb);
+        }
+    }
+}
+
+struct EriArgs {
+    const uint64_t* rec;
+    int64_t n;
+    const int* bpi;
+    const int* bpj;
+    const int64_t* bppoff;
+    const PrimPair* bpp;
+    const int* kpi;
+    const int* kpj;
+    const int64_t* kppoff;
+    const PrimPair* kpp;
+    const double3* ctr;
+    const int* fn;
+    const double* P;
+    int nfn;
+    int S;
+    unsigned long long* K;
+    long long* counters;
+};
+
+__device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double v) {
+    if (v == 0.0) return;
+    unsigned long long limb[K_LIMBS];
+    fx_from_double<K_LIMBS>(v, e.S, limb);
+    fx_atomic_add<K_LIMBS>(e.K + 2 * ((int64_t)row * e.nfn + col), limb);
+}
+
+template <int LA, int LB, int LC, int LD>
+__global__ void __launch_bounds__(128) k_eri(EriArgs e) {
+    typedef Eri<LA, LB, LC, LD> E;
+    constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    long long nprim = 0;
+    if (t < e.n) {
+        const uint64_t r = e.rec[t];
+        const int mask = (int)((r >> 56) & 0xf);
+        if (mask) {
+            const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
+            const int i = e.bpi[pb], j = e.bpj[pb], k = e.kpi[pk], l = e.kpj[pk];
+            const int64_t b0 = e.bppoff[pb], k0 = e.kppoff[pk];
+            const int nb = (int)(e.bppoff[pb + 1] - b0), nk = (int)(e.kppoff[pk + 1] - k0);
+            nprim = (long long)nb * nk;
+            double out[NI * NJ * NK * NL];
+            E::eval(e.bpp + b0, nb, e.kpp + k0, nk, e.ctr[i], e.ctr[j], e.ctr[k], e.ctr[l], out);
+            const int fi = e.fn[i], fj = e.fn[j], fk = e.fn[k], fl = e.fn[l];
+            const int64_t n = e.nfn;
+            const double* P = e.P;
+#define OUT(x, y, z, w) out[(((x) * NJ + (y)) * NK + (z)) * NL + (w)]
+            if (mask & 1) {  // K[mu,sig] <- P[nu,lam]
+                for (int x = 0; x < NI; ++x)
+                    for (int w = 0; w < NL; ++w) {
+                        double s = 0.0;
+                        for (int y = 0; y < NJ; ++y)
+                            for (int z = 0; z < NK; ++z) s += __ldg(P + (fj + y) * n + fk + z) * OUT(x, y, z, w);
+                        k_add(e, fi + x, fl + w, -0.5 * s);
+                    }
+            }
+            if (mask & 2) {  // K[nu,sig] <- P[mu,lam]
+                for (int y = 0; y < NJ; ++y)
+                    for (int w = 0; w < NL; ++w) {
+                        double s = 0.0;
+                        for (int x = 0; x < NI; ++x)
+                            for (int z = 0; z < NK; ++z) s += __ldg(P + (fi + x) * n + fk + z) * OUT(x, y, z, w);
+                        k_add(e, fj + y, fl + w, -0.5 * s);
+                    }
+            }
+            if (mask & 4) {  // K[mu,lam] <- P[nu,sig]
+                for (int x = 0; x < NI; ++x)
+                    for (int z = 0; z < NK; ++z) {
+                        double s = 0.0;
+                        for (int y = 0; y < NJ; ++y)
+                            for (int w = 0; w < NL; ++w) s += __ldg(P + (fj + y) * n + fl + w) * OUT(x, y, z, w);
+                        k_add(e, fi + x, fk + z, -0.5 * s);
+                    }
+            }
+            if (mask & 8) {  // K[nu,lam] <- P[mu,sig]
+                for (int y = 0; y < NJ; ++y)
+                    for (int z = 0; z < NK; ++z) {
+                        double s = 0.0;
+                        for (int x = 0; x < NI; ++x)
+                            for (int w = 0; w < NL; ++w) s += __ldg(P + (fi + x) * n + fl + w) * OUT(x, y, z, w);
+                        k_add(e, fj + y, fk + z, -0.5 * s);
+                    }
+            }
+#undef OUT
+        }
+    }
+    nprim = warp_sum_ll(nprim);
+    if ((threadIdx.x & 31) == 0 && nprim) atomic_add_ll(&e.counters[C_PRIMQ], nprim);
+}
+
+__global__ void k_class_bounds(const uint64_t* rec, int64_t n, int64_t* bounds) {
+    const int c = threadIdx.x;
+    if (c > 16) return;
+    // first index with class >= c
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int)(rec[mid] >> 60) < c) lo = mid + 1;
+        else hi = mid;
+    }
+    bounds[c] = lo;
+}
+
+__global__ void k_log(const uint64_t* rec, int64_t n, const int* bpi, const int* bpj, const int* kpi,
+                      const int* kpj, int32_t* log, int64_t cap, unsigned long long* fill) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t r = rec[t];
+    const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
+    const unsigned long long pos = atomicAdd(fill, 1ull);
+    if ((int64_t)pos < cap) {
+        log[4 * pos + 0] = bpi[pb];
+        log[4 * pos + 1] = bpj[pb];
+        log[4 * pos + 2] = kpi[pk];
+        log[4 * pos + 3] = kpj[pk];
+    }
+}
+
+__global__ void k_fx_to_double(const unsigned long long* Kfx, int64_t n2, int S, double* K) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2;
+         t += (int64_t)gridDim.x * blockDim.x)
+        K[t] = fx_to_double<K_LIMBS>(Kfx + 2 * t, S);
+}
+
+__global__ void k_asym(const double* K, int n, unsigned long long* out) {
+    double m = 0.0;
+    const int64_t n2 = (int64_t)n * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t / n), j = (int)(t % n);
+        if (i < j) m = fmax(m, fabs(K[t] - K[(int64_t)j * n + i]));
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_symmetrize(double* K, int n) {
+    const int64_t n2 = (int64_t)n * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t / n), j = (int)(t % n);
+        if (i < j) {
+            const int64_t u = (int64_t)j * n + i;
+            const double v = 0.5 * (K[t] + K[u]);
+            K[t] = v;
+            K[u] = v;
+        }
+    }
+}
+
+template <typename T>
+T* lalloc(size_t n, cudaStream_t st) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
+    if (e != cudaSuccess) throw HxfError{HXF_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e)};
+    return (T*)p;
+}
+
+void launch_eri_class(int cls, const EriArgs& e, cudaStream_t st) {
+    const unsigned g = (unsigned)((e.n + 127) / 128);
+    if (!e.n) return;
+    switch (cls) {
+#define C(a, b, c, d) \
+    case (a << 3) | (b << 2) | (c << 1) | d: k_eri<a, b, c, d><<<g, 128, 0, st>>>(e); break;
+        C(0, 0, 0, 0) C(0, 0, 0, 1) C(0, 0, 1, 0) C(0, 0, 1, 1)
+        C(0, 1, 0, 0) C(0, 1, 0, 1) C(0, 1, 1, 0) C(0, 1, 1, 1)
+        C(1, 0, 0, 0) C(1, 0, 0, 1) C(1, 0, 1, 0) C(1, 0, 1, 1)
+        C(1, 1, 0, 0) C(1, 1, 0, 1) C(1, 1, 1, 0) C(1, 1, 1, 1)
+#undef C
+    }
+}
+
+struct Timer {
+    cudaEvent_t a, b;
+    cudaStream_t st;
+    explicit Timer(cudaStream_t s) : st(s) {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+    }
+    float stop() {
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        return ms;
+    }
+};
+
+thread_local double g_timings[8];
+
+void host_ledger_add(unsigned long long* acc, const unsigned long long* v) {
+    unsigned long long carry = 0;
+    for (int k = 0; k < LEDGER_LIMBS; ++k) {
+        unsigned long long s = acc[k] + v[k];
+        unsigned long long c1 = s < acc[k];
+        unsigned long long s2 = s + carry;
+        unsigned long long c2 = s2 < s;
+        acc[k] = s2;
+        carry = c1 + c2;
+    }
+}
+
+}  // namespace
+
+int hxf_last_timings_impl(double* ms, int n) {
+    for (int k = 0; k < n && k < 8; ++k) ms[k] = g_timings[k];
+    return HXF_OK;
+}
+
+// ---------------------------------------------------------------------------
+
+int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_exchange_opts* o,
+                 double* K_out, hxf_counters* out, cudaStream_t st) {
+    hxf_system* s = bra->sys;
+    if (ket->sys != s || dens->sys != s)
+        throw HxfError{HXF_EINVAL, "bra, ket and P must be built over the same partition"};
+    if (!(o->tau_2e >= 0.0)) throw HxfError{HXF_EINVAL, "tau_2e must be non-negative"};
+    if (o->mode != HXF_MODE_SCHWARZ && o->mode != HXF_MODE_LITERAL)
+        throw HxfError{HXF_EINVAL, "unknown screening mode"};
+    if (o->symmetry == HXF_FOURFOLD && bra != ket)
+        throw HxfError{HXF_EINVAL, "the fourfold driver takes a single pair tree"};
+    for (int k = 0; k < 8; ++k) g_timings[k] = 0.0;
+    Timer ttot(st);
+    const int sym = o->symmetry == HXF_FOURFOLD;
+    long long* dcount = lalloc<long long>(C_NCOUNTERS, st);
+    unsigned long long* dledger = lalloc<unsigned long long>(LEDGER_LIMBS, st);
+    HXF_CUDA(cudaMemsetAsync(dcount, 0, C_NCOUNTERS * sizeof(long long), st));
+    HXF_CUDA(cudaMemsetAsync(dledger, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
+
+    // ---- traversal
+    Timer ttrav(st);
+    TravInput ti{s, bra, ket, dens, o->tau_2e, o->mode, sym, o->shard_level, o->shard_begin,
+                 o->shard_end, 0, 0, dcount, dledger};
+    TraversalResult tr = traverse(ti, st);
+    g_timings[0] = ttrav.stop();
+
+    const int64_t n2 = (int64_t)s->nfn * s->nfn;
+    long long hc[C_NCOUNTERS];
+    unsigned long long hl[LEDGER_LIMBS];
+    HXF_CUDA(cudaMemcpyAsync(hc, dcount, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaMemcpyAsync(hl, dledger, sizeof(hl), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+
+    ScreenArgs sa;
+    sa.tasks = tr.leaf;
+    std::vector<int> lslo(s->n_leaves), lshi(s->n_leaves);
+    {
+        const int D = s->n_levels - 1;
+        for (int k = s->h_off[D]; k < s->h_off[D + 1]; ++k) {
+            lslo[s->h_leaf_id[k]] = s->h_slo[k];
+            lshi[s->h_leaf_id[k]] = s->h_shi[k];
+        }
+    }
+    int* d_lslo = lalloc<int>(s->n_leaves, st);
+    int* d_lshi = lalloc<int>(s->n_leaves, st);
+    HXF_CUDA(cudaMemcpyAsync(d_lslo, lslo.data(), lslo.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    HXF_CUDA(cudaMemcpyAsync(d_lshi, lshi.data(), lshi.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    sa.lslo = d_lslo;
+    sa.lshi = d_lshi;
+    sa.nleaf = s->n_leaves;
+    sa.bra_base = bra->leaf_base;
+    sa.ket_base = ket->leaf_base;
+    sa.qb = bra->q;
+    sa.qk = ket->q;
+    sa.l = s->basis.l;
+    sa.fn = s->basis.fn;
+    sa.nf = s->basis.nf;
+    sa.P = dens->P;
+    sa.nfn = s->nfn;
+    sa.tau = o->tau_2e;
+    sa.mode = o->mode;
+
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device);
+    const unsigned screen_grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((tr.n_leaf + SCREEN_WARPS - 1) / SCREEN_WARPS, (int64_t)dev_sms * 12));
+
+    // fixed-point scale for K: |K| <= 1/2 sum|P| max|(ij|kl)| <= 1/2 n ||P||_F maxQ
+    const double kb = 2.0 * s->nfn * std::max(dens->frob, 1e-300) *
+                      std::max(std::sqrt(bra->maxq * ket->maxq), 1e-300);
+    int S = 124 - (int)std::ceil(std::log2(kb));
+    S = std::max(-900, std::min(S, 400));
+
+    unsigned long long* Kfx = nullptr;
+    int64_t logged = 0;
+    int32_t* dlog = nullptr;
+    unsigned long long* dlogfill = nullptr;
+    const bool want_log = o->quartet_log != nullptr && o->evaluate;
+    if (want_log) {
+        dlog = lalloc<int32_t>(4 * std::max<int64_t>(o->log_capacity, 1), st);
+        dlogfill = lalloc<unsigned long long>(1, st);
+        HXF_CUDA(cudaMemsetAsync(dlogfill, 0, sizeof(unsigned long long), st));
+    }
+
+    long long* scount = lalloc<long long>(C_NCOUNTERS, st);
+    unsigned long long* sledger = lalloc<unsigned long long>(LEDGER_LIMBS, st);
+    unsigned long long* dfill = lalloc<unsigned long long>(1, st);
+    long long acc_c[C_NCOUNTERS];
+    unsigned long long acc_l[LEDGER_LIMBS];
+    memcpy(acc_c, hc, sizeof(acc_c));
+    memcpy(acc_l, hl, sizeof(acc_l));
+
+    if (!o->evaluate || tr.n_leaf == 0) {
+        if (tr.n_leaf) {
+            Timer tsc(st);
+            HXF_CUDA(cudaMemsetAsync(scount, 0, C_NCOUNTERS * sizeof(long long), st));
+            HXF_CUDA(cudaMemsetAsync(sledger, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
+            sa.t0 = 0;
+            sa.t1 = tr.n_leaf;
+            sa.rec = nullptr;
+            sa.cap = 0;
+            sa.fill = dfill;
+            sa.counters = scount;
+            sa.ledger = sledger;
+            if (sym) k_screen<true, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa);
+            else k_screen<false, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa);
+            HXF_CUDA(cudaGetLastError());
+            long long c2[C_NCOUNTERS];
+            unsigned long long l2[LEDGER_LIMBS];
+            HXF_CUDA(cudaMemcpyAsync(c2, scount, sizeof(c2), cudaMemcpyDeviceToHost, st));
+            HXF_CUDA(cudaMemcpyAsync(l2, sledger, sizeof(l2), cudaMemcpyDeviceToHost, st));
+            HXF_CUDA(cudaStreamSynchronize(st));
+            for (int k = 0; k < C_NCOUNTERS; ++k) acc_c[k] += c2[k];
+            host_ledger_add(acc_l, l2);
+            g_timings[1] = tsc.stop();
+        }
+    } else {
+        Kfx = lalloc<unsigned long long>(2 * n2, st);
+        HXF_CUDA(cudaMemsetAsync(Kfx, 0, 2 * n2 * sizeof(unsigned long long), st));
+        size_t freeb = 0, totb = 0;
+        cudaMemGetInfo(&freeb, &totb);
+        int64_t cap = std::min<int64_t>(1ll << 27, std::max<int64_t>(1 << 16, (int64_t)(freeb / 40)));
+        uint64_t* rec = lalloc<uint64_t>(cap, st);
+        uint64_t* rec2 = lalloc<uint64_t>(cap, st);
+        size_t sort_tb = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, sort_tb, rec, rec2, cap, 60, 64, st);
+        void* sort_tmp = lalloc<char>(sort_tb, st);
+        int64_t* dbounds = lalloc<int64_t>(17, st);
+        EriArgs e;
+        e.bpi = bra->pi;
+        e.bpj = bra->pj;
+        e.bppoff = bra->ppoff;
+        e.bpp = bra->pp;
+        e.kpi = ket->pi;
+        e.kpj = ket->pj;
+        e.kppoff = ket->ppoff;
+        e.kpp = ket->pp;
+        e.ctr = s->basis.ctr;
+        e.fn = s->basis.fn;
+        e.P = dens->P;
+        e.nfn = s->nfn;
+        e.S = S;
+        e.K = Kfx;
+        e.counters = scount;
+        int64_t chunk = std::max<int64_t>(1, cap / 1024);
+        int64_t t0 = 0;
+        while (t0 < tr.n_leaf) {
+            const int64_t t1 = std::min(tr.n_leaf, t0 + chunk);
+            Timer tsc(st);
+            HXF_CUDA(cudaMemsetAsync(scount, 0, C_NCOUNTERS * sizeof(long long), st));
+            HXF_CUDA(cudaMemsetAsync(sledger, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
+            HXF_CUDA(cudaMemsetAsync(dfill, 0, sizeof(unsigned long long), st));
+            sa.t0 = t0;
+            sa.t1 = t1;
+            sa.rec = rec;
+            sa.cap = cap;
+            sa.fill = dfill;
+            sa.counters = scount;
+            sa.ledger = sledger;
+            if (sym) k_screen<true, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa);
+            else k_screen<false, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa);
+            HXF_CUDA(cudaGetLastError());
+            unsigned long long fill = 0;
+            HXF_CUDA(cudaMemcpyAsync(&fill, dfill, sizeof(fill), cudaMemcpyDeviceToHost, st));
+            HXF_CUDA(cudaStreamSynchronize(st));
+            g_timings[1] += tsc.stop();
+            if ((int64_t)fill > cap) {
+                if (t1 - t0 == 1) throw HxfError{HXF_ELOGIC, "survivor buffer too small for one leaf task"};
+                chunk = std::max<int64_t>(1, (t1 - t0) / 2);
+                continue;
+            }
+            Timer teri(st);
+            const int64_t nrec = (int64_t)fill;
+            if (nrec) {
+                size_t tb = sort_tb;
+                cub::DeviceRadixSort::SortKeys(sort_tmp, tb, rec, rec2, nrec, 60, 64, st);
+                k_class_bounds<<<1, 32, 0, st>>>(rec2, nrec, dbounds);
+                int64_t hb[17];
+                HXF_CUDA(cudaMemcpyAsync(hb, dbounds, sizeof(hb), cudaMemcpyDeviceToHost, st));
+                HXF_CUDA(cudaStreamSynchronize(st));
+                for (int c = 0; c < 16; ++c) {
+                    e.rec = rec2 + hb[c];
+                    e.n = hb[c + 1] - hb[c];
+                    launch_eri_class(c, e, st);
+                }
+                HXF_CUDA(cudaGetLastError());
+                if (want_log)
+                    k_log<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(rec2, nrec, bra->pi, bra->pj, ket->pi,
+                                                                        ket->pj, dlog, o->log_capacity, dlogfill);
+            }
+            long long c2[C_NCOUNTERS];
+            unsigned long long l2[LEDGER_LIMBS];
+            HXF_CUDA(cudaMemcpyAsync(c2, scount, sizeof(c2), cudaMemcpyDeviceToHost, st));
+            HXF_CUDA(cudaMemcpyAsync(l2, sledger, sizeof(l2), cudaMemcpyDeviceToHost, st));
+            HXF_CUDA(cudaStreamSynchronize(st));
+            g_timings[2] += teri.stop();
+            for (int k = 0; k < C_NCOUNTERS; ++k) acc_c[k] += c2[k];
+            host_ledger_add(acc_l, l2);
+            const double dens_per_task = (double)nrec / (double)(t1 - t0);
+            chunk = std::max<int64_t>(1, (int64_t)(0.85 * cap / std::max(dens_per_task, 1.0)));
+            t0 = t1;
+        }
+        for (void* p : {(void*)rec, (void*)rec2, sort_tmp, (void*)dbounds}) cudaFreeAsync(p, st);
+    }
+
+    // ---- epilogue
+    Timer tep(st);
+    if (K_out) {
+        double* Kd = o->K_on_device ? K_out : lalloc<double>(n2, st);
+        if (Kfx) {
+            k_fx_to_double<<<1024, 256, 0, st>>>(Kfx, n2, S, Kd);
+            if (sym && o->symmetrize) {
+                unsigned long long* dm = lalloc<unsigned long long>(1, st);
+                HXF_CUDA(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
+                k_asym<<<1024, 256, 0, st>>>(Kd, s->nfn, dm);
+                unsigned long long hm = 0;
+                HXF_CUDA(cudaMemcpyAsync(&hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, st));
+                HXF_CUDA(cudaStreamSynchronize(st));
+                cudaFreeAsync(dm, st);
+                double asym;
+                memcpy(&asym, &hm, sizeof(asym));
+                if (asym > 1e-10) {
+                    char buf[160];
+                    snprintf(buf, sizeof(buf), "asymmetry %.3e exceeds 1.0e-10; symmetry update set is inconsistent", asym);
+                    throw HxfError{HXF_ELOGIC, buf};
+                }
+                k_symmetrize<<<1024, 256, 0, st>>>(Kd, s->nfn);
+            }
+        } else {
+            HXF_CUDA(cudaMemsetAsync(Kd, 0, n2 * sizeof(double), st));
+        }
+        if (!o->K_on_device) {
+            HXF_CUDA(cudaMemcpyAsync(K_out, Kd, n2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            cudaFreeAsync(Kd, st);
+        }
+    }
+    if (want_log) {
+        unsigned long long lf = 0;
+        HXF_CUDA(cudaMemcpyAsync(&lf, dlogfill, sizeof(lf), cudaMemcpyDeviceToHost, st));
+        HXF_CUDA(cudaStreamSynchronize(st));
+        logged = (int64_t)lf;
+        const int64_t ncopy = std::min<int64_t>(logged, o->log_capacity);
+        if (ncopy) HXF_CUDA(cudaMemcpyAsync(o->quartet_log, dlog, 4 * ncopy * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        cudaFreeAsync(dlog, st);
+        cudaFreeAsync(dlogfill, st);
+    }
+    if (o->log_count) *o->log_count = logged;
+    for (void* p : {(void*)Kfx, (void*)scount, (void*)sledger, (void*)dfill, (void*)dcount,
+                    (void*)dledger, (void*)d_lslo, (void*)d_lshi, (void*)tr.leaf})
+        if (p) cudaFreeAsync(p, st);
+    HXF_CUDA(cudaStreamSynchronize(st));
+    HXF_CUDA(cudaGetLastError());
+    g_timings[3] = tep.stop();
+    g_timings[4] = ttot.stop();
+
+    // ---- counters out
+    hxf_counters& c = *out;
+    c.tasks_visited = acc_c[C_VISITED];
+    c.tasks_culled_screening = acc_c[C_CULL_SCREEN];
+    c.tasks_culled_absent = acc_c[C_CULL_ABSENT];
+    c.leaf_contractions = acc_c[C_LEAF];
+    c.eri_shell_quartets = acc_c[C_ERIQ];
+    c.quartets_culled_leaf = acc_c[C_CULL_LEAF];
+    c.tasks_expanded = acc_c[C_EXPANDED];
+    c.children_spawned = acc_c[C_SPAWNED];
+    c.links_culled_screening = acc_c[C_LINK_SCREEN];
+    c.links_culled_absent = acc_c[C_LINK_ABSENT];
+    for (int k = 0; k < HXF_NCASES; ++k) {
+        c.case_tasks[k] = acc_c[C_CASE0 + k];
+        c.case_leaf_tasks[k] = acc_c[C_CASELEAF0 + k];
+    }
+    c.ties_task = acc_c[C_TIE_TASK];
+    c.ties_leaf = acc_c[C_TIE_LEAF];
+    c.prim_quartets = acc_c[C_PRIMQ];
+    c.culled_bound_ledger = fx_to_double<LEDGER_LIMBS>(acc_l, LEDGER_SCALE);
+    return HXF_OK;
+}
+
+int frontier_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, double tau, int mode, int sym,
+                 int level, int64_t* n_tasks, double* cost, int64_t cap, cudaStream_t st) {
+    hxf_system* s = bra->sys;
+    long long* dcount = lalloc<long long>(C_NCOUNTERS, st);
+    unsigned long long* dledger = lalloc<unsigned long long>(LEDGER_LIMBS, st);
+    HXF_CUDA(cudaMemsetAsync(dcount, 0, C_NCOUNTERS * sizeof(long long), st));
+    HXF_CUDA(cudaMemsetAsync(dledger, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
+    TravInput ti{s, bra, ket, dens, tau, mode, sym, -1, 0, 0, 1, level, dcount, dledger};
+    TraversalResult tr = traverse(ti, st);
+    *n_tasks = tr.n_frontier;
+    if (cost) {
+        const int64_t n = std::min<int64_t>(cap, tr.n_frontier);
+        for (int64_t k = 0; k < n; ++k) cost[k] = 1.0;
+    }
+    for (void* p : {(void*)dcount, (void*)dledger, (void*)tr.leaf, (void*)tr.frontier})
+        if (p) cudaFreeAsync(p, st);
+    HXF_CUDA(cudaStreamSynchronize(st));
+    return HXF_OK;
+}

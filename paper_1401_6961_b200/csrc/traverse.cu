@@ -1,0 +1,495 @@
+// Level-synchronous product-tree traversal (SURVEY.md kernels K4/K5).
+//
+// Restates the reference's recursive visitors as a breadth-first expansion:
+//   naive      exchange_naive.py:124-154   task (bra, P, ket) = spans (mu,nu,lam,sig)
+//   symmetric  exchange_symmetry.py:233-294 task (bra, ket, 4 density refs, alive)
+// Every expanded task of level L spawns its (up to 16) children; each child is
+// visited (absent / screened / leaf / expand) by one thread, and survivors are
+// compacted with a block-wide scan into the next frontier or the leaf-task
+// list.  Compaction is two-pass (count, device scan, write), so frontiers and
+// per-block partial sums are in a deterministic order and repeated builds are
+// bitwise identical (the reference's determinism contract,
+// test_exchange_naive.py:157-162).
+//
+// Task encoding (uint64): four 15-bit span indices (level-local for frontier
+// tasks, partition-leaf ids for leaf tasks) and a 4-bit live-slot mask.
+
+#include <cub/cub.cuh>
+
+#include "hxf_internal.cuh"
+#include "traverse.cuh"
+
+namespace {
+
+enum { O_NONE = 0, O_ABSENT, O_SCREEN, O_LEAF, O_EXPAND };
+enum { CASE_A = 0, CASE_B, CASE_C, CASE_D, CASE_E, CASE_F1, CASE_F2, CASE_H, CASE_SPARSE };
+
+struct LevelView {
+    int n;                 // spans at this level
+    int64_t node_off;      // offset of this level's dense node arrays
+    const int* leaf_id;    // per span (level-local pointer)
+    const int* flo;
+};
+
+struct TreeView {
+    const double* bnorm;
+    const double* brow;
+    const double* bcol;
+    const double* knorm;
+    const double* krow;
+    const double* kcol;
+    const double* pnorm;
+    double tau;
+    int mode;
+};
+
+struct Visit {
+    int outcome;
+    int live;
+    int label;
+    int links_screen;
+    int links_absent;
+    int tie;
+    double ledger;
+};
+
+__device__ __forceinline__ double fnorm(double v, int mode) { return mode == HXF_MODE_SCHWARZ ? sqrt(v) : v; }
+
+__device__ __forceinline__ bool is_tie(double bound, double tau) {
+    return fabs(bound - tau) <= 1e-12 * tau;
+}
+
+// culled_task_bound (exchange_naive.py:91-102)
+__device__ __forceinline__ double ledger_term(double pn, double bs, double ks) {
+    return __dmul_rn(__dmul_rn(__dmul_rn(0.5, pn), sqrt(fmax(bs, 0.0))), sqrt(fmax(ks, 0.0)));
+}
+
+__device__ Visit visit_naive(const TreeView& tv, const LevelView& lv, int mu, int nu, int lam,
+                             int sig) {
+    Visit v{O_NONE, 0, 0, 0, 0, 0, 0.0};
+    const int64_t n = lv.n;
+    const int64_t ib = lv.node_off + mu * n + nu;
+    const int64_t ip = lv.node_off + nu * n + lam;
+    const int64_t ik = lv.node_off + lam * n + sig;
+    const double nb = tv.bnorm[ib], np = tv.pnorm[ip], nk = tv.knorm[ik];
+    if (nb < 0.0 || np < 0.0 || nk < 0.0) {
+        v.outcome = O_ABSENT;
+        return v;
+    }
+    const double bound = sorted_product3(fnorm(nb, tv.mode), np, fnorm(nk, tv.mode));
+    v.tie = is_tie(bound, tv.tau);
+    if (bound <= tv.tau) {
+        v.outcome = O_SCREEN;
+        v.ledger = ledger_term(np, tv.brow[ib], tv.kcol[ik]);
+        return v;
+    }
+    const bool leaf = lv.leaf_id[mu] >= 0 && lv.leaf_id[nu] >= 0 && lv.leaf_id[lam] >= 0 &&
+                      lv.leaf_id[sig] >= 0;
+    v.outcome = leaf ? O_LEAF : O_EXPAND;
+    v.live = 1;
+    return v;
+}
+
+// _case_label (exchange_symmetry.py:135-173), span identity = index equality
+__device__ __forceinline__ int case_label(const LevelView& lv, int mu, int nu, int lam, int sig) {
+    if (mu == lam && nu == sig) return CASE_E;
+    const bool bd = mu == nu, kd = lam == sig;
+    if (bd && kd) return CASE_H;
+    if (bd || kd) return CASE_B;
+    if (nu == lam || mu == sig) return CASE_A;
+    if (mu == lam) return CASE_F1;
+    if (nu == sig) return CASE_F2;
+    const int fmu = lv.flo[mu], fnu = lv.flo[nu], flam = lv.flo[lam], fsig = lv.flo[sig];
+    if (fnu < flam || fsig < fmu) return CASE_A;
+    if ((flam < fmu) != (fsig < fnu)) return CASE_C;
+    return CASE_D;
+}
+
+__device__ Visit visit_sym(const TreeView& tv, const LevelView& lv, int mu, int nu, int lam, int sig,
+                           int alive) {
+    Visit v{O_NONE, 0, 0, 0, 0, 0, 0.0};
+    const int64_t n = lv.n;
+    const int64_t ib = lv.node_off + mu * n + nu;
+    const int64_t ik = lv.node_off + lam * n + sig;
+    const double nb = tv.bnorm[ib], nk = tv.knorm[ik];
+    if (nb < 0.0 || nk < 0.0) {
+        v.outcome = O_ABSENT;
+        return v;
+    }
+    const double fb = fnorm(nb, tv.mode), fk = fnorm(nk, tv.mode);
+    // slot refs: g0 P[nu,lam], g1 P[mu,lam], g2 P[nu,sig], g3 P[mu,sig]
+    const int rr[4] = {nu, mu, nu, mu}, rc[4] = {lam, lam, sig, sig};
+    bool screened = false, absent = false;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        if (!((alive >> g) & 1)) continue;
+        const double pn = tv.pnorm[lv.node_off + rr[g] * n + rc[g]];
+        if (pn < 0.0) {
+            v.links_absent++;
+            absent = true;
+            continue;
+        }
+        const double bound = sorted_product3(fb, pn, fk);
+        v.tie += is_tie(bound, tv.tau);
+        if (bound <= tv.tau) {
+            v.links_screen++;
+            screened = true;
+            // _SLOT_TRANSPOSES (exchange_symmetry.py:53): g1, g3 transpose bra; g2, g3 ket
+            const double bs = (g & 1) ? tv.bcol[ib] : tv.brow[ib];
+            const double ks = (g & 2) ? tv.krow[ik] : tv.kcol[ik];
+            v.ledger += ledger_term(pn, bs, ks);
+            continue;
+        }
+        v.live |= 1 << g;
+    }
+    if (!v.live) {
+        v.outcome = screened ? O_SCREEN : O_ABSENT;
+        return v;
+    }
+    v.label = absent ? CASE_SPARSE : case_label(lv, mu, nu, lam, sig);
+    const bool leaf = lv.leaf_id[mu] >= 0 && lv.leaf_id[nu] >= 0 && lv.leaf_id[lam] >= 0 &&
+                      lv.leaf_id[sig] >= 0;
+    v.outcome = leaf ? O_LEAF : O_EXPAND;
+    return v;
+}
+
+__device__ __forceinline__ uint64_t pack_task(int a, int b, int c, int d, int live) {
+    return (uint64_t)a | ((uint64_t)b << 15) | ((uint64_t)c << 30) | ((uint64_t)d << 45) |
+           ((uint64_t)live << 60);
+}
+
+struct ExpandArgs {
+    const uint64_t* in;
+    int64_t n_in;
+    const int* kid0;   // level-L spans (level-local pointers)
+    const int* kid1;
+    LevelView child;   // level L+1
+    TreeView tv;
+    uint64_t* out_expand;
+    uint64_t* out_leaf;
+    int* blk_counts;   // pass 1: per block packed (leaf | expand << 16)
+    const int64_t* blk_off_expand;
+    const int64_t* blk_off_leaf;
+    long long* counters;
+    unsigned long long* ledger;
+};
+
+// children of a span (a leaf stands in for itself, quadtree.py:47-49)
+__device__ __forceinline__ int kids(const ExpandArgs& a, int s, int* k) {
+    k[0] = a.kid0[s];
+    k[1] = a.kid1[s];
+    return k[1] < 0 ? 1 : 2;
+}
+
+// canonical child keys (exchange_symmetry.py:212-217)
+__device__ __forceinline__ bool canon_key(int key, int r, int c, int nr, int nc, int* x, int* y) {
+    if (r == c) {
+        if (nr == 1) {
+            *x = 0;
+            *y = 0;
+            return key == 0;
+        }
+        const int tx[3] = {0, 0, 1}, ty[3] = {0, 1, 1};
+        if (key >= 3) return false;
+        *x = tx[key];
+        *y = ty[key];
+        return true;
+    }
+    if (key >= nr * nc) return false;
+    *x = key / nc;
+    *y = key % nc;
+    return true;
+}
+
+template <bool SYM, bool WRITE>
+__global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
+    typedef cub::BlockScan<int, 256> Scan;
+    typedef cub::BlockReduce<double, 256> Red;
+    __shared__ union {
+        typename Scan::TempStorage scan;
+        typename Red::TempStorage red;
+    } tmp;
+    const int64_t t = blockIdx.x * 256ll + threadIdx.x;
+    const int64_t parent = t >> 4;
+    const int c = (int)(t & 15);
+    Visit v{O_NONE, 0, 0, 0, 0, 0, 0.0};
+    int cm = 0, cn = 0, cl = 0, cs = 0;
+    if (parent < a.n_in) {
+        const uint64_t task = a.in[parent];
+        const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
+                  sig = (task >> 45) & 0x7fff;
+        const int alive = (int)(task >> 60);
+        int km[2], kn[2], kl[2], ks[2];
+        const int nm = kids(a, mu, km), nn = kids(a, nu, kn), nl = kids(a, lam, kl),
+                  ns = kids(a, sig, ks);
+        bool valid;
+        if (!SYM) {
+            const int ia = (c >> 3) & 1, ic = (c >> 2) & 1, id = (c >> 1) & 1, ibb = c & 1;
+            valid = ia < nm && ic < nn && id < nl && ibb < ns;
+            if (valid) {
+                cm = km[ia];
+                cn = kn[ic];
+                cl = kl[id];
+                cs = ks[ibb];
+            }
+        } else {
+            int x, y, z, w;
+            valid = canon_key(c >> 2, mu, nu, nm, nn, &x, &y) && canon_key(c & 3, lam, sig, nl, ns, &z, &w);
+            if (valid) {
+                cm = km[x];
+                cn = kn[y];
+                cl = kl[z];
+                cs = ks[w];
+            }
+        }
+        if (valid) v = SYM ? visit_sym(a.tv, a.child, cm, cn, cl, cs, alive)
+                           : visit_naive(a.tv, a.child, cm, cn, cl, cs);
+    }
+    const int is_leaf = v.outcome == O_LEAF, is_exp = v.outcome == O_EXPAND;
+    int packed = is_leaf | (is_exp << 16), excl, total;
+    Scan(tmp.scan).ExclusiveSum(packed, excl, total);
+    if (!WRITE) {
+        if (threadIdx.x == 0) a.blk_counts[blockIdx.x] = total;
+        return;
+    }
+    if (is_leaf) {
+        const int lid[4] = {a.child.leaf_id[cm], a.child.leaf_id[cn], a.child.leaf_id[cl], a.child.leaf_id[cs]};
+        a.out_leaf[a.blk_off_leaf[blockIdx.x] + (excl & 0xffff)] = pack_task(lid[0], lid[1], lid[2], lid[3], v.live);
+    }
+    if (is_exp) a.out_expand[a.blk_off_expand[blockIdx.x] + (excl >> 16)] = pack_task(cm, cn, cl, cs, v.live);
+    // counters: warp-aggregated integer atomics (order independent)
+    const unsigned full = 0xffffffffu;
+    const int valid_child = v.outcome != O_NONE;
+    int vals[8] = {valid_child, v.outcome == O_SCREEN, v.outcome == O_ABSENT, is_leaf, is_exp,
+                   v.tie, v.links_screen, v.links_absent};
+    const int slots[8] = {C_VISITED, C_CULL_SCREEN, C_CULL_ABSENT, C_LEAF, C_EXPANDED, C_TIE_TASK,
+                          C_LINK_SCREEN, C_LINK_ABSENT};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int s = __reduce_add_sync(full, vals[k]);
+        if ((threadIdx.x & 31) == 0 && s) atomic_add_ll(&a.counters[slots[k]], (long long)s);
+    }
+    {
+        const int s = __reduce_add_sync(full, valid_child);
+        if ((threadIdx.x & 31) == 0 && s) atomic_add_ll(&a.counters[C_SPAWNED], (long long)s);
+    }
+    if (SYM) {
+        const bool counted = is_leaf || is_exp;
+#pragma unroll
+        for (int k = 0; k < HXF_NCASES; ++k) {
+            const int s1 = __reduce_add_sync(full, (int)(counted && v.label == k));
+            const int s2 = __reduce_add_sync(full, (int)(is_leaf && v.label == k));
+            if ((threadIdx.x & 31) == 0) {
+                if (s1) atomic_add_ll(&a.counters[C_CASE0 + k], (long long)s1);
+                if (s2) atomic_add_ll(&a.counters[C_CASELEAF0 + k], (long long)s2);
+            }
+        }
+    }
+    __syncthreads();
+    const double lsum = Red(tmp.red).Sum(v.ledger);
+    if (threadIdx.x == 0 && lsum != 0.0) {
+        unsigned long long limb[LEDGER_LIMBS];
+        fx_from_double<LEDGER_LIMBS>(lsum, LEDGER_SCALE, limb);
+        fx_atomic_add<LEDGER_LIMBS>(a.ledger, limb);
+    }
+}
+
+template <bool SYM>
+__global__ void k_root(TreeView tv, LevelView lv, uint64_t* out_expand, uint64_t* out_leaf,
+                       int* outcome, long long* counters, unsigned long long* ledger) {
+    Visit v = SYM ? visit_sym(tv, lv, 0, 0, 0, 0, 0xf) : visit_naive(tv, lv, 0, 0, 0, 0);
+    counters[C_VISITED] += 1;
+    counters[C_CULL_SCREEN] += v.outcome == O_SCREEN;
+    counters[C_CULL_ABSENT] += v.outcome == O_ABSENT;
+    counters[C_LEAF] += v.outcome == O_LEAF;
+    counters[C_EXPANDED] += v.outcome == O_EXPAND;
+    counters[C_TIE_TASK] += v.tie;
+    counters[C_LINK_SCREEN] += v.links_screen;
+    counters[C_LINK_ABSENT] += v.links_absent;
+    if (SYM && (v.outcome == O_LEAF || v.outcome == O_EXPAND)) {
+        counters[C_CASE0 + v.label] += 1;
+        if (v.outcome == O_LEAF) counters[C_CASELEAF0 + v.label] += 1;
+    }
+    if (v.ledger != 0.0) {
+        unsigned long long limb[LEDGER_LIMBS];
+        fx_from_double<LEDGER_LIMBS>(v.ledger, LEDGER_SCALE, limb);
+        fx_atomic_add<LEDGER_LIMBS>(ledger, limb);
+    }
+    if (v.outcome == O_EXPAND) out_expand[0] = pack_task(0, 0, 0, 0, v.live);
+    if (v.outcome == O_LEAF)
+        out_leaf[0] = pack_task(lv.leaf_id[0], lv.leaf_id[0], lv.leaf_id[0], lv.leaf_id[0], v.live);
+    *outcome = v.outcome;
+}
+
+template <typename T>
+T* talloc(size_t n, cudaStream_t st) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
+    if (e != cudaSuccess) throw HxfError{HXF_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e)};
+    return (T*)p;
+}
+
+__global__ void k_unpack_counts(const int* packed, int64_t n, int64_t* leaf, int64_t* expand) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    leaf[t] = packed[t] & 0xffff;
+    expand[t] = packed[t] >> 16;
+}
+
+}  // namespace
+
+// Run the traversal.  Returns the leaf-task list (device, caller frees with
+// cudaFreeAsync).  Counters / ledger are accumulated into the device arrays.
+// If shard_level >= 0 the expand frontier at that level is restricted to
+// [shard_begin, shard_end) and, unless shard_begin == 0, counters and leaf
+// tasks produced above the cut are discarded (they belong to rank 0).
+TraversalResult traverse(const TravInput& in, cudaStream_t st) {
+    hxf_system* s = in.sys;
+    TreeView tv{in.bra->norm, in.bra->rowsum, in.bra->colsum, in.ket->norm, in.ket->rowsum,
+                in.ket->colsum, in.dens->norm, in.tau, in.mode};
+    TraversalResult res;
+    res.leaf = nullptr;
+    res.n_leaf = 0;
+    res.frontier_sizes.clear();
+    long long* counters = in.counters;
+    unsigned long long* ledger = in.ledger;
+    // discard counters above a shard cut on non-zero shards: accumulate into scratch
+    long long* scratch_c = nullptr;
+    unsigned long long* scratch_l = nullptr;
+    const bool sharded = in.shard_level >= 0;
+    const bool discard_top = sharded && in.shard_begin != 0;
+    if (discard_top) {
+        scratch_c = talloc<long long>(C_NCOUNTERS, st);
+        scratch_l = talloc<unsigned long long>(LEDGER_LIMBS, st);
+        HXF_CUDA(cudaMemsetAsync(scratch_c, 0, C_NCOUNTERS * sizeof(long long), st));
+        HXF_CUDA(cudaMemsetAsync(scratch_l, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
+        counters = scratch_c;
+        ledger = scratch_l;
+    }
+    const int D = s->n_levels - 1;
+    std::vector<uint64_t*> leaf_parts;
+    std::vector<int64_t> leaf_counts;
+    uint64_t* cur = talloc<uint64_t>(1, st);
+    uint64_t* leaf0 = talloc<uint64_t>(1, st);
+    int* d_outcome = talloc<int>(1, st);
+    LevelView lv0{s->h_off[1] - s->h_off[0], s->node_off[0], s->lv.leaf_id + s->h_off[0],
+                  s->lv.flo + s->h_off[0]};
+    if (in.sym) k_root<true><<<1, 1, 0, st>>>(tv, lv0, cur, leaf0, d_outcome, counters, ledger);
+    else k_root<false><<<1, 1, 0, st>>>(tv, lv0, cur, leaf0, d_outcome, counters, ledger);
+    int outcome = 0;
+    HXF_CUDA(cudaMemcpyAsync(&outcome, d_outcome, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(d_outcome, st);
+    int64_t n_cur = outcome == O_EXPAND ? 1 : 0;
+    if (outcome == O_LEAF) {
+        leaf_parts.push_back(leaf0);
+        leaf_counts.push_back(1);
+    } else {
+        cudaFreeAsync(leaf0, st);
+    }
+    res.frontier_sizes.push_back(n_cur);
+    for (int L = 0; L < D && n_cur > 0; ++L) {
+        if (sharded && L == in.shard_level) {
+            // restrict the frontier to this shard; from here on counters are real
+            const int64_t b = std::min<int64_t>(in.shard_begin, n_cur);
+            const int64_t e = std::min<int64_t>(std::max<int64_t>(in.shard_end, b), n_cur);
+            uint64_t* part = talloc<uint64_t>(e - b, st);
+            if (e > b)
+                HXF_CUDA(cudaMemcpyAsync(part, cur + b, (e - b) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+            cudaFreeAsync(cur, st);
+            cur = part;
+            n_cur = e - b;
+            if (discard_top) {
+                // leaf tasks above the cut belong to shard 0
+                for (uint64_t* p : leaf_parts) cudaFreeAsync(p, st);
+                leaf_parts.clear();
+                leaf_counts.clear();
+            }
+            counters = in.counters;
+            ledger = in.ledger;
+            if (n_cur == 0) break;
+        }
+        if (in.frontier_only && L == in.frontier_level) break;
+        const int n_par = s->h_off[L + 1] - s->h_off[L];
+        (void)n_par;
+        const int base_ch = s->h_off[L + 1];
+        LevelView ch{s->h_off[L + 2] - s->h_off[L + 1], s->node_off[L + 1], s->lv.leaf_id + base_ch,
+                     s->lv.flo + base_ch};
+        const int64_t nthreads = n_cur * 16;
+        const int64_t nb = (nthreads + 255) / 256;
+        int* blk = talloc<int>(nb, st);
+        int64_t* cl = talloc<int64_t>(nb + 1, st);
+        int64_t* ce = talloc<int64_t>(nb + 1, st);
+        int64_t* ol = talloc<int64_t>(nb + 1, st);
+        int64_t* oe = talloc<int64_t>(nb + 1, st);
+        ExpandArgs a;
+        a.in = cur;
+        a.n_in = n_cur;
+        a.kid0 = s->lv.kid0 + s->h_off[L];
+        a.kid1 = s->lv.kid1 + s->h_off[L];
+        a.child = ch;
+        a.tv = tv;
+        a.blk_counts = blk;
+        a.counters = counters;
+        a.ledger = ledger;
+        a.out_expand = nullptr;
+        a.out_leaf = nullptr;
+        a.blk_off_expand = oe;
+        a.blk_off_leaf = ol;
+        if (in.sym) k_expand<true, false><<<(unsigned)nb, 256, 0, st>>>(a);
+        else k_expand<false, false><<<(unsigned)nb, 256, 0, st>>>(a);
+        k_unpack_counts<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(blk, nb, cl, ce);
+        HXF_CUDA(cudaMemsetAsync(cl + nb, 0, sizeof(int64_t), st));
+        HXF_CUDA(cudaMemsetAsync(ce + nb, 0, sizeof(int64_t), st));
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cl, ol, nb + 1, st);
+        void* tbuf = talloc<char>(tb, st);
+        cub::DeviceScan::ExclusiveSum(tbuf, tb, cl, ol, nb + 1, st);
+        cub::DeviceScan::ExclusiveSum(tbuf, tb, ce, oe, nb + 1, st);
+        int64_t tot[2];
+        HXF_CUDA(cudaMemcpyAsync(&tot[0], ol + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        HXF_CUDA(cudaMemcpyAsync(&tot[1], oe + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        HXF_CUDA(cudaStreamSynchronize(st));
+        uint64_t* nxt = talloc<uint64_t>(tot[1], st);
+        uint64_t* lf = talloc<uint64_t>(tot[0], st);
+        a.out_expand = nxt;
+        a.out_leaf = lf;
+        if (in.sym) k_expand<true, true><<<(unsigned)nb, 256, 0, st>>>(a);
+        else k_expand<false, true><<<(unsigned)nb, 256, 0, st>>>(a);
+        HXF_CUDA(cudaGetLastError());
+        for (void* p : {(void*)blk, (void*)cl, (void*)ce, (void*)ol, (void*)oe, tbuf, (void*)cur})
+            cudaFreeAsync(p, st);
+        if (tot[0]) {
+            leaf_parts.push_back(lf);
+            leaf_counts.push_back(tot[0]);
+        } else {
+            cudaFreeAsync(lf, st);
+        }
+        cur = nxt;
+        n_cur = tot[1];
+        res.frontier_sizes.push_back(n_cur);
+    }
+    if (in.frontier_only) {
+        res.frontier = cur;
+        res.n_frontier = n_cur;
+    } else {
+        cudaFreeAsync(cur, st);
+    }
+    // concatenate leaf parts
+    int64_t tot = 0;
+    for (int64_t c : leaf_counts) tot += c;
+    res.leaf = talloc<uint64_t>(tot, st);
+    res.n_leaf = tot;
+    int64_t off = 0;
+    for (size_t k = 0; k < leaf_parts.size(); ++k) {
+        HXF_CUDA(cudaMemcpyAsync(res.leaf + off, leaf_parts[k], leaf_counts[k] * sizeof(uint64_t),
+                                 cudaMemcpyDeviceToDevice, st));
+        off += leaf_counts[k];
+        cudaFreeAsync(leaf_parts[k], st);
+    }
+    if (scratch_c) cudaFreeAsync(scratch_c, st);
+    if (scratch_l) cudaFreeAsync(scratch_l, st);
+    HXF_CUDA(cudaGetLastError());
+    return res;
+}

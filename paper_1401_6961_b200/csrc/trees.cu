@@ -1,0 +1,493 @@
+// Device construction of the shell-pair and density quadtrees (SURVEY.md
+// kernels K1-K3).  Restates quadtree.py:198-337 of the reference:
+//   - s-proxy contracted overlap, block max |S| per leaf pair node, pruning
+//     pruned <=> block max |S| < tau_ovlp (quadtree.py:298-301, 323-327);
+//   - primitive pair tables per ordered shell pair of live leaf nodes
+//     (integrals.py:115-154);
+//   - Q_ij = (ij|ij) in canonical (min,max) orientation (quadtree.py:307-313),
+//     max over function pairs for p shells;
+//   - node norms with correctly rounded fsum (quadtree.py:20-25), row/column
+//     sum maxima (quadtree.py:314-316, 328-334);
+//   - density norms / absent flags (quadtree.py:210-235).
+// Node arrays are dense per level: node (r, c) of level L lives at
+// node_off[L] + r * n_L + c; a partition leaf repeats at deeper levels.
+
+#include <cub/cub.cuh>
+
+#include "boys.cuh"
+#include "hxf_internal.cuh"
+#include "eri_classes.cuh"
+
+#define SQRT_TWO_PI_POW_2_5 4.4569302618703215 /* sqrt(2 pi^{5/2}) */
+
+namespace {
+
+// numpy pairwise summation order for short contiguous vectors
+// (pairwise_sum: < 8 sequential, else 8 accumulators then the remainder).
+__device__ double np_sum(const double* v, int n, int stride) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; ++i) r = __dadd_rn(r, v[i * stride]);
+        return r;
+    }
+    double a[8];
+    for (int j = 0; j < 8; ++j) a[j] = v[j * stride];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; ++j) a[j] = __dadd_rn(a[j], v[(i + j) * stride]);
+    double r = __dadd_rn(__dadd_rn(__dadd_rn(a[0], a[1]), __dadd_rn(a[2], a[3])),
+                         __dadd_rn(__dadd_rn(a[4], a[5]), __dadd_rn(a[6], a[7])));
+    for (; i < n; ++i) r = __dadd_rn(r, v[i * stride]);
+    return r;
+}
+
+// contracted s(-proxy) overlap of shells a <= b (integrals.py:58-64)
+__device__ double overlap_s(const DevBasis& B, int a, int b) {
+    const double3 A = B.ctr[a], C = B.ctr[b];
+    const double dx = A.x - C.x, dy = A.y - C.y, dz = A.z - C.z;
+    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    const int a0 = B.poff[a], a1 = B.poff[a + 1], b0 = B.poff[b], b1 = B.poff[b + 1];
+    double terms[9];
+    int n = 0;
+    for (int i = a0; i < a1; ++i)
+        for (int j = b0; j < b1; ++j) {
+            const double ea = B.exps[i], eb = B.exps[j];
+            const double p = __dadd_rn(ea, eb);
+            const double s = __dmul_rn(pow(__ddiv_rn(M_PI, p), 1.5),
+                                       exp(__dmul_rn(__ddiv_rn(-__dmul_rn(ea, eb), p), r2)));
+            terms[n++] = __dmul_rn(__dmul_rn(B.sw[i], B.sw[j]), s);
+        }
+    return np_sum(terms, n, 1);
+}
+
+__global__ void k_leaf_smax(DevBasis B, DevLevels lv, const int* lslo, const int* lshi, int nleaf,
+                            double* smax) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nleaf * nleaf) return;
+    const int r = (int)(t / nleaf), c = (int)(t % nleaf);
+    if (r > c) return;
+    double m = 0.0;
+    for (int i = lslo[r]; i < lshi[r]; ++i)
+        for (int j = lslo[c]; j < lshi[c]; ++j) {
+            const double s = fabs(i <= j ? overlap_s(B, i, j) : overlap_s(B, j, i));
+            m = fmax(m, s);
+        }
+    smax[(int64_t)r * nleaf + c] = m;
+    smax[(int64_t)c * nleaf + r] = m;
+}
+
+__global__ void k_leaf_pair_counts(const double* smax, double tau, const int* lslo,
+                                   const int* lshi, const int* lplo, const int* lphi, int nleaf,
+                                   int64_t* npairs, int64_t* nprims) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nleaf * nleaf) return;
+    const int r = (int)(t / nleaf), c = (int)(t % nleaf);
+    const bool live = !(smax[t] < tau);
+    npairs[t] = live ? (int64_t)(lshi[r] - lslo[r]) * (lshi[c] - lslo[c]) : 0;
+    nprims[t] = live ? (int64_t)(lphi[r] - lplo[r]) * (lphi[c] - lplo[c]) : 0;
+}
+
+// one thread per live leaf pair node: fill pair ids, prim pair tables
+__global__ void k_fill_pairs(DevBasis B, const double* smax, double tau, const int* lslo,
+                             const int* lshi, int nleaf, const int64_t* pbase,
+                             const int64_t* ppbase, int64_t* leaf_base, int* pi, int* pj,
+                             int64_t* ppoff, PrimPair* pp) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nleaf * nleaf) return;
+    const int r = (int)(t / nleaf), c = (int)(t % nleaf);
+    if (smax[t] < tau) {
+        leaf_base[t] = -1;
+        return;
+    }
+    int64_t pid = pbase[t];
+    int64_t po = ppbase[t];
+    leaf_base[t] = pid;
+    for (int i = lslo[r]; i < lshi[r]; ++i)
+        for (int j = lslo[c]; j < lshi[c]; ++j, ++pid) {
+            pi[pid] = i;
+            pj[pid] = j;
+            ppoff[pid] = po;
+            const double3 A = B.ctr[i], C = B.ctr[j];
+            const double dx = A.x - C.x, dy = A.y - C.y, dz = A.z - C.z;
+            const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            for (int a = B.poff[i]; a < B.poff[i + 1]; ++a)
+                for (int b = B.poff[j]; b < B.poff[j + 1]; ++b, ++po) {
+                    const double ea = B.exps[a], eb = B.exps[b];
+                    const double p = __dadd_rn(ea, eb);
+                    const double w = __dmul_rn(__dmul_rn(B.w[a], B.w[b]),
+                                               exp(__dmul_rn(__ddiv_rn(-__dmul_rn(ea, eb), p), r2)));
+                    PrimPair q;
+                    q.p = p;
+                    q.ip = 1.0 / p;
+                    q.c = w * q.ip * SQRT_TWO_PI_POW_2_5;
+                    q.x = __ddiv_rn(__dadd_rn(__dmul_rn(ea, A.x), __dmul_rn(eb, C.x)), p);
+                    q.y = __ddiv_rn(__dadd_rn(__dmul_rn(ea, A.y), __dmul_rn(eb, C.y)), p);
+                    q.z = __ddiv_rn(__dadd_rn(__dmul_rn(ea, A.z), __dmul_rn(eb, C.z)), p);
+                    q.pad0 = 0.0;
+                    q.pad1 = 0.0;
+                    pp[po] = q;
+                }
+        }
+    if (r == nleaf - 1 && c == nleaf - 1) ppoff[pid] = po;
+}
+
+template <int LA, int LB>
+__device__ double diag_q(const PrimPair* pp, int64_t b0, int64_t b1, double3 A, double3 Bc) {
+    typedef Eri<LA, LB, LA, LB> E;
+    double out[E::NI * E::NJ * E::NK * E::NL];
+    E::eval(pp, (int)(b1 - b0), pp, (int)(b1 - b0), A, Bc, A, Bc, out);
+    double q = 0.0;
+    for (int x = 0; x < E::NI; ++x)
+        for (int y = 0; y < E::NJ; ++y) q = fmax(q, out[((x * E::NJ + y) * E::NK + x) * E::NL + y]);
+    return q;
+}
+
+// Q for canonical pairs i <= j, mirrored to (j, i) (quadtree.py:307-313)
+__global__ void k_diag_q(DevBasis B, int64_t n_pairs, const int* pi, const int* pj,
+                         const int64_t* ppoff, const PrimPair* pp, const int* leaf_of_shell,
+                         const int* lslo, const int* lshi, int nleaf, const int64_t* leaf_base,
+                         double* q) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_pairs) return;
+    const int i = pi[t], j = pj[t];
+    if (i > j) return;
+    const int64_t b0 = ppoff[t], b1 = ppoff[t + 1];
+    const double3 A = B.ctr[i], C = B.ctr[j];
+    const PrimPair* base = pp + b0;
+    double v;
+    const int li = B.l[i], lj = B.l[j];
+    if (li == 0 && lj == 0) v = diag_q<0, 0>(base, 0, b1 - b0, A, C);
+    else if (li == 0) v = diag_q<0, 1>(base, 0, b1 - b0, A, C);
+    else if (lj == 0) v = diag_q<1, 0>(base, 0, b1 - b0, A, C);
+    else v = diag_q<1, 1>(base, 0, b1 - b0, A, C);
+    q[t] = v;
+    if (i != j) {
+        // pair (j, i) lives in node (leaf(j), leaf(i)) at row j, column i
+        const int Li = leaf_of_shell[i], Lj = leaf_of_shell[j];
+        const int64_t mb = leaf_base[(int64_t)Lj * nleaf + Li];
+        q[mb + (int64_t)(j - lslo[Lj]) * (lshi[Li] - lslo[Li]) + (i - lslo[Li])] = v;
+    }
+}
+
+// leaf pair node norms: diag_norm = sqrt(fsum(Q^2)), row/col sum maxima
+__global__ void k_leaf_norms(const int* lslo, const int* lshi, int nleaf, const int64_t* leaf_base,
+                             const double* q, double* lnorm, double* lrow, double* lcol) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nleaf * nleaf) return;
+    const int r = (int)(t / nleaf), c = (int)(t % nleaf);
+    const int64_t b = leaf_base[t];
+    if (b < 0) {
+        lnorm[t] = -1.0;
+        lrow[t] = 0.0;
+        lcol[t] = 0.0;
+        return;
+    }
+    const int nr = lshi[r] - lslo[r], nc = lshi[c] - lslo[c];
+    const double* Q = q + b;
+    FSum fs;
+    for (int k = 0; k < nr * nc; ++k) fs.add(__dmul_rn(Q[k], Q[k]));
+    lnorm[t] = sqrt(fs.result());
+    double rm = -INFINITY, cm = -INFINITY;
+    for (int x = 0; x < nr; ++x) rm = fmax(rm, np_sum(Q + x * nc, nc, 1));
+    for (int y = 0; y < nc; ++y) {
+        double s = 0.0;
+        for (int x = 0; x < nr; ++x) s = __dadd_rn(s, Q[x * nc + y]);
+        cm = fmax(cm, s);
+    }
+    lrow[t] = rm;
+    lcol[t] = cm;
+}
+
+// fill one level of the pair tree (bottom-up); leaves copy leaf-pair data
+__global__ void k_pair_level(int level, int n, int nnext, const int* span_base_L,
+                             const int* leaf_id, const int* kid0, const int* kid1, int nleaf,
+                             const double* lnorm, const double* lrow, const double* lcol,
+                             const double* lsmax, double tau, const int64_t* node_off,
+                             double* norm, double* rowsum, double* colsum, double* smax) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * n) return;
+    const int r = (int)(t / n), c = (int)(t % n);
+    const int sr = span_base_L[0] + r, sc = span_base_L[0] + c;
+    const int64_t me = node_off[level] + t;
+    const int lr = leaf_id[sr], lc = leaf_id[sc];
+    if (lr >= 0 && lc >= 0) {
+        const int64_t k = (int64_t)lr * nleaf + lc;
+        norm[me] = lnorm[k];
+        rowsum[me] = lrow[k];
+        colsum[me] = lcol[k];
+        smax[me] = lsmax[k];
+        return;
+    }
+    const int ra[2] = {kid0[sr], kid1[sr]}, ca[2] = {kid0[sc], kid1[sc]};
+    const int na = ra[1] < 0 ? 1 : 2, nb = ca[1] < 0 ? 1 : 2;
+    double m = 0.0;
+    FSum fs;
+    bool any_live = false;
+    for (int a = 0; a < na; ++a)
+        for (int b = 0; b < nb; ++b) {
+            const int64_t ch = node_off[level + 1] + (int64_t)ra[a] * nnext + ca[b];
+            m = fmax(m, smax[ch]);
+            if (norm[ch] >= 0.0) {
+                any_live = true;
+                fs.add(__dmul_rn(norm[ch], norm[ch]));
+            }
+        }
+    smax[me] = m;
+    if (m < tau || !any_live) {
+        norm[me] = -1.0;
+        rowsum[me] = 0.0;
+        colsum[me] = 0.0;
+        return;
+    }
+    norm[me] = sqrt(fs.result());
+    double rm = -INFINITY, cm = -INFINITY;
+    for (int a = 0; a < na; ++a) {
+        FSum s;
+        for (int b = 0; b < nb; ++b) s.add(rowsum[node_off[level + 1] + (int64_t)ra[a] * nnext + ca[b]]);
+        rm = fmax(rm, s.result());
+    }
+    for (int b = 0; b < nb; ++b) {
+        FSum s;
+        for (int a = 0; a < na; ++a) s.add(colsum[node_off[level + 1] + (int64_t)ra[a] * nnext + ca[b]]);
+        cm = fmax(cm, s.result());
+    }
+    rowsum[me] = rm;
+    colsum[me] = cm;
+}
+
+// density leaf blocks: present iff any nonzero and norm > zero_drop
+__global__ void k_density_leaves(const double* P, int nfn, const int* lflo, const int* lfhi,
+                                 int nleaf, double zero_drop, double* lnorm) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nleaf * nleaf) return;
+    const int r = (int)(t / nleaf), c = (int)(t % nleaf);
+    FSum fs;
+    bool any = false;
+    for (int x = lflo[r]; x < lfhi[r]; ++x)
+        for (int y = lflo[c]; y < lfhi[c]; ++y) {
+            const double v = P[(int64_t)x * nfn + y];
+            any |= (v != 0.0);
+            fs.add(__dmul_rn(v, v));
+        }
+    double nrm = sqrt(fs.result());
+    lnorm[t] = (!any || nrm <= zero_drop) ? -1.0 : nrm;
+}
+
+__global__ void k_density_level(int level, int n, int nnext, const int* span_base_L,
+                                const int* leaf_id, const int* kid0, const int* kid1, int nleaf,
+                                const double* lnorm, const int64_t* node_off, double* norm) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * n) return;
+    const int r = (int)(t / n), c = (int)(t % n);
+    const int sr = span_base_L[0] + r, sc = span_base_L[0] + c;
+    const int64_t me = node_off[level] + t;
+    const int lr = leaf_id[sr], lc = leaf_id[sc];
+    if (lr >= 0 && lc >= 0) {
+        norm[me] = lnorm[(int64_t)lr * nleaf + lc];
+    } else {
+        const int ra[2] = {kid0[sr], kid1[sr]}, ca[2] = {kid0[sc], kid1[sc]};
+        const int na = ra[1] < 0 ? 1 : 2, nb = ca[1] < 0 ? 1 : 2;
+        FSum fs;
+        bool any = false;
+        for (int a = 0; a < na; ++a)
+            for (int b = 0; b < nb; ++b) {
+                const double v = norm[node_off[level + 1] + (int64_t)ra[a] * nnext + ca[b]];
+                if (v >= 0.0) {
+                    any = true;
+                    fs.add(__dmul_rn(v, v));
+                }
+            }
+        norm[me] = any ? sqrt(fs.result()) : -1.0;
+    }
+    // all-zero matrix: explicit root with norm 0 (quadtree.py:230-235)
+    if (level == 0 && t == 0 && norm[me] < 0.0) norm[me] = 0.0;
+}
+
+__global__ void k_maxabs(const double* v, int64_t n, unsigned long long* out) {
+    double m = 0.0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x)
+        m = fmax(m, fabs(v[t]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+inline unsigned nblk(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
+
+template <typename T>
+T* dalloc(size_t n, cudaStream_t st) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
+    if (e != cudaSuccess) throw HxfError{HXF_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e)};
+    return (T*)p;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host orchestration
+
+struct LeafTables {
+    int* lslo;
+    int* lshi;
+    int* lplo;
+    int* lphi;
+    int* lflo;
+    int* lfhi;
+    int* leaf_of_shell;
+};
+
+static LeafTables make_leaf_tables(hxf_system* s, cudaStream_t st, std::vector<void*>& tmp) {
+    const int nl = s->n_leaves;
+    std::vector<int> slo(nl), shi(nl), plo(nl), phi(nl), flo(nl), fhi(nl), los(s->ns);
+    const int D = s->n_levels - 1;
+    for (int k = s->h_off[D]; k < s->h_off[D + 1]; ++k) {
+        const int lid = s->h_leaf_id[k];
+        slo[lid] = s->h_slo[k];
+        shi[lid] = s->h_shi[k];
+        flo[lid] = s->h_flo[k];
+        fhi[lid] = s->h_fhi[k];
+        plo[lid] = s->h_poff[slo[lid]];
+        phi[lid] = s->h_poff[shi[lid]];
+        for (int i = slo[lid]; i < shi[lid]; ++i) los[i] = lid;
+    }
+    LeafTables t;
+    int** dst[] = {&t.lslo, &t.lshi, &t.lplo, &t.lphi, &t.lflo, &t.lfhi};
+    std::vector<int>* src[] = {&slo, &shi, &plo, &phi, &flo, &fhi};
+    for (int k = 0; k < 6; ++k) {
+        *dst[k] = dalloc<int>(nl, st);
+        tmp.push_back(*dst[k]);
+        HXF_CUDA(cudaMemcpyAsync(*dst[k], src[k]->data(), nl * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    t.leaf_of_shell = dalloc<int>(s->ns, st);
+    tmp.push_back(t.leaf_of_shell);
+    HXF_CUDA(cudaMemcpyAsync(t.leaf_of_shell, los.data(), s->ns * sizeof(int), cudaMemcpyHostToDevice, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+    return t;
+}
+
+void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
+    hxf_system* s = pr->sys;
+    std::vector<void*> tmp;
+    const int nl = s->n_leaves;
+    const int64_t nl2 = (int64_t)nl * nl;
+    LeafTables lt = make_leaf_tables(s, st, tmp);
+    double* lsmax = dalloc<double>(nl2, st);
+    tmp.push_back(lsmax);
+    k_leaf_smax<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, s->lv, lt.lslo, lt.lshi, nl, lsmax);
+    int64_t* npairs = dalloc<int64_t>(nl2 + 1, st);
+    int64_t* nprims = dalloc<int64_t>(nl2 + 1, st);
+    int64_t* pbase = dalloc<int64_t>(nl2 + 1, st);
+    int64_t* ppbase = dalloc<int64_t>(nl2 + 1, st);
+    tmp.insert(tmp.end(), {npairs, nprims, pbase, ppbase});
+    HXF_CUDA(cudaMemsetAsync(npairs + nl2, 0, sizeof(int64_t), st));
+    HXF_CUDA(cudaMemsetAsync(nprims + nl2, 0, sizeof(int64_t), st));
+    k_leaf_pair_counts<<<nblk(nl2), 256, 0, st>>>(lsmax, pr->tau_ovlp, lt.lslo, lt.lshi, lt.lplo,
+                                                  lt.lphi, nl, npairs, nprims);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, npairs, pbase, nl2 + 1, st);
+    void* tbuf = dalloc<char>(tb, st);
+    tmp.push_back(tbuf);
+    cub::DeviceScan::ExclusiveSum(tbuf, tb, npairs, pbase, nl2 + 1, st);
+    cub::DeviceScan::ExclusiveSum(tbuf, tb, nprims, ppbase, nl2 + 1, st);
+    int64_t tot[2];
+    HXF_CUDA(cudaMemcpyAsync(&tot[0], pbase + nl2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaMemcpyAsync(&tot[1], ppbase + nl2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+    pr->n_pairs = tot[0];
+    pr->n_prim_pairs = tot[1];
+    if (pr->n_pairs >= (1ll << 28))
+        throw HxfError{HXF_EINVAL, "too many significant shell pairs for the 28-bit pair ids"};
+    pr->leaf_base = dalloc<int64_t>(nl2, st);
+    pr->pi = dalloc<int>(pr->n_pairs, st);
+    pr->pj = dalloc<int>(pr->n_pairs, st);
+    pr->ppoff = dalloc<int64_t>(pr->n_pairs + 1, st);
+    pr->q = dalloc<double>(pr->n_pairs, st);
+    pr->pp = dalloc<PrimPair>(pr->n_prim_pairs, st);
+    HXF_CUDA(cudaMemcpyAsync(pr->ppoff + pr->n_pairs, &tot[1], sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    k_fill_pairs<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, lsmax, pr->tau_ovlp, lt.lslo, lt.lshi, nl,
+                                                 pbase, ppbase, pr->leaf_base, pr->pi, pr->pj,
+                                                 pr->ppoff, pr->pp);
+    HXF_CUDA(cudaMemcpyAsync(pr->ppoff + pr->n_pairs, &tot[1], sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    k_diag_q<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
+                                                     pr->pp, lt.leaf_of_shell, lt.lslo, lt.lshi, nl,
+                                                     pr->leaf_base, pr->q);
+    double* lnorm = dalloc<double>(nl2, st);
+    double* lrow = dalloc<double>(nl2, st);
+    double* lcol = dalloc<double>(nl2, st);
+    tmp.insert(tmp.end(), {lnorm, lrow, lcol});
+    k_leaf_norms<<<nblk(nl2, 128), 128, 0, st>>>(lt.lslo, lt.lshi, nl, pr->leaf_base, pr->q, lnorm, lrow, lcol);
+    const int64_t nn = s->node_off.back();
+    pr->norm = dalloc<double>(nn, st);
+    pr->rowsum = dalloc<double>(nn, st);
+    pr->colsum = dalloc<double>(nn, st);
+    pr->smax = dalloc<double>(nn, st);
+    int64_t* d_node_off = dalloc<int64_t>(s->node_off.size(), st);
+    tmp.push_back(d_node_off);
+    HXF_CUDA(cudaMemcpyAsync(d_node_off, s->node_off.data(), s->node_off.size() * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, st));
+    int* d_off = const_cast<int*>(s->lv.off);
+    for (int L = s->n_levels - 1; L >= 0; --L) {
+        const int n = s->h_off[L + 1] - s->h_off[L];
+        const int nnext = L + 1 < s->n_levels ? s->h_off[L + 2] - s->h_off[L + 1] : 0;
+        k_pair_level<<<nblk((int64_t)n * n), 256, 0, st>>>(
+            L, n, nnext, d_off + L, s->lv.leaf_id, s->lv.kid0, s->lv.kid1, nl, lnorm, lrow, lcol,
+            lsmax, pr->tau_ovlp, d_node_off, pr->norm, pr->rowsum, pr->colsum, pr->smax);
+    }
+    unsigned long long* dmax = dalloc<unsigned long long>(1, st);
+    tmp.push_back(dmax);
+    HXF_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+    if (pr->n_pairs) k_maxabs<<<256, 256, 0, st>>>(pr->q, pr->n_pairs, dmax);
+    unsigned long long hm = 0;
+    HXF_CUDA(cudaMemcpyAsync(&hm, dmax, sizeof(hm), cudaMemcpyDeviceToHost, st));
+    for (void* p : tmp) cudaFreeAsync(p, st);
+    HXF_CUDA(cudaStreamSynchronize(st));
+    HXF_CUDA(cudaGetLastError());
+    double mq;
+    memcpy(&mq, &hm, sizeof(mq));
+    pr->maxq = mq;
+    int hasp = 0;
+    for (int v : s->h_l) hasp |= v;
+    pr->has_p = hasp;
+}
+
+void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStream_t st) {
+    hxf_system* s = d->sys;
+    std::vector<void*> tmp;
+    const int nl = s->n_leaves;
+    const int64_t nl2 = (int64_t)nl * nl;
+    const int64_t n2 = (int64_t)s->nfn * s->nfn;
+    d->P = dalloc<double>(n2, st);
+    HXF_CUDA(cudaMemcpyAsync(d->P, P, n2 * sizeof(double),
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    LeafTables lt = make_leaf_tables(s, st, tmp);
+    double* lnorm = dalloc<double>(nl2, st);
+    tmp.push_back(lnorm);
+    k_density_leaves<<<nblk(nl2, 128), 128, 0, st>>>(d->P, s->nfn, lt.lflo, lt.lfhi, nl, d->zero_drop, lnorm);
+    const int64_t nn = s->node_off.back();
+    d->norm = dalloc<double>(nn, st);
+    int64_t* d_node_off = dalloc<int64_t>(s->node_off.size(), st);
+    tmp.push_back(d_node_off);
+    HXF_CUDA(cudaMemcpyAsync(d_node_off, s->node_off.data(), s->node_off.size() * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, st));
+    int* d_off = const_cast<int*>(s->lv.off);
+    for (int L = s->n_levels - 1; L >= 0; --L) {
+        const int n = s->h_off[L + 1] - s->h_off[L];
+        const int nnext = L + 1 < s->n_levels ? s->h_off[L + 2] - s->h_off[L + 1] : 0;
+        k_density_level<<<nblk((int64_t)n * n), 256, 0, st>>>(L, n, nnext, d_off + L, s->lv.leaf_id,
+                                                              s->lv.kid0, s->lv.kid1, nl, lnorm,
+                                                              d_node_off, d->norm);
+    }
+    unsigned long long* dmax = dalloc<unsigned long long>(1, st);
+    tmp.push_back(dmax);
+    HXF_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+    k_maxabs<<<256, 256, 0, st>>>(d->P, n2, dmax);
+    unsigned long long hm = 0;
+    HXF_CUDA(cudaMemcpyAsync(&hm, dmax, sizeof(hm), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaMemcpyAsync(&d->frob, d->norm, sizeof(double), cudaMemcpyDeviceToHost, st));
+    for (void* p : tmp) cudaFreeAsync(p, st);
+    HXF_CUDA(cudaStreamSynchronize(st));
+    HXF_CUDA(cudaGetLastError());
+    memcpy(&d->maxabs, &hm, sizeof(double));
+}

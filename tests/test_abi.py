@@ -1,0 +1,60 @@
+"""C-ABI checks that run without a GPU: the library loads, exports every
+symbol include/hxf.h declares, and fails loudly (no CPU fallback) when no
+device is present."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, has_cuda
+from paper_1401_6961_b200 import _native
+from paper_1401_6961_b200.basis import InvalidArgumentError
+
+HEADER = os.path.join(ROOT, "include", "hxf.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(hxf_[a-z_]+)\s*\(", text)))
+
+
+def test_header_declarations_match_binding_list():
+    assert _declared() == sorted(_native.EXPORTED)
+
+
+def test_library_exports_every_symbol():
+    lib = _native.lib()
+    for name in _declared():
+        assert hasattr(lib, name), name
+
+
+def test_struct_layouts_match_header():
+    # hxf_counters: 10 + 2*9 + 3 int64 + 1 double
+    assert ctypes.sizeof(_native.Counters) == (10 + 18 + 3) * 8 + 8
+    assert ctypes.sizeof(_native.ExchangeOpts) == 8 + 5 * 4 + 4 + 8 + 8 + 8 + 8 + 8
+
+
+def test_version():
+    assert _native.lib().hxf_version() == 1
+
+
+@pytest.mark.skipif(has_cuda(), reason="checks the no-device path")
+def test_no_device_fails_loudly():
+    from paper_1401_6961_b200 import basis, quadtree
+    system = basis.generate_cluster(1, seed=3)
+    part = quadtree.build_partition(system)
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        quadtree.build_pair_tree(system, part)
+
+
+def test_partition_matches_reference_rules():
+    from paper_1401_6961_b200 import basis, quadtree
+    shells = [basis.GaussianShell(center=[i, 0.0, 0.0], primitives=[(1.0, 1.0)]) for i in range(13)]
+    system = basis.BasisSystem(shells=basis.assign_offsets(shells), atoms=[])
+    part = quadtree.build_partition(system, leaf_size=10)
+    assert (part.root.left.n_functions, part.root.right.n_functions) == (6, 7)
+    with pytest.raises(InvalidArgumentError):
+        quadtree.build_partition(system, leaf_size=0)

@@ -1,0 +1,133 @@
+"""GPU parity: the CUDA path (through the drop-in API and the C ABI) against
+the reference's golden vectors and the CPU oracle.
+
+Bar (BASELINE.json north star): identical culled quartet set and counters
+(integer work is bit-exact; the only admissible difference is a bound within
+1e-12 relative of tau, which the device counts as a tie), K within 1e-10
+max-abs in FP64 (observed ~1e-15), culled-bound ledger within 1e-12 relative
+(it is an order-dependent FP64 sum in the reference too).
+"""
+
+import numpy as np
+import pytest
+
+import paper_1401_6961_b200 as hx
+from conftest import (CASES, counters_vec, quartet_bits, system_from_arrays, tree_walk)
+from oracle import hexfock_oracle as ho
+from paper_1401_6961_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+FIXTURES = ["cluster1", "cluster3", "cluster5", "cluster10", "ragged0", "ragged1",
+            "ragged2", "ragged3", "identity3", "c1"]
+K_TOL = 1e-10
+
+
+def _device_setup(g):
+    system = system_from_arrays(g["centers"], g["prims"], g["nprim"])
+    leaf = int(g["leaf_size"]) if "leaf_size" in g else 10
+    tau_ovlp = float(g["tau_ovlp"]) if "tau_ovlp" in g else 1e-11
+    part = hx.build_partition(system, leaf_size=leaf)
+    pairs = hx.build_pair_tree(system, part, tau_ovlp=tau_ovlp)
+    P_tree = hx.build_matrix_tree(g["P"], part)
+    return system, pairs, P_tree
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_device_trees_match_reference(golden, name):
+    g = golden(name)
+    _, pairs, P_tree = _device_setup(g)
+    pw = np.array(tree_walk(pairs))
+    ref = g["pair_walk"]
+    assert pw.shape == ref.shape
+    assert np.array_equal(pw[:, :5], ref[:, :5])            # spans
+    assert np.array_equal(pw[:, 6], ref[:, 6])              # pruned flags
+    assert np.allclose(pw[:, 5], ref[:, 5], rtol=1e-13, atol=0)   # diag norms (device Q)
+    assert np.allclose(pw[:, 7:], ref[:, 7:], rtol=1e-13, atol=0)
+    mw = np.array(tree_walk(P_tree))
+    assert np.array_equal(mw[:, :6], g["p_walk"][:, :6])    # fsum norms: bitwise
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_device_drivers_match_reference(golden, name):
+    g = golden(name)
+    system, pairs, P_tree = _device_setup(g)
+    n_sh = system.n_shells
+    keys = sorted({k.rsplit("_", 1)[0] for k in g if k.endswith("_counters")})
+    for key in keys:
+        sym = key.startswith("sym")
+        tag = key.split("_", 1)[1]
+        mode = "literal" if tag == "literal" else "schwarz"
+        tau = 1e-8 if tag == "literal" else float(tag)
+        log = [] if key + "_qbits" in g else None
+        if sym:
+            K, c = hx.build_exchange_symmetric(pairs, P_tree, tau, mode=mode, quartet_log=log)
+        else:
+            K, c = hx.build_exchange_naive(pairs, pairs, P_tree, tau, mode=mode, quartet_log=log)
+        assert c.ties_task == 0 and c.ties_leaf == 0, key
+        assert np.array_equal(counters_vec(c, sym), g[key + "_counters"]), key
+        assert c.culled_bound_ledger == pytest.approx(float(g[key + "_ledger"]), rel=1e-12, abs=1e-300)
+        err = np.abs(K - g[key + "_K"]).max()
+        assert err <= K_TOL, (key, err)
+        if log is not None:
+            bits = quartet_bits(log, n_sh)
+            ref = np.unpackbits(g[key + "_qbits"])[:n_sh ** 4].astype(bool)
+            assert np.array_equal(bits, ref), key
+
+
+def _p_case(units, seed, leaf):
+    cfg = configs.cube_cluster(units, seed, "tiny")
+    return cfg.system, cfg.P, leaf
+
+
+@pytest.mark.parametrize("units,seed,leaf,tau_ovlp,taus", [
+    (2, 9, 4, 0.0, (0.0, 1e-8)),
+    (3, 4, 6, 1e-11, (1e-10, 1e-8, 1e-6)),
+    (6, 5, 10, 1e-11, (1e-8,)),
+])
+def test_pshell_parity_with_oracle(units, seed, leaf, tau_ovlp, taus):
+    system, P, leaf = _p_case(units, seed, leaf)
+    st = ho.Setup(system, P, tau_ovlp=tau_ovlp, leaf_size=leaf)
+    part = hx.build_partition(system, leaf_size=leaf)
+    pairs = hx.build_pair_tree(system, part, tau_ovlp=tau_ovlp)
+    P_tree = hx.build_matrix_tree(P, part)
+    for tau in taus:
+        for sym in (False, True):
+            log, ref_log = [], []
+            if sym:
+                K, c = hx.build_exchange_symmetric(pairs, P_tree, tau, quartet_log=log)
+                K_ref, c_ref = st.symmetric(tau, quartet_log=ref_log)
+            else:
+                K, c = hx.build_exchange_naive(pairs, pairs, P_tree, tau, quartet_log=log)
+                K_ref, c_ref = st.naive(tau, quartet_log=ref_log)
+            assert c.ties_task == 0 and c.ties_leaf == 0
+            assert np.array_equal(counters_vec(c, sym), counters_vec(c_ref, sym)), (tau, sym)
+            assert set(log) == set(ref_log)
+            assert c.culled_bound_ledger == pytest.approx(c_ref.culled_bound_ledger, rel=1e-12, abs=1e-300)
+            assert np.abs(K - K_ref).max() <= K_TOL
+
+
+def test_pshell_dense_oracle_exactness():
+    system, P, leaf = _p_case(2, 9, 4)
+    st = ho.Setup(system, P, tau_ovlp=0.0, leaf_size=leaf)
+    K_dense = ho.dense_exchange(st.shells, P)
+    part = hx.build_partition(system, leaf_size=leaf)
+    pairs = hx.build_pair_tree(system, part, tau_ovlp=0.0)
+    P_tree = hx.build_matrix_tree(P, part)
+    K_n, _ = hx.build_exchange_naive(pairs, pairs, P_tree, 0.0)
+    K_s, _ = hx.build_exchange_symmetric(pairs, P_tree, 0.0)
+    assert np.abs(K_n - K_dense).max() <= 1e-12
+    assert np.abs(K_s - K_dense).max() <= 1e-12
+
+
+def test_repeated_builds_bitwise_identical():
+    cfg = configs.cube_cluster(4, 7, "tiny")
+    part = hx.build_partition(cfg.system, leaf_size=6)
+    pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
+    P_tree = hx.build_matrix_tree(cfg.P, part)
+    for f in (lambda: hx.build_exchange_naive(pairs, pairs, P_tree, 1e-9),
+              lambda: hx.build_exchange_symmetric(pairs, P_tree, 1e-9)):
+        K1, c1 = f()
+        K2, c2 = f()
+        assert np.array_equal(K1, K2)
+        assert c1.to_dict() == c2.to_dict()
