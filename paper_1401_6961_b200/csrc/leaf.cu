@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
                     if (!((live >> g) & 1)) continue;
                     const double pm = sm.pm[g][rowv[g] * cn[g] + colv[g]];
                     const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
-                    n_tie += fabs(bound - a.tau) <= 1e-12 * a.tau;
+                    n_tie += a.tau > 0.0 && fabs(bound - a.tau) <= 1e-12 * a.tau;
                     if (bound > a.tau) {
                         keep_any = true;
                         mask |= 1 << g;

@@ -56,7 +56,7 @@ struct Visit {
 __device__ __forceinline__ double fnorm(double v, int mode) { return mode == HXF_MODE_SCHWARZ ? sqrt(v) : v; }
 
 __device__ __forceinline__ bool is_tie(double bound, double tau) {
-    return fabs(bound - tau) <= 1e-12 * tau;
+    return tau > 0.0 && fabs(bound - tau) <= 1e-12 * tau;
 }
 
 // culled_task_bound (exchange_naive.py:91-102)

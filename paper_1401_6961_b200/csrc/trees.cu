@@ -18,7 +18,7 @@
 #include "hxf_internal.cuh"
 #include "eri_classes.cuh"
 
-#define SQRT_TWO_PI_POW_2_5 4.4569302618703215 /* sqrt(2 pi^{5/2}) */
+#define SQRT_TWO_PI_POW_2_5 5.914967172795613 /* sqrt(2 pi^{5/2}) */
 
 namespace {
 
