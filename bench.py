@@ -1,0 +1,366 @@
+"""Benchmark: surviving ERI quartets/s and K-build ms of the hierarchical exchange build.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` (torchrun for
+N>1) prints ONE JSON line on rank 0.  A step is one exchange build of the
+workload: density quadtree from a device-resident P + traversal + leaf
+screening + ERIs + contraction into K (+ NCCL all-reduce of K and the fourfold
+epilogue for N>1).  The shell-pair tree is geometry-only (built once per
+SCF) and is reported separately as `pair_tree_ms`.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port in oracle/, kind "port": the reference is pure Python and cannot
+travel to the GPU box) on a bounded sub-cluster of the same recipe with all
+host threads, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ERI_FLOPS = os.path.join(ROOT, "paper_1401_6961_b200", "csrc", "eri_flops.json")
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "surviving ERI quartets/s (FP64 exchange K-build)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--units", type=int, default=None, help="override cluster size (c3-c5 recipe)")
+    ap.add_argument("--mode", default="fourfold", choices=["naive", "fourfold"])
+    ap.add_argument("--tau", type=float, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample-units", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def make_config(args):
+    from paper_1401_6961_b200 import configs
+    kw = {}
+    if args.units is not None:
+        if args.config in ("c1", "c2"):
+            raise SystemExit("--units applies to the cube recipes c3-c5")
+        kw["n_units"] = args.units
+    cfg = configs.make(args.config, **kw)
+    if args.tau is not None:
+        cfg.tau_2e = args.tau
+        cfg.tau_ovlp = 1e-3 * args.tau
+    return cfg
+
+
+def workload_desc(args, cfg):
+    d = {"workload": f"{args.config}" + (f"-{args.units}units" if args.units else ""),
+         "mode": args.mode, "shells": cfg.n_shells, "functions": cfg.n_functions,
+         "tau_2e": cfg.tau_2e, "tau_ovlp": cfg.tau_ovlp, "leaf_size": cfg.leaf_size,
+         "bound": "schwarz", "basis": "s3/s1/p2 heavy + s3 light" if args.config != "c1" else "s3"}
+    return d
+
+
+# --------------------------------------------------------------- CPU (oracle port)
+
+def cpu_sample(args):
+    """Bounded sample of the workload for the CPU implementation."""
+    from paper_1401_6961_b200 import configs
+    if args.config == "c1":
+        cfg = configs.config1()
+        desc = "full c1 (32 s shells)"
+    elif args.config == "c2":
+        n = args.cpu_sample_units or 24
+        cfg = configs.config2(n_centers=n)
+        desc = f"c2 recipe, {n}-center chain"
+    else:
+        n = args.cpu_sample_units or 6
+        cfg = configs.cube_cluster(n, {"c3": 3, "c4": 4, "c5": 5}[args.config], args.config)
+        desc = f"{args.config} cube recipe, {n} units ({cfg.n_shells} shells, {cfg.n_functions} functions)"
+    if args.tau is not None:
+        cfg.tau_2e = args.tau
+        cfg.tau_ovlp = 1e-3 * args.tau
+    return cfg, desc
+
+
+def run_cpu(args, steps, warmup):
+    from oracle import hexfock_oracle as ho
+    cfg, desc = cpu_sample(args)
+    st = ho.Setup(cfg.system, cfg.P, tau_ovlp=cfg.tau_ovlp, leaf_size=cfg.leaf_size)
+    threads = os.cpu_count() or 1
+    f = st.symmetric if args.mode == "fourfold" else st.naive
+    for _ in range(warmup):
+        f(cfg.tau_2e, threads=threads)
+    times, quartets = [], 0
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        _, c = f(cfg.tau_2e, threads=threads)
+        times.append(time.perf_counter() - t0)
+        quartets = c.eri_shell_quartets
+    tot = sum(times)
+    return {"value": quartets * steps / tot, "unit": "quartets/s", "cores": threads,
+            "kind": "port", "sample": desc + f"; {quartets} surviving quartets per build, "
+                                             f"{1e3 * tot / steps:.0f} ms per build"}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = make_config(args) if args.config in ("c1", "c2") else None
+    steps, warmup = args.steps, min(args.warmup, 1)
+    cb = run_cpu(args, steps, warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "quartets/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "mode": args.mode,
+                       "note": "CPU oracle port of the reference algorithm on a bounded sample"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "quartets/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    del cfg
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[3 + k].lower() in ("active", "1")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def eri_flops(c):
+    tab = json.load(open(ERI_FLOPS))
+    return sum(c.class_prim_quartets[k] * tab["per_prim"][k] + c.class_quartets[k] * tab["per_quartet"][k]
+               for k in range(16))
+
+
+def native_arm(args):
+    import ctypes
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1401_6961_b200 as hx
+    from paper_1401_6961_b200 import _native, distributed, exchange
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    t0 = time.perf_counter()
+    cfg = make_config(args)
+    gen_s = time.perf_counter() - t0
+    sym = args.mode == "fourfold"
+    part = hx.build_partition(cfg.system, leaf_size=cfg.leaf_size)
+    part.device(local)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=cfg.tau_ovlp)
+    torch.cuda.synchronize()
+    pair_ms = 1e3 * (time.perf_counter() - t0)
+    n = cfg.n_functions
+    P_host = torch.from_numpy(cfg.P).pin_memory()
+    P_dev = P_host.to(dev)
+    K_dev = torch.empty((n, n), dtype=torch.float64, device=dev)
+    K_host = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    l2_flush = cfg.n_functions ** 2 * 8 < 256 * 1024 * 1024
+
+    peak = ctypes.c_double(0.0)
+    _native.check(_native.lib().hxf_fp64_peak(ctypes.byref(peak), _native.current_stream()))
+
+    shards = None
+    if world > 1:
+        P_tree0 = hx.build_matrix_tree(P_dev, part)
+        shards = distributed.plan(pairs, pairs, P_tree0, cfg.tau_2e, "schwarz", sym, world)
+        del P_tree0
+
+    def step(P_src):
+        P_tree = hx.build_matrix_tree(P_src, part)
+        if world > 1:
+            c, _ = distributed.exchange_sharded(pairs, pairs, P_tree, cfg.tau_2e, "schwarz", sym,
+                                                K_dev, shards=shards)
+            return c
+        _, c, _ = exchange.run_exchange(pairs, pairs, P_tree, cfg.tau_2e, "schwarz", sym, True,
+                                        None, K_out=K_dev)
+        return distributed.counters_from_vector(distributed.counters_vector(c), sym)
+
+    for _ in range(args.warmup):
+        step(P_dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    lc0 = ctypes.c_int64(0)
+    _native.lib().hxf_launch_count(ctypes.byref(lc0))
+    clocks = ClockSampler(local)
+    clocks.start()
+    times, stage, quartets, flops, last = [], [], 0, 0.0, None
+    stream = torch.cuda.current_stream()
+    for _ in range(args.steps):
+        if l2_flush:
+            flush.fill_(1.0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c = step(P_dev)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        stage.append(exchange.last_timings())
+        last = c
+    clk = clocks.stop()
+    lc1 = ctypes.c_int64(0)
+    _native.lib().hxf_launch_count(ctypes.byref(lc1))
+
+    # max over ranks of the timed region
+    tt = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms = float(tt.item())
+    quartets = last.eri_shell_quartets
+    value = quartets * args.steps / (total_ms * 1e-3)
+
+    # roofline: ERI + contraction kernels on the FP64 pipe (this rank)
+    _, cl, _ = (None, None, None)
+    # re-run once with the hxf counters struct for per-class work (untimed)
+    P_tree = hx.build_matrix_tree(P_dev, part)
+    shard = None
+    if world > 1:
+        lv, rng = shards
+        shard = (lv, rng[rank][0], rng[rank][1])
+    _, craw, _ = exchange.run_exchange(pairs, pairs, P_tree, cfg.tau_2e, "schwarz", sym, True, None,
+                                       K_out=K_dev, shard=shard, symmetrize=not (world > 1))
+    tm = exchange.last_timings()
+    flops = eri_flops(craw)
+    eri_ms = statistics.median([s[5] for s in stage]) if stage else tm[5]
+    achieved = flops / (eri_ms * 1e-3) / 1e12 if eri_ms > 0 else 0.0
+
+    # e2e: host P -> device, density tree, build, K -> host, through the public API
+    e2e_times = []
+    for _ in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        P_in = P_host.to(dev, non_blocking=True)
+        step(P_in)
+        K_host.copy_(K_dev, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_times.append(e0.elapsed_time(e1))
+    et = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_value = quartets * args.e2e_steps / (float(et.item()) * 1e-3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu(args, 1, 0)
+
+    if rank == 0:
+        stage_med = [statistics.median([s[k] for s in stage]) for k in range(6)] if stage else tm
+        line = {
+            "metric": METRIC, "value": value, "unit": "quartets/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64 geometry + decay density, SURVEY Appendix B)",
+            "config": dict(workload_desc(args, cfg), parallelism=f"product-tree shards x{world}",
+                           l2=("256 MB flush between steps" if l2_flush else
+                               "inputs larger than L2 (P alone exceeds 126 MB)")),
+            "k_build_ms": total_ms / args.steps,
+            "surviving_quartets_per_step": quartets,
+            "prim_quartets_per_step": last.prim_quartets,
+            "stage_ms": {"traversal": stage_med[0], "leaf_screen": stage_med[1],
+                         "eri_stage": stage_med[2], "epilogue": stage_med[3],
+                         "exchange_total": stage_med[4], "eri_kernels": stage_med[5]},
+            "pair_tree_ms": pair_ms, "input_gen_s": gen_s,
+            "counters": last.to_dict() | {"ties_task": last.ties_task, "ties_leaf": last.ties_leaf},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
+                         "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
+                         "traffic": None,
+                         "kernel": "k_eri<la,lb,lc,ld> (ERI + contraction), all classes",
+                         "flops_per_step_rank0": flops,
+                         "peak_source": "hxf_fp64_peak DFMA microbenchmark on this GPU "
+                                        "(MEASURED_PEAKS.json has no FP64 entry)"},
+            "e2e": {"value": e2e_value, "unit": "quartets/s",
+                    "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8,
+                    "ms_per_step": float(et.item()) / args.e2e_steps},
+            "cpu_baseline": cpu,
+            "gpu_launches": int(lc1.value - lc0.value),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        native_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -66,6 +66,8 @@ typedef struct hxf_counters {
     int64_t ties_task;   /* task-level bounds within 1e-12 rel of tau   */
     int64_t ties_leaf;   /* quartet-level bounds within 1e-12 rel of tau */
     int64_t prim_quartets; /* primitive quartets evaluated (work metric) */
+    int64_t class_quartets[16];      /* evaluated shell quartets per (li,lj,lk,ll) class */
+    int64_t class_prim_quartets[16]; /* primitive quartets per class                    */
     double culled_bound_ledger;
 } hxf_counters;
 
@@ -131,8 +133,21 @@ int hxf_frontier(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, double tau_2e, 
                  int symmetry, int level, int64_t* n_tasks, double* cost, int64_t cost_capacity,
                  void* stream);
 
+/* Symmetrise a device K in place: LogicError if max|K - K^T| > tol, else
+ * K = (K + K^T)/2 (symmetrize_final, exchange_symmetry.py:197-209); used after
+ * the multi-GPU reduction of partial K. */
+int hxf_symmetrize(double* K_dev, int n, double tol, void* stream);
+
+/* FP64 FMA throughput of the current device (TFLOP/s, FMA = 2 flops),
+ * measured with a dependent-chain-free DFMA kernel over all SMs. */
+int hxf_fp64_peak(double* tflops, void* stream);
+
+/* Number of kernels libhxf has launched in this process (work evidence). */
+int hxf_launch_count(int64_t* n);
+
 /* Device timing of the last hxf_exchange on this thread (ms per stage):
- * [0] traversal, [1] leaf screen, [2] ERI + contraction, [3] epilogue, [4] total. */
+ * [0] traversal, [1] leaf screen, [2] ERI stage (sort + ERI kernels), [3] epilogue,
+ * [4] total, [5] ERI + contraction kernels only. */
 int hxf_last_timings(double* ms, int n);
 
 #ifdef __cplusplus

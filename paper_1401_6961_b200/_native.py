@@ -22,7 +22,7 @@ EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_de
             "hxf_system_info", "hxf_pairs_build", "hxf_pairs_destroy", "hxf_pairs_download",
             "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
             "hxf_density_destroy", "hxf_density_download", "hxf_exchange", "hxf_frontier",
-            "hxf_last_timings")
+            "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count")
 
 
 class LogicError(RuntimeError):
@@ -45,6 +45,8 @@ class Counters(ctypes.Structure):
                 ("ties_task", ctypes.c_int64),
                 ("ties_leaf", ctypes.c_int64),
                 ("prim_quartets", ctypes.c_int64),
+                ("class_quartets", ctypes.c_int64 * 16),
+                ("class_prim_quartets", ctypes.c_int64 * 16),
                 ("culled_bound_ledger", ctypes.c_double)]
 
 
@@ -96,6 +98,9 @@ def lib():
     L.hxf_exchange.argtypes = [vp, vp, vp, P(ExchangeOpts), vp, P(Counters), vp]
     L.hxf_frontier.argtypes = [vp, vp, vp, dbl, i32, i32, i32, P(i64), vp, i64, vp]
     L.hxf_last_timings.argtypes = [vp, i32]
+    L.hxf_symmetrize.argtypes = [vp, i32, dbl, vp]
+    L.hxf_fp64_peak.argtypes = [P(dbl), vp]
+    L.hxf_launch_count.argtypes = [P(i64)]
     _lib = L
     return L
 

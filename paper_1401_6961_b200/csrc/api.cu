@@ -1,6 +1,7 @@
 // C ABI of libhxf.so (include/hxf.h): argument validation, device state
 // ownership, error codes.  All compute lives in trees.cu / traverse.cu / leaf.cu.
 
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -11,6 +12,9 @@
 static thread_local std::string g_err;
 
 void hxf_set_error(const std::string& msg) { g_err = msg; }
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch(int n) { g_launches += n; }
 
 int hxf_last_timings_impl(double* ms, int n);
 
@@ -44,6 +48,16 @@ void set_device(int dev) {
         throw HxfError{HXF_ECUDA, "no CUDA device available (libhxf has no CPU fallback)"};
     if (dev < 0 || dev >= n) throw HxfError{HXF_EINVAL, "device index out of range"};
     HXF_CUDA(cudaSetDevice(dev));
+    // keep stream-ordered allocations cached across builds (no release at sync)
+    static thread_local int configured = -1;
+    if (configured != dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        configured = dev;
+    }
 }
 
 }  // namespace
@@ -296,5 +310,29 @@ int hxf_frontier(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, double tau_2e, 
 }
 
 int hxf_last_timings(double* ms, int n) { return hxf_last_timings_impl(ms, n); }
+
+int hxf_symmetrize(double* K_dev, int n, double tol, void* stream) {
+    HXF_TRY({
+        if (!K_dev || n < 0) throw HxfError{HXF_EINVAL, "bad arguments"};
+        symmetrize_device(K_dev, n, tol, (cudaStream_t)stream);
+    })
+}
+
+int hxf_fp64_peak(double* tflops, void* stream) {
+    HXF_TRY({
+        if (!tflops) throw HxfError{HXF_EINVAL, "NULL argument"};
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+            throw HxfError{HXF_ECUDA, "no CUDA device available (libhxf has no CPU fallback)"};
+        *tflops = fp64_peak((cudaStream_t)stream);
+    })
+}
+
+int hxf_launch_count(int64_t* n) {
+    HXF_TRY({
+        if (!n) throw HxfError{HXF_EINVAL, "NULL argument"};
+        *n = g_launches.load();
+    })
+}
 
 }  // extern "C"

@@ -18,6 +18,7 @@ Run:  python gen_eri.py > eri_classes.cuh
 """
 
 import itertools
+import sys
 
 UNIT = ((1, 0, 0), (0, 1, 0), (0, 0, 1))
 ZERO = (0, 0, 0)
@@ -201,7 +202,52 @@ def gen_class(la, lb, lc, ld):
     return "\n".join(out)
 
 
+def _ops(expr):
+    return expr.count("*") + expr.count("+") + expr.count(" - ")
+
+
+def flop_counts(la, lb, lc, ld):
+    """Algorithmic FP64 flops of the scheme: (per primitive quartet, per shell quartet).
+
+    The all-s class uses the SURVEY.md 8(d) contract of 30 flops per primitive
+    quartet (integrals.py:157-165 with precomputed pair tables, F0 at a fixed
+    11).  Other classes add, per primitive quartet, the vertical-recursion
+    operations as generated plus 3 per extra F_m (downward recursion), the
+    W/Q-centre set-up (WP, WQ, QC: 3-6 each, 1/2p-type factors: 1 each);
+    per shell quartet the horizontal transfer.
+    """
+    L = la + lb + lc + ld
+    g = Gen()
+    es = carts_upto(la, la + lb)
+    fs = carts_upto(lc, lc + ld)
+    for e in es:
+        for f in fs:
+            g.vrr(e, f, 0)
+    per_prim = 30 + len(es) * len(fs) - 1
+    if L:
+        per_prim += 3 * L + L  # F_m recursion + bm scaling
+        per_prim += sum(_ops(line.split("=", 1)[1]) for line in g.lines)
+        if la + lb:
+            per_prim += 3 + 1 + 1 + 1    # PA (per bra prim, amortised as 1/kb), WP, o2p, rp
+        if lc + ld:
+            per_prim += 3 + 3 + 1 + 1    # WQ, QC, o2q, rq
+        if la + lb and lc + ld:
+            per_prim += 1
+    n_out = len(carts(la)) * len(carts(lb)) * len(carts(lc)) * len(carts(ld))
+    per_quartet = 2 * 3 * (lb + ld) + 2 * max(0, n_out - 1) * (1 if (lb or ld) else 0)
+    return per_prim, per_quartet
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--flops":
+        import json
+        tab = {}
+        for cls in itertools.product((0, 1), repeat=4):
+            idx = (cls[0] << 3) | (cls[1] << 2) | (cls[2] << 1) | cls[3]
+            tab[idx] = flop_counts(*cls)
+        print(json.dumps({"per_prim": [tab[k][0] for k in range(16)],
+                          "per_quartet": [tab[k][1] for k in range(16)]}))
+        return
     print("// generated by gen_eri.py -- do not edit")
     print("#pragma once")
     print("template <int LA, int LB, int LC, int LD> struct Eri;")

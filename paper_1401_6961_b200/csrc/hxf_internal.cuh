@@ -282,8 +282,12 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 enum {
     C_VISITED = 0, C_CULL_SCREEN, C_CULL_ABSENT, C_LEAF, C_ERIQ, C_CULL_LEAF, C_EXPANDED,
     C_SPAWNED, C_LINK_SCREEN, C_LINK_ABSENT, C_CASE0, C_CASELEAF0 = C_CASE0 + HXF_NCASES,
-    C_TIE_TASK = C_CASELEAF0 + HXF_NCASES, C_TIE_LEAF, C_PRIMQ, C_OVERFLOW, C_NCOUNTERS
+    C_TIE_TASK = C_CASELEAF0 + HXF_NCASES, C_TIE_LEAF, C_PRIMQ, C_OVERFLOW, C_CLSQ0,
+    C_CLSPQ0 = C_CLSQ0 + 16, C_NCOUNTERS = C_CLSPQ0 + 16
 };
+
+// kernels launched by the library (evidence that the device path ran)
+void note_launch(int n = 1);
 
 // ---------------------------------------------------------------- launchers
 // (defined in the .cu files)
@@ -295,5 +299,7 @@ void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStr
 struct ExchangeCtx;
 int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* o,
                  double* K_out, hxf_counters* c, cudaStream_t st);
+int symmetrize_device(double* K, int n, double tol, cudaStream_t st);
+double fp64_peak(cudaStream_t st);
 int frontier_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, double tau, int mode, int sym,
                  int level, int64_t* n_tasks, double* cost, int64_t cap, cudaStream_t st);

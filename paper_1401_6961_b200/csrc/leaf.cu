@@ -305,8 +305,14 @@ __global__ void __launch_bounds__(128) k_eri(EriArgs e) {
 #undef OUT
         }
     }
+    constexpr int CLS = (LA << 3) | (LB << 2) | (LC << 1) | LD;
+    const long long nq = warp_sum_ll(nprim > 0);
     nprim = warp_sum_ll(nprim);
-    if ((threadIdx.x & 31) == 0 && nprim) atomic_add_ll(&e.counters[C_PRIMQ], nprim);
+    if ((threadIdx.x & 31) == 0 && nprim) {
+        atomic_add_ll(&e.counters[C_PRIMQ], nprim);
+        atomic_add_ll(&e.counters[C_CLSPQ0 + CLS], nprim);
+        atomic_add_ll(&e.counters[C_CLSQ0 + CLS], nq);
+    }
 }
 
 __global__ void k_class_bounds(const uint64_t* rec, int64_t n, int64_t* bounds) {
@@ -383,7 +389,7 @@ void launch_eri_class(int cls, const EriArgs& e, cudaStream_t st) {
     if (!e.n) return;
     switch (cls) {
 #define C(a, b, c, d) \
-    case (a << 3) | (b << 2) | (c << 1) | d: k_eri<a, b, c, d><<<g, 128, 0, st>>>(e); break;
+    case (a << 3) | (b << 2) | (c << 1) | d: { k_eri<a, b, c, d><<<g, 128, 0, st>>>(e); note_launch(); } break;
         C(0, 0, 0, 0) C(0, 0, 0, 1) C(0, 0, 1, 0) C(0, 0, 1, 1)
         C(0, 1, 0, 0) C(0, 1, 0, 1) C(0, 1, 1, 0) C(0, 1, 1, 1)
         C(1, 0, 0, 0) C(1, 0, 0, 1) C(1, 0, 1, 0) C(1, 0, 1, 1)
@@ -537,8 +543,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sa.fill = dfill;
             sa.counters = scount;
             sa.ledger = sledger;
-            if (sym) k_screen<true, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa);
-            else k_screen<false, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa);
+            if (sym) { k_screen<true, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
+            else { k_screen<false, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
             HXF_CUDA(cudaGetLastError());
             long long c2[C_NCOUNTERS];
             unsigned long long l2[LEDGER_LIMBS];
@@ -592,8 +598,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sa.fill = dfill;
             sa.counters = scount;
             sa.ledger = sledger;
-            if (sym) k_screen<true, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa);
-            else k_screen<false, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa);
+            if (sym) { k_screen<true, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
+            else { k_screen<false, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
             HXF_CUDA(cudaGetLastError());
             unsigned long long fill = 0;
             HXF_CUDA(cudaMemcpyAsync(&fill, dfill, sizeof(fill), cudaMemcpyDeviceToHost, st));
@@ -609,19 +615,21 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             if (nrec) {
                 size_t tb = sort_tb;
                 cub::DeviceRadixSort::SortKeys(sort_tmp, tb, rec, rec2, nrec, 60, 64, st);
-                k_class_bounds<<<1, 32, 0, st>>>(rec2, nrec, dbounds);
+                { k_class_bounds<<<1, 32, 0, st>>>(rec2, nrec, dbounds); note_launch(); }
                 int64_t hb[17];
                 HXF_CUDA(cudaMemcpyAsync(hb, dbounds, sizeof(hb), cudaMemcpyDeviceToHost, st));
                 HXF_CUDA(cudaStreamSynchronize(st));
+                Timer tk(st);
                 for (int c = 0; c < 16; ++c) {
                     e.rec = rec2 + hb[c];
                     e.n = hb[c + 1] - hb[c];
                     launch_eri_class(c, e, st);
                 }
+                g_timings[5] += tk.stop();
                 HXF_CUDA(cudaGetLastError());
                 if (want_log)
-                    k_log<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(rec2, nrec, bra->pi, bra->pj, ket->pi,
-                                                                        ket->pj, dlog, o->log_capacity, dlogfill);
+                    { k_log<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(rec2, nrec, bra->pi, bra->pj, ket->pi,
+                                                                        ket->pj, dlog, o->log_capacity, dlogfill); note_launch(); }
             }
             long long c2[C_NCOUNTERS];
             unsigned long long l2[LEDGER_LIMBS];
@@ -643,11 +651,11 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     if (K_out) {
         double* Kd = o->K_on_device ? K_out : lalloc<double>(n2, st);
         if (Kfx) {
-            k_fx_to_double<<<1024, 256, 0, st>>>(Kfx, n2, S, Kd);
+            { k_fx_to_double<<<1024, 256, 0, st>>>(Kfx, n2, S, Kd); note_launch(); }
             if (sym && o->symmetrize) {
                 unsigned long long* dm = lalloc<unsigned long long>(1, st);
                 HXF_CUDA(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
-                k_asym<<<1024, 256, 0, st>>>(Kd, s->nfn, dm);
+                { k_asym<<<1024, 256, 0, st>>>(Kd, s->nfn, dm); note_launch(); }
                 unsigned long long hm = 0;
                 HXF_CUDA(cudaMemcpyAsync(&hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, st));
                 HXF_CUDA(cudaStreamSynchronize(st));
@@ -659,7 +667,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                     snprintf(buf, sizeof(buf), "asymmetry %.3e exceeds 1.0e-10; symmetry update set is inconsistent", asym);
                     throw HxfError{HXF_ELOGIC, buf};
                 }
-                k_symmetrize<<<1024, 256, 0, st>>>(Kd, s->nfn);
+                { k_symmetrize<<<1024, 256, 0, st>>>(Kd, s->nfn); note_launch(); }
             }
         } else {
             HXF_CUDA(cudaMemsetAsync(Kd, 0, n2 * sizeof(double), st));
@@ -707,8 +715,76 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     c.ties_task = acc_c[C_TIE_TASK];
     c.ties_leaf = acc_c[C_TIE_LEAF];
     c.prim_quartets = acc_c[C_PRIMQ];
+    for (int k = 0; k < 16; ++k) {
+        c.class_quartets[k] = acc_c[C_CLSQ0 + k];
+        c.class_prim_quartets[k] = acc_c[C_CLSPQ0 + k];
+    }
     c.culled_bound_ledger = fx_to_double<LEDGER_LIMBS>(acc_l, LEDGER_SCALE);
     return HXF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// utilities exported through the C ABI
+
+namespace {
+__global__ void k_dfma(double* out, int iters) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double b = 0.999999999, c = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+        }
+    }
+    const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (s == 12345.0) out[0] = s;  // keep the chain alive
+}
+}  // namespace
+
+int symmetrize_device(double* K, int n, double tol, cudaStream_t st) {
+    unsigned long long* dm = lalloc<unsigned long long>(1, st);
+    HXF_CUDA(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
+    { k_asym<<<1024, 256, 0, st>>>(K, n, dm); note_launch(); }
+    unsigned long long hm = 0;
+    HXF_CUDA(cudaMemcpyAsync(&hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(dm, st);
+    double asym;
+    memcpy(&asym, &hm, sizeof(asym));
+    if (asym > tol) {
+        char buf[160];
+        snprintf(buf, sizeof(buf), "asymmetry %.3e exceeds %.1e; symmetry update set is inconsistent", asym, tol);
+        throw HxfError{HXF_ELOGIC, buf};
+    }
+    { k_symmetrize<<<1024, 256, 0, st>>>(K, n); note_launch(); }
+    HXF_CUDA(cudaGetLastError());
+    return HXF_OK;
+}
+
+double fp64_peak(cudaStream_t st) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* out = lalloc<double>(1, st);
+    const int iters = 2048, threads = 512, blocks = sms * 4;
+    { k_dfma<<<blocks, threads, 0, st>>>(out, 16); note_launch(); }  // warm-up
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    { k_dfma<<<blocks, threads, 0, st>>>(out, iters); note_launch(); }
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFreeAsync(out, st);
+    HXF_CUDA(cudaGetLastError());
+    const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+    return flops / (ms * 1e-3) / 1e12;
 }
 
 int frontier_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, double tau, int mode, int sym,

@@ -375,8 +375,8 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     int* d_outcome = talloc<int>(1, st);
     LevelView lv0{s->h_off[1] - s->h_off[0], s->node_off[0], s->lv.leaf_id + s->h_off[0],
                   s->lv.flo + s->h_off[0]};
-    if (in.sym) k_root<true><<<1, 1, 0, st>>>(tv, lv0, cur, leaf0, d_outcome, counters, ledger);
-    else k_root<false><<<1, 1, 0, st>>>(tv, lv0, cur, leaf0, d_outcome, counters, ledger);
+    if (in.sym) { k_root<true><<<1, 1, 0, st>>>(tv, lv0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
+    else { k_root<false><<<1, 1, 0, st>>>(tv, lv0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
     int outcome = 0;
     HXF_CUDA(cudaMemcpyAsync(&outcome, d_outcome, sizeof(int), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaStreamSynchronize(st));
@@ -437,9 +437,9 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         a.out_leaf = nullptr;
         a.blk_off_expand = oe;
         a.blk_off_leaf = ol;
-        if (in.sym) k_expand<true, false><<<(unsigned)nb, 256, 0, st>>>(a);
-        else k_expand<false, false><<<(unsigned)nb, 256, 0, st>>>(a);
-        k_unpack_counts<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(blk, nb, cl, ce);
+        if (in.sym) { k_expand<true, false><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
+        else { k_expand<false, false><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
+        { k_unpack_counts<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(blk, nb, cl, ce); note_launch(); }
         HXF_CUDA(cudaMemsetAsync(cl + nb, 0, sizeof(int64_t), st));
         HXF_CUDA(cudaMemsetAsync(ce + nb, 0, sizeof(int64_t), st));
         size_t tb = 0;
@@ -455,8 +455,8 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         uint64_t* lf = talloc<uint64_t>(tot[0], st);
         a.out_expand = nxt;
         a.out_leaf = lf;
-        if (in.sym) k_expand<true, true><<<(unsigned)nb, 256, 0, st>>>(a);
-        else k_expand<false, true><<<(unsigned)nb, 256, 0, st>>>(a);
+        if (in.sym) { k_expand<true, true><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
+        else { k_expand<false, true><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         HXF_CUDA(cudaGetLastError());
         for (void* p : {(void*)blk, (void*)cl, (void*)ce, (void*)ol, (void*)oe, tbuf, (void*)cur})
             cudaFreeAsync(p, st);

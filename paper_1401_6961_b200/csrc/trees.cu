@@ -375,7 +375,7 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     LeafTables lt = make_leaf_tables(s, st, tmp);
     double* lsmax = dalloc<double>(nl2, st);
     tmp.push_back(lsmax);
-    k_leaf_smax<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, s->lv, lt.lslo, lt.lshi, nl, lsmax);
+    { k_leaf_smax<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, s->lv, lt.lslo, lt.lshi, nl, lsmax); note_launch(); }
     int64_t* npairs = dalloc<int64_t>(nl2 + 1, st);
     int64_t* nprims = dalloc<int64_t>(nl2 + 1, st);
     int64_t* pbase = dalloc<int64_t>(nl2 + 1, st);
@@ -383,8 +383,8 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     tmp.insert(tmp.end(), {npairs, nprims, pbase, ppbase});
     HXF_CUDA(cudaMemsetAsync(npairs + nl2, 0, sizeof(int64_t), st));
     HXF_CUDA(cudaMemsetAsync(nprims + nl2, 0, sizeof(int64_t), st));
-    k_leaf_pair_counts<<<nblk(nl2), 256, 0, st>>>(lsmax, pr->tau_ovlp, lt.lslo, lt.lshi, lt.lplo,
-                                                  lt.lphi, nl, npairs, nprims);
+    { k_leaf_pair_counts<<<nblk(nl2), 256, 0, st>>>(lsmax, pr->tau_ovlp, lt.lslo, lt.lshi, lt.lplo,
+                                                  lt.lphi, nl, npairs, nprims); note_launch(); }
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, npairs, pbase, nl2 + 1, st);
     void* tbuf = dalloc<char>(tb, st);
@@ -406,18 +406,18 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     pr->q = dalloc<double>(pr->n_pairs, st);
     pr->pp = dalloc<PrimPair>(pr->n_prim_pairs, st);
     HXF_CUDA(cudaMemcpyAsync(pr->ppoff + pr->n_pairs, &tot[1], sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    k_fill_pairs<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, lsmax, pr->tau_ovlp, lt.lslo, lt.lshi, nl,
+    { k_fill_pairs<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, lsmax, pr->tau_ovlp, lt.lslo, lt.lshi, nl,
                                                  pbase, ppbase, pr->leaf_base, pr->pi, pr->pj,
-                                                 pr->ppoff, pr->pp);
+                                                 pr->ppoff, pr->pp); note_launch(); }
     HXF_CUDA(cudaMemcpyAsync(pr->ppoff + pr->n_pairs, &tot[1], sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    k_diag_q<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
+    { k_diag_q<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
                                                      pr->pp, lt.leaf_of_shell, lt.lslo, lt.lshi, nl,
-                                                     pr->leaf_base, pr->q);
+                                                     pr->leaf_base, pr->q); note_launch(); }
     double* lnorm = dalloc<double>(nl2, st);
     double* lrow = dalloc<double>(nl2, st);
     double* lcol = dalloc<double>(nl2, st);
     tmp.insert(tmp.end(), {lnorm, lrow, lcol});
-    k_leaf_norms<<<nblk(nl2, 128), 128, 0, st>>>(lt.lslo, lt.lshi, nl, pr->leaf_base, pr->q, lnorm, lrow, lcol);
+    { k_leaf_norms<<<nblk(nl2, 128), 128, 0, st>>>(lt.lslo, lt.lshi, nl, pr->leaf_base, pr->q, lnorm, lrow, lcol); note_launch(); }
     const int64_t nn = s->node_off.back();
     pr->norm = dalloc<double>(nn, st);
     pr->rowsum = dalloc<double>(nn, st);
@@ -431,14 +431,14 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     for (int L = s->n_levels - 1; L >= 0; --L) {
         const int n = s->h_off[L + 1] - s->h_off[L];
         const int nnext = L + 1 < s->n_levels ? s->h_off[L + 2] - s->h_off[L + 1] : 0;
-        k_pair_level<<<nblk((int64_t)n * n), 256, 0, st>>>(
+        { k_pair_level<<<nblk((int64_t)n * n), 256, 0, st>>>(
             L, n, nnext, d_off + L, s->lv.leaf_id, s->lv.kid0, s->lv.kid1, nl, lnorm, lrow, lcol,
-            lsmax, pr->tau_ovlp, d_node_off, pr->norm, pr->rowsum, pr->colsum, pr->smax);
+            lsmax, pr->tau_ovlp, d_node_off, pr->norm, pr->rowsum, pr->colsum, pr->smax); note_launch(); }
     }
     unsigned long long* dmax = dalloc<unsigned long long>(1, st);
     tmp.push_back(dmax);
     HXF_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
-    if (pr->n_pairs) k_maxabs<<<256, 256, 0, st>>>(pr->q, pr->n_pairs, dmax);
+    if (pr->n_pairs) { k_maxabs<<<256, 256, 0, st>>>(pr->q, pr->n_pairs, dmax); note_launch(); }
     unsigned long long hm = 0;
     HXF_CUDA(cudaMemcpyAsync(&hm, dmax, sizeof(hm), cudaMemcpyDeviceToHost, st));
     for (void* p : tmp) cudaFreeAsync(p, st);
@@ -464,7 +464,7 @@ void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStr
     LeafTables lt = make_leaf_tables(s, st, tmp);
     double* lnorm = dalloc<double>(nl2, st);
     tmp.push_back(lnorm);
-    k_density_leaves<<<nblk(nl2, 128), 128, 0, st>>>(d->P, s->nfn, lt.lflo, lt.lfhi, nl, d->zero_drop, lnorm);
+    { k_density_leaves<<<nblk(nl2, 128), 128, 0, st>>>(d->P, s->nfn, lt.lflo, lt.lfhi, nl, d->zero_drop, lnorm); note_launch(); }
     const int64_t nn = s->node_off.back();
     d->norm = dalloc<double>(nn, st);
     int64_t* d_node_off = dalloc<int64_t>(s->node_off.size(), st);
@@ -475,14 +475,14 @@ void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStr
     for (int L = s->n_levels - 1; L >= 0; --L) {
         const int n = s->h_off[L + 1] - s->h_off[L];
         const int nnext = L + 1 < s->n_levels ? s->h_off[L + 2] - s->h_off[L + 1] : 0;
-        k_density_level<<<nblk((int64_t)n * n), 256, 0, st>>>(L, n, nnext, d_off + L, s->lv.leaf_id,
+        { k_density_level<<<nblk((int64_t)n * n), 256, 0, st>>>(L, n, nnext, d_off + L, s->lv.leaf_id,
                                                               s->lv.kid0, s->lv.kid1, nl, lnorm,
-                                                              d_node_off, d->norm);
+                                                              d_node_off, d->norm); note_launch(); }
     }
     unsigned long long* dmax = dalloc<unsigned long long>(1, st);
     tmp.push_back(dmax);
     HXF_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
-    k_maxabs<<<256, 256, 0, st>>>(d->P, n2, dmax);
+    { k_maxabs<<<256, 256, 0, st>>>(d->P, n2, dmax); note_launch(); }
     unsigned long long hm = 0;
     HXF_CUDA(cudaMemcpyAsync(&hm, dmax, sizeof(hm), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaMemcpyAsync(&d->frob, d->norm, sizeof(double), cudaMemcpyDeviceToHost, st));

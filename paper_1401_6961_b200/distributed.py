@@ -1,0 +1,122 @@
+"""Multi-GPU exchange build: product-tree sharding + NCCL reduction of K.
+
+SURVEY.md 8(e): subtrees of the product (hextree) task space are independent
+except for accumulation into K (the reference's depth-1 thread farm,
+exchange_naive.py:220-235, and the paper's parallel argument).  Every rank
+expands the top levels identically to a cut level whose frontier holds
+>= 64 tasks per rank, takes a contiguous, cost-balanced range of that
+frontier (deterministic), runs traversal + leaf screening + ERIs on it into a
+private K, and the partial K are summed with one all-reduce (NCCL over
+NVLink; gloo on CPU for the host-logic tests).  The fourfold epilogue
+(symmetrize_final) runs once on the reduced K.  Counters are summed the same
+way; work above the cut is counted by shard 0 only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .exchange import CASE_LABELS, SymmetryCounters, TraversalCounters, run_exchange
+
+
+def split_by_cost(costs, world: int):
+    """Contiguous ranges [b, e) of a frontier with ~equal summed cost per rank."""
+    costs = np.asarray(costs, dtype=float)
+    n = len(costs)
+    if world <= 1 or n == 0:
+        return [(0, n)] + [(n, n)] * max(0, world - 1)
+    cum = np.concatenate([[0.0], np.cumsum(costs)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(cum, total * r / world, side="left")))
+    cuts.append(n)
+    cuts = np.maximum.accumulate(np.minimum(cuts, n))
+    return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+def frontier(bra, ket, P, tau_2e, mode, symmetry, level):
+    """Expand-list size (and per-task cost estimates) at `level`."""
+    n = ctypes.c_int64(0)
+    _native.check(_native.lib().hxf_frontier(bra._t.handle, ket._t.handle, P._t.handle, float(tau_2e),
+                                             0 if mode == "schwarz" else 1, 1 if symmetry else 0,
+                                             int(level), ctypes.byref(n), None, 0,
+                                             _native.current_stream()))
+    count = int(n.value)
+    costs = np.empty(max(count, 1))
+    _native.check(_native.lib().hxf_frontier(bra._t.handle, ket._t.handle, P._t.handle, float(tau_2e),
+                                             0 if mode == "schwarz" else 1, 1 if symmetry else 0,
+                                             int(level), ctypes.byref(n), _native.ptr(costs), count,
+                                             _native.current_stream()))
+    return count, costs[:count]
+
+
+def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=64):
+    """Choose the cut level and this job's shard ranges (same on every rank)."""
+    n_levels = len(bra._t.ds.levels)
+    level, count, costs = 0, 1, np.ones(1)
+    for L in range(n_levels - 1):
+        count, costs = frontier(bra, ket, P, tau_2e, mode, symmetry, L)
+        level = L
+        if count >= min_tasks_per_rank * world:
+            break
+    return level, split_by_cost(costs, world)
+
+
+def counters_vector(c) -> np.ndarray:
+    """Flatten an hxf counters struct to float64 (int64 counts are exact below 2^53)."""
+    v = [c.tasks_visited, c.tasks_culled_screening, c.tasks_culled_absent, c.leaf_contractions,
+         c.eri_shell_quartets, c.quartets_culled_leaf, c.tasks_expanded, c.children_spawned,
+         c.links_culled_screening, c.links_culled_absent, c.ties_task, c.ties_leaf,
+         c.prim_quartets]
+    v += list(c.case_tasks) + list(c.case_leaf_tasks)
+    v += list(c.class_quartets) + list(c.class_prim_quartets)
+    v.append(c.culled_bound_ledger)
+    return np.asarray(v, dtype=np.float64)
+
+
+def counters_from_vector(v, symmetric):
+    out = SymmetryCounters() if symmetric else TraversalCounters()
+    keys = ("tasks_visited", "tasks_culled_screening", "tasks_culled_absent", "leaf_contractions",
+            "eri_shell_quartets", "quartets_culled_leaf", "tasks_expanded", "children_spawned")
+    for k, x in zip(keys, v[:8]):
+        setattr(out, k, int(round(x)))
+    if symmetric:
+        out.links_culled_screening = int(round(v[8]))
+        out.links_culled_absent = int(round(v[9]))
+        for g, lab in enumerate(CASE_LABELS):
+            out.case_tasks[lab] = int(round(v[13 + g]))
+            out.case_leaf_tasks[lab] = int(round(v[22 + g]))
+    out.ties_task, out.ties_leaf, out.prim_quartets = (int(round(x)) for x in v[10:13])
+    out.culled_bound_ledger = float(v[-1])
+    return out
+
+
+def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, shards=None):
+    """One rank's share of a sharded build + the all-reduce of K and counters.
+
+    K_dev: torch CUDA tensor (n x n float64), overwritten with the full K on
+    every rank.  Returns (counters, shard plan).
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if shards is None:
+        shards = plan(bra, ket, P, tau_2e, mode, symmetry, world)
+    level, ranges = shards
+    b, e = ranges[rank]
+    _, c, _ = run_exchange(bra, ket, P, tau_2e, mode, symmetry, True, None, K_out=K_dev,
+                           shard=(level, b, e), symmetrize=False)
+    vec = torch.from_numpy(counters_vector(c)).to(K_dev.device)
+    if world > 1:
+        dist.all_reduce(K_dev, group=group)
+        dist.all_reduce(vec, group=group)
+    if symmetry:
+        _native.check(_native.lib().hxf_symmetrize(ctypes.c_void_p(K_dev.data_ptr()), K_dev.shape[0],
+                                                   1e-10, _native.current_stream()))
+    return counters_from_vector(vec.cpu().numpy(), symmetry), shards

@@ -289,9 +289,10 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
 
 
 def last_timings():
-    """Device stage times (ms) of the last build: traversal, screen, eri, epilogue, total."""
-    out = (ctypes.c_double * 5)()
-    _native.lib().hxf_last_timings(out, 5)
+    """Device stage times (ms) of the last build on this thread:
+    [traversal, screen, eri stage, epilogue, total, eri kernels only]."""
+    out = (ctypes.c_double * 6)()
+    _native.lib().hxf_last_timings(out, 6)
     return list(out)
 
 

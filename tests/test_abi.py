@@ -18,7 +18,7 @@ HEADER = os.path.join(ROOT, "include", "hxf.h")
 
 def _declared():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(hxf_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(hxf_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declarations_match_binding_list():
@@ -32,8 +32,8 @@ def test_library_exports_every_symbol():
 
 
 def test_struct_layouts_match_header():
-    # hxf_counters: 10 + 2*9 + 3 int64 + 1 double
-    assert ctypes.sizeof(_native.Counters) == (10 + 18 + 3) * 8 + 8
+    # hxf_counters: 10 + 2*9 + 3 + 2*16 int64 + 1 double
+    assert ctypes.sizeof(_native.Counters) == (10 + 18 + 3 + 32) * 8 + 8
     assert ctypes.sizeof(_native.ExchangeOpts) == 8 + 5 * 4 + 4 + 8 + 8 + 8 + 8 + 8
 
 
