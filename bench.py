@@ -310,7 +310,7 @@ def native_arm(args):
     et = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = quartets * args.e2e_steps / (float(et.item()) * 1e-3)
+    e2e_value = quartets * args.e2e_steps / (float(et.item()) * 1e-3) if args.e2e_steps else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -343,7 +343,7 @@ def native_arm(args):
                                         "(MEASURED_PEAKS.json has no FP64 entry)"},
             "e2e": {"value": e2e_value, "unit": "quartets/s",
                     "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8,
-                    "ms_per_step": float(et.item()) / args.e2e_steps},
+                    "ms_per_step": float(et.item()) / max(args.e2e_steps, 1)},
             "cpu_baseline": cpu,
             "gpu_launches": int(lc1.value - lc0.value),
             "clocks": clk,

@@ -198,7 +198,7 @@ void hxf_pairs_destroy(hxf_pairs* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     void* ptrs[] = {p->norm, p->rowsum, p->colsum, p->smax, p->leaf_base, p->pi,
-                    p->pj,   p->ppoff,  p->q,      p->pp};
+                    p->pj,   p->ppoff,  p->q,      p->pp,       p->info};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     delete p;

@@ -4,7 +4,7 @@ For each angular class (la, lb, lc, ld) in {0,1}^4 this emits
 
     struct Eri<la,lb,lc,ld> {
         static constexpr int NI, NJ, NK, NL;
-        __device__ static void eval(bra, nb, ket, nk, A, B, C, D, out);
+        __device__ static void eval(bra, nb, ket, nk, A, B, C, D, tab, out);
     };
 
 where bra[0:nb] / ket[0:nk] are the primitive pairs of the bra / ket shell
@@ -110,17 +110,47 @@ def gen_class(la, lb, lc, ld):
     w(f"  static constexpr int NI = {ni}, NJ = {nj}, NK = {nk}, NL = {nl}, L = {L};")
     w("  __device__ __forceinline__ static void eval(const PrimPair* __restrict__ bra, int nb,")
     w("      const PrimPair* __restrict__ ket, int nk, const double3 A, const double3 B,")
-    w("      const double3 C, const double3 D, double* __restrict__ out) {")
+    w("      const double3 C, const double3 D, const double* __restrict__ tab,")
+    w("      double* __restrict__ out) {")
     accs = [(e, f) for e in es for f in fs]
     for e, f in accs:
         w(f"    double acc_{name(e)}_{name(f)} = 0.0;")
+    # Light classes (L <= 1): the ket primitives of the quartet are loaded once
+    # into registers (inner loop fully unrolled to MAXK = 9; the primitive
+    # counts are warp-uniform because survivors are sorted by them), so each
+    # primitive quartet costs no global load.  Heavier classes reload them.
+    cached = L <= 1
+    if cached:
+        w("    constexpr int MK = 9;")
+        need_ip = lc + ld > 0
+        w("    double kqp[MK], kqc[MK], kqx[MK], kqy[MK], kqz[MK];")
+        if need_ip:
+            w("    double kqi[MK];")
+        w("#pragma unroll")
+        w("    for (int t = 0; t < MK; ++t)")
+        w("      if (t < nk) {")
+        w("        const PrimPair q = load_pp(ket + t);")
+        w("        kqp[t] = q.p; kqc[t] = q.c; kqx[t] = q.x; kqy[t] = q.y; kqz[t] = q.z;")
+        if need_ip:
+            w("        kqi[t] = q.ip;")
+        w("      }")
     w("    for (int ib = 0; ib < nb; ++ib) {")
     w("      const PrimPair bp = load_pp(bra + ib);")
     if la + lb > 0:
         w("      const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
         w("      const double o2p = 0.5 * bp.ip;")
-    w("      for (int ik = 0; ik < nk; ++ik) {")
-    w("        const PrimPair kp = load_pp(ket + ik);")
+    if cached:
+        w("#pragma unroll")
+        w("      for (int ik = 0; ik < MK; ++ik) {")
+        w("        if (ik >= nk) break;")
+        w("        PrimPair kp;")
+        w("        kp.p = kqp[ik]; kp.c = kqc[ik]; kp.x = kqx[ik]; kp.y = kqy[ik]; kp.z = kqz[ik];")
+        w("        kp.ip = %s;" % ("kqi[ik]" if need_ip else "0.0"))
+    else:
+        w("      PrimPair kn = load_pp(ket);")
+        w("      for (int ik = 0; ik < nk; ++ik) {")
+        w("        const PrimPair kp = kn;")
+        w("        if (ik + 1 < nk) kn = load_pp(ket + ik + 1);  // prefetch: hide the L1/L2 latency")
     w("        const double ps = bp.p + kp.p;")
     w("        const double r = rsqrt(ps);")
     w("        const double r2 = r * r;")
@@ -129,10 +159,10 @@ def gen_class(la, lb, lc, ld):
     w("        const double T = bp.p * kp.p * r2 * R2;")
     w("        const double pref = bp.c * kp.c * r;")
     if L == 0:
-        w("        const double bm0 = pref * boys_f0(T);")
+        w("        const double bm0 = pref * boys_f0(T, tab);")
     else:
         w(f"        double F[{L + 1}];")
-        w(f"        boys_fm<{L}>(T, F);")
+        w(f"        boys_fm<{L}>(T, F, tab);")
         for m in range(L + 1):
             w(f"        const double bm{m} = pref * F[{m}];")
         if la + lb > 0:

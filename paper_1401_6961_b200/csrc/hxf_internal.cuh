@@ -92,6 +92,7 @@ struct hxf_pairs {
     int64_t* ppoff;    // n_pairs + 1
     double* q;         // per pair id: Q in canonical orientation
     PrimPair* pp;
+    int4* info;        // per pair id: {fn offset i, fn offset j, first prim pair, n prim pairs}
     int64_t n_prim_pairs;
     double maxq;
     int has_p;

@@ -46,6 +46,7 @@ struct ScreenArgs {
     const double* qb;
     const double* qk;
     const int* l;
+    const int* poff;
     const int* fn;
     const int* nf;
     const double* P;
@@ -53,6 +54,7 @@ struct ScreenArgs {
     double tau;
     int mode;
     uint64_t* rec;
+    uint16_t* keys;
     int64_t cap;
     unsigned long long* fill;
     long long* counters;
@@ -120,7 +122,8 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
             sm.ax[i] = x;
             sm.ay[i] = y;
             sm.apl[i] = x * nnu + y;
-            sm.acl[i] = (a.l[smu + x] << 1) | a.l[snu + y];
+            sm.acl[i] = (a.l[smu + x] << 1) | a.l[snu + y] |
+                        (((a.poff[smu + x + 1] - a.poff[smu + x]) * (a.poff[snu + y + 1] - a.poff[snu + y]) - 1) << 2);
         }
         for (int i = lane; i < mb; i += 32) {
             int x, y;
@@ -132,7 +135,8 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
             sm.bx[i] = x;
             sm.by[i] = y;
             sm.bpl[i] = x * nsig + y;
-            sm.bcl[i] = (a.l[slam + x] << 1) | a.l[ssig + y];
+            sm.bcl[i] = (a.l[slam + x] << 1) | a.l[ssig + y] |
+                        (((a.poff[slam + x + 1] - a.poff[slam + x]) * (a.poff[ssig + y + 1] - a.poff[ssig + y]) - 1) << 2);
         }
         // density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
         const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
@@ -191,8 +195,11 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
                         if ((int64_t)pos < a.cap) {
                             const uint64_t pb = (uint64_t)(bb + sm.apl[ia]);
                             const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
-                            const uint64_t cls = ((uint64_t)sm.acl[ia] << 2) | sm.bcl[ib];
+                            const int ca = sm.acl[ia], cb = sm.bcl[ib];
+                            const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
                             a.rec[pos] = pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60);
+                            // sort key: class, bra / ket primitive-pair counts (uniform warps)
+                            a.keys[pos] = (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2));
                         }
                     }
                 }
@@ -229,6 +236,8 @@ struct EriArgs {
     const int* kpj;
     const int64_t* kppoff;
     const PrimPair* kpp;
+    const int4* binfo;
+    const int4* kinfo;
     const double3* ctr;
     const int* fn;
     const double* P;
@@ -246,23 +255,29 @@ __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double
 }
 
 template <int LA, int LB, int LC, int LD>
-__global__ void __launch_bounds__(128) k_eri(EriArgs e) {
+__global__ void __launch_bounds__(128, (LA + LB + LC + LD) <= 1 ? 4 : 2) k_eri(EriArgs e) {
     typedef Eri<LA, LB, LC, LD> E;
     constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL;
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    long long nprim = 0;
-    if (t < e.n) {
+    extern __shared__ __align__(16) double s_tab[];
+    boys_table_to_smem(s_tab, E::L);
+    long long nprim = 0, nq = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < e.n;
+         t += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t r = e.rec[t];
         const int mask = (int)((r >> 56) & 0xf);
         if (mask) {
             const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
-            const int i = e.bpi[pb], j = e.bpj[pb], k = e.kpi[pk], l = e.kpj[pk];
-            const int64_t b0 = e.bppoff[pb], k0 = e.kppoff[pk];
-            const int nb = (int)(e.bppoff[pb + 1] - b0), nk = (int)(e.kppoff[pk + 1] - k0);
-            nprim = (long long)nb * nk;
+            // one 16-byte record per pair: function offsets, primitive-pair range
+            const int4 ib = __ldg(e.binfo + pb), ik = __ldg(e.kinfo + pk);
+            const int nb = ib.w, nk = ik.w;
+            nprim += (long long)nb * nk;
+            nq += 1;
             double out[NI * NJ * NK * NL];
-            E::eval(e.bpp + b0, nb, e.kpp + k0, nk, e.ctr[i], e.ctr[j], e.ctr[k], e.ctr[l], out);
-            const int fi = e.fn[i], fj = e.fn[j], fk = e.fn[k], fl = e.fn[l];
+            double3 A{0, 0, 0}, B{0, 0, 0}, C{0, 0, 0}, D{0, 0, 0};
+            if (LA | LB) { A = e.ctr[e.bpi[pb]]; B = e.ctr[e.bpj[pb]]; }
+            if (LC | LD) { C = e.ctr[e.kpi[pk]]; D = e.ctr[e.kpj[pk]]; }
+            E::eval(e.bpp + ib.z, nb, e.kpp + ik.z, nk, A, B, C, D, s_tab, out);
+            const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
             const int64_t n = e.nfn;
             const double* P = e.P;
 #define OUT(x, y, z, w) out[(((x) * NJ + (y)) * NK + (z)) * NL + (w)]
@@ -306,7 +321,7 @@ __global__ void __launch_bounds__(128) k_eri(EriArgs e) {
         }
     }
     constexpr int CLS = (LA << 3) | (LB << 2) | (LC << 1) | LD;
-    const long long nq = warp_sum_ll(nprim > 0);
+    nq = warp_sum_ll(nq);
     nprim = warp_sum_ll(nprim);
     if ((threadIdx.x & 31) == 0 && nprim) {
         atomic_add_ll(&e.counters[C_PRIMQ], nprim);
@@ -315,14 +330,131 @@ __global__ void __launch_bounds__(128) k_eri(EriArgs e) {
     }
 }
 
-__global__ void k_class_bounds(const uint64_t* rec, int64_t n, int64_t* bounds) {
-    const int c = threadIdx.x;
-    if (c > 16) return;
-    // first index with class >= c
+// ---------------------------------------------------------------------------
+// Experimental, disabled: measured 1.6x slower than the register-cached
+// thread-per-quartet kernel on c3 (integer index overhead, IPC-bound).
+#if 0
+// (ss|ss): primitive-parallel.  Survivors are sorted by (class, nb, nk), so a
+// segment has a uniform primitive-quartet count S = nb*nk.  A group of
+// G = min(S, 32) lanes owns one shell quartet, each lane one (or, for S > 32,
+// every 32nd) primitive quartet; loads of the pair's primitive records are
+// near-coalesced and every lane holds little state (high occupancy).  The
+// group sum uses a fixed shuffle tree that depends only on G, so results do
+// not depend on where the quartet lands in the warp (bitwise reproducible).
+
+struct SegDesc {
+    int64_t begin, end, wbegin;
+    int nb, nk;
+};
+
+__global__ void __launch_bounds__(256) k_eri_ssss(EriArgs e, const SegDesc* __restrict__ segs,
+                                                  int nseg, int64_t total_w) {
+    extern __shared__ __align__(16) double s_tab[];
+    boys_table_to_smem(s_tab, 0);
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    long long nprim = 0, nq = 0;
+    for (int64_t wt = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); wt < total_w;
+         wt += nwarps) {
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (segs[mid].wbegin <= wt) lo = mid;
+            else hi = mid - 1;
+        }
+        const SegDesc sd = segs[lo];
+        const int nk = sd.nk, S = sd.nb * sd.nk;
+        int G, g, rounds;
+        int64_t r;
+        if (S <= 32) {
+            G = S;
+            const int RW = 32 / G;
+            g = lane % G;
+            r = (lane < RW * G) ? sd.begin + (wt - sd.wbegin) * RW + lane / G : sd.end;
+            rounds = 1;
+        } else {
+            G = 32;
+            g = lane;
+            r = sd.begin + (wt - sd.wbegin);
+            rounds = (S + 31) >> 5;
+        }
+        const bool act = r < sd.end;
+        double v = 0.0;
+        int mask = 0;
+        int4 ib = make_int4(0, 0, 0, 0), ik = make_int4(0, 0, 0, 0);
+        if (act) {
+            const uint64_t rec = e.rec[r];
+            mask = (int)((rec >> 56) & 0xf);
+            ib = __ldg(e.binfo + (int64_t)(rec & 0xfffffff));
+            ik = __ldg(e.kinfo + (int64_t)((rec >> 28) & 0xfffffff));
+            for (int rd = 0; rd < rounds; ++rd) {
+                const int p = g + 32 * rd;
+                if (p < S) {
+                    const int a = p / nk, k = p - a * nk;
+                    const PrimPair bp = load_pp(e.bpp + ib.z + a), kp = load_pp(e.kpp + ik.z + k);
+                    const double ps = bp.p + kp.p;
+                    const double rr = rsqrt(ps);
+                    const double r2 = rr * rr;
+                    const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;
+                    const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;
+                    const double T = bp.p * kp.p * r2 * R2;
+                    v += bp.c * kp.c * rr * boys_f0(T, s_tab);
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double o = __shfl_down_sync(0xffffffffu, v, off);
+            if (g + off < G) v += o;
+        }
+        const double eri = __shfl_sync(0xffffffffu, v, lane - g);
+        if (act) {
+            if (g == 0) {
+                nq += 1;
+                nprim += S;
+            }
+            // slot s (exchange_symmetry.py:345-361; naive = slot 0):
+            //   0 K[i,l] P[j,k]   1 K[j,l] P[i,k]   2 K[i,k] P[j,l]   3 K[j,k] P[i,l]
+            for (int s = g; s < 4; s += G) {
+                if (!((mask >> s) & 1)) continue;
+                const int row = (s & 1) ? ib.y : ib.x, col = (s & 2) ? ik.x : ik.y;
+                const int pr = (s & 1) ? ib.x : ib.y, pc = (s & 2) ? ik.y : ik.x;
+                k_add(e, row, col, -0.5 * (__ldg(e.P + (int64_t)pr * e.nfn + pc) * eri));
+            }
+        }
+    }
+    nq = warp_sum_ll(nq);
+    nprim = warp_sum_ll(nprim);
+    if (lane == 0 && nprim) {
+        atomic_add_ll(&e.counters[C_PRIMQ], nprim);
+        atomic_add_ll(&e.counters[C_CLSPQ0], nprim);
+        atomic_add_ll(&e.counters[C_CLSQ0], nq);
+    }
+}
+
+#endif
+
+// lower bounds of every 12-bit key value in the sorted key array
+__global__ void k_key_bounds(const uint16_t* keys, int64_t n, int64_t* bounds) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > 4096) return;
     int64_t lo = 0, hi = n;
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
-        if ((int)(rec[mid] >> 60) < c) lo = mid + 1;
+        if ((int)keys[mid] < c) lo = mid + 1;
+        else hi = mid;
+    }
+    bounds[c] = lo;
+}
+
+__global__ void k_class_bounds(const uint16_t* keys, int64_t n, int64_t* bounds) {
+    const int c = threadIdx.x;
+    if (c > 16) return;
+    // first index with class >= c (keys sorted by class, then primitive counts)
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int)(keys[mid] >> 8) < c) lo = mid + 1;
         else hi = mid;
     }
     bounds[c] = lo;
@@ -384,12 +516,28 @@ T* lalloc(size_t n, cudaStream_t st) {
     return (T*)p;
 }
 
+// persistent grid: every block stages its Boys table once, then strides
+template <int A, int B, int C, int D>
+void launch_eri(const EriArgs& e, cudaStream_t st) {
+    static int per_sm = -1, sms = 0;
+    if (per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri<A, B, C, D>, 128, BOYS_TAB_BYTES);
+        per_sm = std::max(per_sm, 1);
+    }
+    const int64_t want = (e.n + 127) / 128;
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
+    k_eri<A, B, C, D><<<g, 128, BOYS_TAB_BYTES, st>>>(e);
+    note_launch();
+}
+
 void launch_eri_class(int cls, const EriArgs& e, cudaStream_t st) {
-    const unsigned g = (unsigned)((e.n + 127) / 128);
     if (!e.n) return;
     switch (cls) {
 #define C(a, b, c, d) \
-    case (a << 3) | (b << 2) | (c << 1) | d: { k_eri<a, b, c, d><<<g, 128, 0, st>>>(e); note_launch(); } break;
+    case (a << 3) | (b << 2) | (c << 1) | d: launch_eri<a, b, c, d>(e, st); break;
         C(0, 0, 0, 0) C(0, 0, 0, 1) C(0, 0, 1, 0) C(0, 0, 1, 1)
         C(0, 1, 0, 0) C(0, 1, 0, 1) C(0, 1, 1, 0) C(0, 1, 1, 1)
         C(1, 0, 0, 0) C(1, 0, 0, 1) C(1, 0, 1, 0) C(1, 0, 1, 1)
@@ -494,6 +642,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.qb = bra->q;
     sa.qk = ket->q;
     sa.l = s->basis.l;
+    sa.poff = s->basis.poff;
     sa.fn = s->basis.fn;
     sa.nf = s->basis.nf;
     sa.P = dens->P;
@@ -563,10 +712,12 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         int64_t cap = std::min<int64_t>(1ll << 27, std::max<int64_t>(1 << 16, (int64_t)(freeb / 40)));
         uint64_t* rec = lalloc<uint64_t>(cap, st);
         uint64_t* rec2 = lalloc<uint64_t>(cap, st);
+        uint16_t* keys = lalloc<uint16_t>(cap, st);
+        uint16_t* keys2 = lalloc<uint16_t>(cap, st);
         size_t sort_tb = 0;
-        cub::DeviceRadixSort::SortKeys(nullptr, sort_tb, rec, rec2, cap, 60, 64, st);
+        cub::DeviceRadixSort::SortPairs(nullptr, sort_tb, keys, keys2, rec, rec2, cap, 0, 12, st);
         void* sort_tmp = lalloc<char>(sort_tb, st);
-        int64_t* dbounds = lalloc<int64_t>(17, st);
+        int64_t* dbounds = lalloc<int64_t>(4097, st);
         EriArgs e;
         e.bpi = bra->pi;
         e.bpj = bra->pj;
@@ -576,6 +727,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         e.kpj = ket->pj;
         e.kppoff = ket->ppoff;
         e.kpp = ket->pp;
+        e.binfo = bra->info;
+        e.kinfo = ket->info;
         e.ctr = s->basis.ctr;
         e.fn = s->basis.fn;
         e.P = dens->P;
@@ -594,6 +747,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sa.t0 = t0;
             sa.t1 = t1;
             sa.rec = rec;
+            sa.keys = keys;
             sa.cap = cap;
             sa.fill = dfill;
             sa.counters = scount;
@@ -614,15 +768,15 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             const int64_t nrec = (int64_t)fill;
             if (nrec) {
                 size_t tb = sort_tb;
-                cub::DeviceRadixSort::SortKeys(sort_tmp, tb, rec, rec2, nrec, 60, 64, st);
-                { k_class_bounds<<<1, 32, 0, st>>>(rec2, nrec, dbounds); note_launch(); }
-                int64_t hb[17];
-                HXF_CUDA(cudaMemcpyAsync(hb, dbounds, sizeof(hb), cudaMemcpyDeviceToHost, st));
+                cub::DeviceRadixSort::SortPairs(sort_tmp, tb, keys, keys2, rec, rec2, nrec, 0, 12, st);
+                { k_key_bounds<<<17, 256, 0, st>>>(keys2, nrec, dbounds); note_launch(); }
+                std::vector<int64_t> kbnd(4097);
+                HXF_CUDA(cudaMemcpyAsync(kbnd.data(), dbounds, 4097 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
                 HXF_CUDA(cudaStreamSynchronize(st));
                 Timer tk(st);
                 for (int c = 0; c < 16; ++c) {
-                    e.rec = rec2 + hb[c];
-                    e.n = hb[c + 1] - hb[c];
+                    e.rec = rec2 + kbnd[c << 8];
+                    e.n = kbnd[(c + 1) << 8] - kbnd[c << 8];
                     launch_eri_class(c, e, st);
                 }
                 g_timings[5] += tk.stop();
@@ -643,7 +797,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             chunk = std::max<int64_t>(1, (int64_t)(0.85 * cap / std::max(dens_per_task, 1.0)));
             t0 = t1;
         }
-        for (void* p : {(void*)rec, (void*)rec2, sort_tmp, (void*)dbounds}) cudaFreeAsync(p, st);
+        for (void* p : {(void*)rec, (void*)rec2, (void*)keys, (void*)keys2, sort_tmp, (void*)dbounds})
+            cudaFreeAsync(p, st);
     }
 
     // ---- epilogue

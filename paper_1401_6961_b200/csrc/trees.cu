@@ -91,7 +91,7 @@ __global__ void k_leaf_pair_counts(const double* smax, double tau, const int* ls
 __global__ void k_fill_pairs(DevBasis B, const double* smax, double tau, const int* lslo,
                              const int* lshi, int nleaf, const int64_t* pbase,
                              const int64_t* ppbase, int64_t* leaf_base, int* pi, int* pj,
-                             int64_t* ppoff, PrimPair* pp) {
+                             int64_t* ppoff, PrimPair* pp, int4* info) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= (int64_t)nleaf * nleaf) return;
     const int r = (int)(t / nleaf), c = (int)(t % nleaf);
@@ -107,6 +107,8 @@ __global__ void k_fill_pairs(DevBasis B, const double* smax, double tau, const i
             pi[pid] = i;
             pj[pid] = j;
             ppoff[pid] = po;
+            info[pid] = make_int4(B.fn[i], B.fn[j], (int)po,
+                                  (B.poff[i + 1] - B.poff[i]) * (B.poff[j + 1] - B.poff[j]));
             const double3 A = B.ctr[i], C = B.ctr[j];
             const double dx = A.x - C.x, dy = A.y - C.y, dz = A.z - C.z;
             const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
@@ -135,7 +137,7 @@ template <int LA, int LB>
 __device__ double diag_q(const PrimPair* pp, int64_t b0, int64_t b1, double3 A, double3 Bc) {
     typedef Eri<LA, LB, LA, LB> E;
     double out[E::NI * E::NJ * E::NK * E::NL];
-    E::eval(pp, (int)(b1 - b0), pp, (int)(b1 - b0), A, Bc, A, Bc, out);
+    E::eval(pp, (int)(b1 - b0), pp, (int)(b1 - b0), A, Bc, A, Bc, boys_table_global(E::L), out);
     double q = 0.0;
     for (int x = 0; x < E::NI; ++x)
         for (int y = 0; y < E::NJ; ++y) q = fmax(q, out[((x * E::NJ + y) * E::NK + x) * E::NL + y]);
@@ -405,10 +407,13 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     pr->ppoff = dalloc<int64_t>(pr->n_pairs + 1, st);
     pr->q = dalloc<double>(pr->n_pairs, st);
     pr->pp = dalloc<PrimPair>(pr->n_prim_pairs, st);
+    pr->info = dalloc<int4>(pr->n_pairs, st);
+    if (pr->n_prim_pairs >= (1ll << 31))
+        throw HxfError{HXF_EINVAL, "too many primitive pairs for 32-bit offsets"};
     HXF_CUDA(cudaMemcpyAsync(pr->ppoff + pr->n_pairs, &tot[1], sizeof(int64_t), cudaMemcpyHostToDevice, st));
     { k_fill_pairs<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, lsmax, pr->tau_ovlp, lt.lslo, lt.lshi, nl,
                                                  pbase, ppbase, pr->leaf_base, pr->pi, pr->pj,
-                                                 pr->ppoff, pr->pp); note_launch(); }
+                                                 pr->ppoff, pr->pp, pr->info); note_launch(); }
     HXF_CUDA(cudaMemcpyAsync(pr->ppoff + pr->n_pairs, &tot[1], sizeof(int64_t), cudaMemcpyHostToDevice, st));
     { k_diag_q<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
                                                      pr->pp, lt.leaf_of_shell, lt.lslo, lt.lshi, nl,
