@@ -225,6 +225,270 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Hierarchical leaf screen.  Same decisions as k_screen, fewer tests:
+// for a bra pair a and a ket row shell k (the "triple"), every ket pair
+// b = (k, l) satisfies bound_g(a,b) = fl(fl(f_a p_g) f_b) <= fl(fl(f_a Pmax_g) Fmax_k)
+// because IEEE rounding is monotone.  If that upper bound is <= tau(1 - 1e-12)
+// for every live slot, the whole row is culled without per-quartet tests
+// (and no quartet in it can be a tie); its culled count is exact and its
+// ledger contribution is the row sum (within 1e-15 relative of the
+// per-quartet sum).  Passing triples go to a per-warp queue whose entries
+// are expanded lane-parallel into exact per-quartet tests.
+
+template <bool SYM>
+struct Smem2 {
+    static constexpr int NG = SYM ? 4 : 1;
+    double fa[MAXP], sa[MAXP], fb[MAXP], sb[MAXP];
+    double pm[NG][MAXP];
+    double w[SYM ? 2 : 1][SYM ? MAXP : 1];    // g2/g3 row ledgers: sum_{b in L_k} pm_g[r, l(b)] sb[b]
+    double fbmax[MAXS], sbsum[MAXS];
+    double pmx[SYM ? 2 : 1][SYM ? MAXS : 1];  // g2/g3: max over l of pm_g[r, l]
+    unsigned char ax[MAXP], ay[MAXP], acl[MAXP], bx[MAXP], by[MAXP], bcl[MAXP];
+    unsigned short apl[MAXP], bpl[MAXP];
+    unsigned char bstart[MAXS], nl[MAXS];
+    unsigned short queue[64];
+};
+
+template <bool SYM>
+constexpr int screen2_warps() { return SYM ? 3 : 6; }  // static smem <= 48 KB
+
+__device__ __forceinline__ int fdiv(int a, int n, float inv) {
+    return __float2int_rz(((float)a + 0.5f) * inv);  // exact for a < 2^20, n <= 32
+}
+
+template <bool SYM, bool EMIT>
+__global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArgs a) {
+    constexpr int NW = screen2_warps<SYM>();
+    __shared__ Smem2<SYM> sm_all[NW];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Smem2<SYM>& sm = sm_all[wid];
+    const int64_t gw = blockIdx.x * (int64_t)NW + wid;
+    const int64_t Wt = (int64_t)gridDim.x * NW;
+    long long n_eri = 0, n_cull = 0, n_tie = 0;
+    double ledger = 0.0;
+    const bool schwarz = a.mode == HXF_MODE_SCHWARZ;
+    const double tau = a.tau;
+    const double tau_skip = tau * (1.0 - 1e-12);
+    for (int64_t t = a.t0 + gw; t < a.t1; t += Wt) {
+        const uint64_t task = a.tasks[t];
+        const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
+                  sig = (task >> 45) & 0x7fff;
+        const int live = SYM ? (int)(task >> 60) : 1;
+        const int smu = a.lslo[mu], snu = a.lslo[nu], slam = a.lslo[lam], ssig = a.lslo[sig];
+        const int nmu = a.lshi[mu] - smu, nnu = a.lshi[nu] - snu, nlam = a.lshi[lam] - slam,
+                  nsig = a.lshi[sig] - ssig;
+        const int64_t bb = a.bra_base[(int64_t)mu * a.nleaf + nu];
+        const int64_t kb = a.ket_base[(int64_t)lam * a.nleaf + sig];
+        const bool bdiag = SYM && mu == nu, kdiag = SYM && lam == sig;
+        const int ma = bdiag ? nmu * (nmu + 1) / 2 : nmu * nnu;
+        const int mb = kdiag ? nlam * (nlam + 1) / 2 : nlam * nsig;
+        const float inv_nnu = 1.0f / nnu, inv_nsig = 1.0f / nsig, inv_nlam = 1.0f / nlam;
+        // ---- stage pair factors
+        for (int i = lane; i < ma; i += 32) {
+            int x, y;
+            if (bdiag) tri_decode(i, nmu, &x, &y);
+            else { x = fdiv(i, nnu, inv_nnu); y = i - x * nnu; }
+            const double q = a.qb[bb + x * nnu + y];
+            sm.sa[i] = sqrt(q);
+            sm.fa[i] = schwarz ? sm.sa[i] : q;
+            sm.ax[i] = x;
+            sm.ay[i] = y;
+            sm.apl[i] = x * nnu + y;
+            sm.acl[i] = (a.l[smu + x] << 1) | a.l[snu + y] |
+                        (((a.poff[smu + x + 1] - a.poff[smu + x]) * (a.poff[snu + y + 1] - a.poff[snu + y]) - 1) << 2);
+        }
+        for (int i = lane; i < mb; i += 32) {
+            int x, y;
+            if (kdiag) tri_decode(i, nlam, &x, &y);
+            else { x = fdiv(i, nsig, inv_nsig); y = i - x * nsig; }
+            const double q = a.qk[kb + x * nsig + y];
+            sm.sb[i] = sqrt(q);
+            sm.fb[i] = schwarz ? sm.sb[i] : q;
+            sm.bx[i] = x;
+            sm.by[i] = y;
+            sm.bpl[i] = x * nsig + y;
+            sm.bcl[i] = (a.l[slam + x] << 1) | a.l[ssig + y] |
+                        (((a.poff[slam + x + 1] - a.poff[slam + x]) * (a.poff[ssig + y + 1] - a.poff[ssig + y]) - 1) << 2);
+        }
+        // density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
+        const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
+        const int cs[4] = {slam, slam, ssig, ssig}, cn[4] = {nlam, nlam, nsig, nsig};
+#pragma unroll
+        for (int g = 0; g < Smem2<SYM>::NG; ++g) {
+            if (!((live >> g) & 1)) continue;
+            const float inv = 1.0f / cn[g];
+            for (int i = lane; i < rn[g] * cn[g]; i += 32) {
+                const int x = fdiv(i, cn[g], inv), y = i - x * cn[g];
+                sm.pm[g][i] = pblock_max(a, rs[g] + x, cs[g] + y);
+            }
+        }
+        // ket rows: L_k = ket pairs with row shell k (contiguous in the pair order)
+        if (lane < nlam) {
+            const int k = lane;
+            const int st = kdiag ? k * nlam - k * (k - 1) / 2 : k * nsig;
+            const int n = kdiag ? nlam - k : nsig;
+            sm.bstart[k] = st;
+            sm.nl[k] = n;
+        }
+        __syncwarp();
+        if (lane < nlam) {
+            const int k = lane, st = sm.bstart[k], n = sm.nl[k];
+            double fm = 0.0, ss = 0.0;
+            for (int b = st; b < st + n; ++b) {
+                fm = fmax(fm, sm.fb[b]);
+                ss += sm.sb[b];
+            }
+            sm.fbmax[k] = fm;
+            sm.sbsum[k] = ss;
+        }
+        if (SYM) {
+            // g2/g3: row maxima over l, and row ledgers per (r, k)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int g = 2 + h;
+                if (!((live >> g) & 1)) continue;
+                for (int r = lane; r < rn[g]; r += 32) {
+                    double m = 0.0;
+                    for (int l = 0; l < nsig; ++l) m = fmax(m, sm.pm[g][r * nsig + l]);
+                    sm.pmx[h][r] = m;
+                }
+                for (int i = lane; i < rn[g] * nlam; i += 32) {
+                    const int r = fdiv(i, nlam, inv_nlam), k = i - r * nlam;
+                    const int st = kdiag ? k * nlam - k * (k - 1) / 2 : k * nsig;
+                    const int n = kdiag ? nlam - k : nsig;
+                    double s = 0.0;
+                    for (int b = st; b < st + n; ++b) s += sm.pm[g][r * nsig + sm.by[b]] * sm.sb[b];
+                    sm.w[h][i] = s;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- phase 1: triples (a, k); phase 2: queued triples x l, exact tests
+        int qn = 0;
+        const int ntrip = ma * nlam;
+        const int Wl = kdiag ? nlam : nsig;       // lanes per queued triple
+        const int per = 32 / Wl;                  // triples per phase-2 pass
+        const int my_e = lane / Wl, my_l = lane - my_e * Wl;
+        auto flush = [&](int count) {
+            for (int e0 = 0; e0 < count; e0 += per) {
+                const int e = e0 + my_e;
+                bool keep_any = false;
+                int mask = 0, ia = 0, ib = 0;
+                if (my_e < per && e < count) {
+                    const int ent = sm.queue[e];
+                    ia = ent >> 4;
+                    const int k = ent & 15;
+                    if (my_l < sm.nl[k]) {
+                        ib = sm.bstart[k] + my_l;
+                        const double fa = sm.fa[ia], fb = sm.fb[ib];
+                        const int x = sm.ax[ia], y = sm.ay[ia], z = sm.bx[ib], w = sm.by[ib];
+                        const int rowv[4] = {y, x, y, x}, colv[4] = {z, z, w, w};
+#pragma unroll
+                        for (int g = 0; g < Smem2<SYM>::NG; ++g) {
+                            if (!((live >> g) & 1)) continue;
+                            const double pm = sm.pm[g][rowv[g] * cn[g] + colv[g]];
+                            const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
+                            n_tie += tau > 0.0 && fabs(bound - tau) <= 1e-12 * tau;
+                            if (bound > tau) {
+                                keep_any = true;
+                                mask |= 1 << g;
+                            } else {
+                                ++n_cull;
+                                ledger += schwarz ? bound : __dmul_rn(__dmul_rn(sm.sa[ia], pm), sm.sb[ib]);
+                            }
+                        }
+                        if (SYM) {
+                            const bool ij = !(bdiag && x == y), kl = !(kdiag && z == w);
+                            if (!ij) mask &= ~0xa;
+                            if (!kl) mask &= ~0xc;
+                        }
+                        n_eri += keep_any;
+                    }
+                }
+                if (EMIT) {
+                    const unsigned bal = __ballot_sync(0xffffffffu, keep_any);
+                    if (bal) {
+                        unsigned long long base = 0;
+                        if (lane == 0) base = atomicAdd(a.fill, (unsigned long long)__popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (keep_any) {
+                            const uint64_t pos = base + __popc(bal & ((1u << lane) - 1u));
+                            if ((int64_t)pos < a.cap) {
+                                const uint64_t pb = (uint64_t)(bb + sm.apl[ia]);
+                                const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
+                                const int ca = sm.acl[ia], cb = sm.bcl[ib];
+                                const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
+                                a.rec[pos] = pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60);
+                                a.keys[pos] = (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2));
+                            }
+                        }
+                    }
+                }
+            }
+        };
+        for (int t0 = 0; t0 < ntrip; t0 += 32) {
+            const int tt = t0 + lane;
+            bool pass = false;
+            int ia = 0, k = 0;
+            if (tt < ntrip) {
+                ia = fdiv(tt, nlam, inv_nlam);
+                k = tt - ia * nlam;
+                const double fa = sm.fa[ia], sa = sm.sa[ia], fm = sm.fbmax[k];
+                const int x = sm.ax[ia], y = sm.ay[ia];
+                double lsum = 0.0;
+                int ncul = 0;
+#pragma unroll
+                for (int g = 0; g < Smem2<SYM>::NG; ++g) {
+                    if (!((live >> g) & 1)) continue;
+                    double ub, led;
+                    if (g < 2) {
+                        const double pm = sm.pm[g][(g == 0 ? y : x) * nlam + k];
+                        ub = __dmul_rn(__dmul_rn(fa, pm), fm);
+                        led = __dmul_rn(sa, pm) * sm.sbsum[k];
+                    } else {
+                        const int r = (g == 2) ? y : x;
+                        ub = __dmul_rn(__dmul_rn(fa, sm.pmx[g - 2][r]), fm);
+                        led = sa * sm.w[g - 2][r * nlam + k];
+                    }
+                    if (!(ub <= tau_skip)) pass = true;
+                    lsum += led;
+                    ncul += sm.nl[k];
+                }
+                if (!pass) {
+                    n_cull += ncul;
+                    ledger += lsum;
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, pass);
+            if (pass) sm.queue[qn + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)((ia << 4) | k);
+            qn += __popc(bal);
+            __syncwarp();
+            if (qn >= 32) {
+                flush(qn);
+                qn = 0;
+                __syncwarp();
+            }
+        }
+        if (qn) flush(qn);
+        __syncwarp();
+    }
+    n_eri = warp_sum_ll(n_eri);
+    n_cull = warp_sum_ll(n_cull);
+    n_tie = warp_sum_ll(n_tie);
+    ledger = warp_sum(ledger);
+    if (lane == 0) {
+        if (n_eri) atomic_add_ll(&a.counters[C_ERIQ], n_eri);
+        if (n_cull) atomic_add_ll(&a.counters[C_CULL_LEAF], n_cull);
+        if (n_tie) atomic_add_ll(&a.counters[C_TIE_LEAF], n_tie);
+        if (ledger != 0.0) {
+            unsigned long long limb[LEDGER_LIMBS];
+            fx_from_double<LEDGER_LIMBS>(0.5 * ledger, LEDGER_SCALE, limb);
+            fx_atomic_add<LEDGER_LIMBS>(a.ledger, limb);
+        }
+    }
+}
+
 struct EriArgs {
     const uint64_t* rec;
     int64_t n;
@@ -652,8 +916,11 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
 
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device);
+    // fixed grid (depends only on the device): the task -> warp assignment, and
+    // so every per-warp ledger partial, is reproducible
+    const int sw = sym ? SCREEN_WARPS : screen2_warps<false>();
     const unsigned screen_grid = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>((tr.n_leaf + SCREEN_WARPS - 1) / SCREEN_WARPS, (int64_t)dev_sms * 12));
+        1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * (sym ? 12 : 8)));
 
     // fixed-point scale for K: |K| <= 1/2 sum|P| max|(ij|kl)| <= 1/2 n ||P||_F maxQ
     const double kb = 2.0 * s->nfn * std::max(dens->frob, 1e-300) *
@@ -692,8 +959,9 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sa.fill = dfill;
             sa.counters = scount;
             sa.ledger = sledger;
+            // fourfold: the flat screen is faster (the triple bound is weaker with 4 slots)
             if (sym) { k_screen<true, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
-            else { k_screen<false, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
+            else { k_screen2<false, false><<<screen_grid, sw * 32, 0, st>>>(sa); note_launch(); }
             HXF_CUDA(cudaGetLastError());
             long long c2[C_NCOUNTERS];
             unsigned long long l2[LEDGER_LIMBS];
@@ -753,7 +1021,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sa.counters = scount;
             sa.ledger = sledger;
             if (sym) { k_screen<true, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
-            else { k_screen<false, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
+            else { k_screen2<false, true><<<screen_grid, sw * 32, 0, st>>>(sa); note_launch(); }
             HXF_CUDA(cudaGetLastError());
             unsigned long long fill = 0;
             HXF_CUDA(cudaMemcpyAsync(&fill, dfill, sizeof(fill), cudaMemcpyDeviceToHost, st));
