@@ -117,8 +117,8 @@ int hxf_system_create(int device, int ns, const double* centers, const int* l, c
         s->n_leaves = s->h_off[D + 1] - s->h_off[D];
         for (int k = s->h_off[D]; k < s->h_off[D + 1]; ++k) {
             s->h_leaf_id[k] = k - s->h_off[D];
-            if (s->h_shi[k] - s->h_slo[k] > 12)
-                throw HxfError{HXF_EINVAL, "leaf spans hold at most 12 shells on the device path"};
+            if (s->h_shi[k] - s->h_slo[k] > 10)
+                throw HxfError{HXF_EINVAL, "leaf spans hold at most 10 shells on the device path"};
         }
         for (int L = D - 1; L >= 0; --L)
             for (int k = s->h_off[L]; k < s->h_off[L + 1]; ++k)
@@ -198,7 +198,7 @@ void hxf_pairs_destroy(hxf_pairs* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     void* ptrs[] = {p->norm, p->rowsum, p->colsum, p->smax, p->leaf_base, p->pi,
-                    p->pj,   p->ppoff,  p->q,      p->pp,       p->info};
+                    p->pj,   p->ppoff,  p->q,      p->pp,       p->info, p->sq, p->meta};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     delete p;
@@ -275,6 +275,7 @@ void hxf_density_destroy(hxf_density* d) {
     cudaSetDevice(d->device);
     if (d->P) cudaFree(d->P);
     if (d->norm) cudaFree(d->norm);
+    if (d->pmax) cudaFree(d->pmax);
     delete d;
 }
 

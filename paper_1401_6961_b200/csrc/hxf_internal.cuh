@@ -91,6 +91,8 @@ struct hxf_pairs {
     int* pj;
     int64_t* ppoff;    // n_pairs + 1
     double* q;         // per pair id: Q in canonical orientation
+    double* sq;        // per pair id: sqrt(Q) (correctly rounded, = math.sqrt)
+    uint8_t* meta;     // per pair id: (l_i << 1 | l_j) | (n prim pairs - 1) << 2
     PrimPair* pp;
     int4* info;        // per pair id: {fn offset i, fn offset j, first prim pair, n prim pairs}
     int64_t n_prim_pairs;
@@ -106,6 +108,7 @@ struct hxf_density {
     double zero_drop;
     double frob;       // root norm
     double maxabs;
+    double* pmax;      // n_shells^2: max |P| over each shell-pair function block
 };
 
 // ---------------------------------------------------------------- helpers

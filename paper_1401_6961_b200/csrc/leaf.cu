@@ -29,7 +29,7 @@
 #include "eri_classes.cuh"
 #include "traverse.cuh"
 
-#define MAXS 12
+#define MAXS 10  // shells per leaf span (leaf_size <= 10 functions; checked in api.cu)
 #define MAXP (MAXS * MAXS)
 #define SCREEN_WARPS 4
 
@@ -47,6 +47,12 @@ struct ScreenArgs {
     const double* qk;
     const int* l;
     const int* poff;
+    const double* sqb;        // sqrt(Q) per bra / ket pair id
+    const double* sqk;
+    const uint8_t* metab;     // class bits | primitive count per pair id
+    const uint8_t* metak;
+    const double* pmax;       // shell-level max |P| (n_shells^2)
+    int ns;
     const int* fn;
     const int* nf;
     const double* P;
@@ -112,31 +118,32 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
         const bool bdiag = SYM && mu == nu, kdiag = SYM && lam == sig;
         const int ma = bdiag ? nmu * (nmu + 1) / 2 : nmu * nnu;
         const int mb = kdiag ? nlam * (nlam + 1) / 2 : nlam * nsig;
+        const float inv_nnu = 1.0f / nnu, inv_nsig = 1.0f / nsig, inv_mb = 1.0f / mb;
         for (int i = lane; i < ma; i += 32) {
             int x, y;
             if (bdiag) tri_decode(i, nmu, &x, &y);
-            else { x = i / nnu; y = i - x * nnu; }
-            const double q = a.qb[bb + x * nnu + y];
-            sm.sa[i] = sqrt(q);
-            sm.fa[i] = schwarz ? sm.sa[i] : q;
+            else { x = __float2int_rz(((float)i + 0.5f) * inv_nnu); y = i - x * nnu; }
+            const int64_t pid = bb + x * nnu + y;
+            const double sq = a.sqb[pid];
+            sm.sa[i] = sq;
+            sm.fa[i] = schwarz ? sq : a.qb[pid];
             sm.ax[i] = x;
             sm.ay[i] = y;
             sm.apl[i] = x * nnu + y;
-            sm.acl[i] = (a.l[smu + x] << 1) | a.l[snu + y] |
-                        (((a.poff[smu + x + 1] - a.poff[smu + x]) * (a.poff[snu + y + 1] - a.poff[snu + y]) - 1) << 2);
+            sm.acl[i] = a.metab[pid];
         }
         for (int i = lane; i < mb; i += 32) {
             int x, y;
             if (kdiag) tri_decode(i, nlam, &x, &y);
-            else { x = i / nsig; y = i - x * nsig; }
-            const double q = a.qk[kb + x * nsig + y];
-            sm.sb[i] = sqrt(q);
-            sm.fb[i] = schwarz ? sm.sb[i] : q;
+            else { x = __float2int_rz(((float)i + 0.5f) * inv_nsig); y = i - x * nsig; }
+            const int64_t pid = kb + x * nsig + y;
+            const double sq = a.sqk[pid];
+            sm.sb[i] = sq;
+            sm.fb[i] = schwarz ? sq : a.qk[pid];
             sm.bx[i] = x;
             sm.by[i] = y;
             sm.bpl[i] = x * nsig + y;
-            sm.bcl[i] = (a.l[slam + x] << 1) | a.l[ssig + y] |
-                        (((a.poff[slam + x + 1] - a.poff[slam + x]) * (a.poff[ssig + y + 1] - a.poff[ssig + y]) - 1) << 2);
+            sm.bcl[i] = a.metak[pid];
         }
         // density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
         const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
@@ -144,20 +151,22 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
             if (!((live >> g) & 1)) continue;
+            const float inv = 1.0f / cn[g];
             for (int i = lane; i < rn[g] * cn[g]; i += 32) {
-                const int x = i / cn[g], y = i - x * cn[g];
-                sm.pm[g][i] = pblock_max(a, rs[g] + x, cs[g] + y);
+                const int x = __float2int_rz(((float)i + 0.5f) * inv), y = i - x * cn[g];
+                sm.pm[g][i] = a.pmax[(int64_t)(rs[g] + x) * a.ns + cs[g] + y];
             }
         }
         __syncwarp();
         const int total = ma * mb;
+        const double tie_lo = a.tau * (1.0 - 1e-12), tie_hi = a.tau * (1.0 + 1e-12);
         for (int q0 = 0; q0 < total; q0 += 32) {
             const int q = q0 + lane;
             bool keep_any = false;
             int mask = 0;
             int ia = 0, ib = 0;
             if (q < total) {
-                ia = q / mb;
+                ia = __float2int_rz(((float)q + 0.5f) * inv_mb);
                 ib = q - ia * mb;
                 const double fa = sm.fa[ia], fb = sm.fb[ib];
                 const int x = sm.ax[ia], y = sm.ay[ia], z = sm.bx[ib], w = sm.by[ib];
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
                     if (!((live >> g) & 1)) continue;
                     const double pm = sm.pm[g][rowv[g] * cn[g] + colv[g]];
                     const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
-                    n_tie += a.tau > 0.0 && fabs(bound - a.tau) <= 1e-12 * a.tau;
+                    n_tie += bound >= tie_lo && bound <= tie_hi && a.tau > 0.0;
                     if (bound > a.tau) {
                         keep_any = true;
                         mask |= 1 << g;
@@ -243,7 +252,7 @@ struct Smem2 {
     double pm[NG][MAXP];
     double w[SYM ? 2 : 1][SYM ? MAXP : 1];    // g2/g3 row ledgers: sum_{b in L_k} pm_g[r, l(b)] sb[b]
     double fbmax[MAXS], sbsum[MAXS];
-    double pmx[SYM ? 2 : 1][SYM ? MAXS : 1];  // g2/g3: max over l of pm_g[r, l]
+    double z[SYM ? 2 : 1][SYM ? MAXP : 1];    // g2/g3: max_{b in L_k} pm_g[r, l(b)] f_b
     unsigned char ax[MAXP], ay[MAXP], acl[MAXP], bx[MAXP], by[MAXP], bcl[MAXP];
     unsigned short apl[MAXP], bpl[MAXP];
     unsigned char bstart[MAXS], nl[MAXS];
@@ -251,7 +260,7 @@ struct Smem2 {
 };
 
 template <bool SYM>
-constexpr int screen2_warps() { return SYM ? 3 : 6; }  // static smem <= 48 KB
+constexpr int screen2_warps() { return SYM ? 4 : 8; }  // static smem <= 48 KB
 
 __device__ __forceinline__ int fdiv(int a, int n, float inv) {
     return __float2int_rz(((float)a + 0.5f) * inv);  // exact for a < 2^20, n <= 32
@@ -289,27 +298,27 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
             int x, y;
             if (bdiag) tri_decode(i, nmu, &x, &y);
             else { x = fdiv(i, nnu, inv_nnu); y = i - x * nnu; }
-            const double q = a.qb[bb + x * nnu + y];
-            sm.sa[i] = sqrt(q);
-            sm.fa[i] = schwarz ? sm.sa[i] : q;
+            const int64_t pid = bb + x * nnu + y;
+            const double sq = a.sqb[pid];
+            sm.sa[i] = sq;
+            sm.fa[i] = schwarz ? sq : a.qb[pid];
             sm.ax[i] = x;
             sm.ay[i] = y;
             sm.apl[i] = x * nnu + y;
-            sm.acl[i] = (a.l[smu + x] << 1) | a.l[snu + y] |
-                        (((a.poff[smu + x + 1] - a.poff[smu + x]) * (a.poff[snu + y + 1] - a.poff[snu + y]) - 1) << 2);
+            sm.acl[i] = a.metab[pid];
         }
         for (int i = lane; i < mb; i += 32) {
             int x, y;
             if (kdiag) tri_decode(i, nlam, &x, &y);
             else { x = fdiv(i, nsig, inv_nsig); y = i - x * nsig; }
-            const double q = a.qk[kb + x * nsig + y];
-            sm.sb[i] = sqrt(q);
-            sm.fb[i] = schwarz ? sm.sb[i] : q;
+            const int64_t pid = kb + x * nsig + y;
+            const double sq = a.sqk[pid];
+            sm.sb[i] = sq;
+            sm.fb[i] = schwarz ? sq : a.qk[pid];
             sm.bx[i] = x;
             sm.by[i] = y;
             sm.bpl[i] = x * nsig + y;
-            sm.bcl[i] = (a.l[slam + x] << 1) | a.l[ssig + y] |
-                        (((a.poff[slam + x + 1] - a.poff[slam + x]) * (a.poff[ssig + y + 1] - a.poff[ssig + y]) - 1) << 2);
+            sm.bcl[i] = a.metak[pid];
         }
         // density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
         const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
             const float inv = 1.0f / cn[g];
             for (int i = lane; i < rn[g] * cn[g]; i += 32) {
                 const int x = fdiv(i, cn[g], inv), y = i - x * cn[g];
-                sm.pm[g][i] = pblock_max(a, rs[g] + x, cs[g] + y);
+                sm.pm[g][i] = a.pmax[(int64_t)(rs[g] + x) * a.ns + cs[g] + y];
             }
         }
         // ket rows: L_k = ket pairs with row shell k (contiguous in the pair order)
@@ -348,18 +357,18 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
             for (int h = 0; h < 2; ++h) {
                 const int g = 2 + h;
                 if (!((live >> g) & 1)) continue;
-                for (int r = lane; r < rn[g]; r += 32) {
-                    double m = 0.0;
-                    for (int l = 0; l < nsig; ++l) m = fmax(m, sm.pm[g][r * nsig + l]);
-                    sm.pmx[h][r] = m;
-                }
                 for (int i = lane; i < rn[g] * nlam; i += 32) {
                     const int r = fdiv(i, nlam, inv_nlam), k = i - r * nlam;
                     const int st = kdiag ? k * nlam - k * (k - 1) / 2 : k * nsig;
                     const int n = kdiag ? nlam - k : nsig;
-                    double s = 0.0;
-                    for (int b = st; b < st + n; ++b) s += sm.pm[g][r * nsig + sm.by[b]] * sm.sb[b];
+                    double s = 0.0, zm = 0.0;
+                    for (int b = st; b < st + n; ++b) {
+                        const double pv = sm.pm[g][r * nsig + sm.by[b]];
+                        s += pv * sm.sb[b];
+                        zm = fmax(zm, pv * sm.fb[b]);
+                    }
                     sm.w[h][i] = s;
+                    sm.z[h][i] = zm;
                 }
             }
         }
@@ -447,8 +456,10 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
                         ub = __dmul_rn(__dmul_rn(fa, pm), fm);
                         led = __dmul_rn(sa, pm) * sm.sbsum[k];
                     } else {
+                        // fl(fl(f_a p) f_b) <= f_a max(p f_b) (1 + 4 eps): the skip
+                        // threshold tau (1 - 1e-12) leaves far more slack than that
                         const int r = (g == 2) ? y : x;
-                        ub = __dmul_rn(__dmul_rn(fa, sm.pmx[g - 2][r]), fm);
+                        ub = fa * sm.z[g - 2][r * nlam + k] * (1.0 + 1e-15);
                         led = sa * sm.w[g - 2][r * nlam + k];
                     }
                     if (!(ub <= tau_skip)) pass = true;
@@ -907,6 +918,12 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.qk = ket->q;
     sa.l = s->basis.l;
     sa.poff = s->basis.poff;
+    sa.sqb = bra->sq;
+    sa.sqk = ket->sq;
+    sa.metab = bra->meta;
+    sa.metak = ket->meta;
+    sa.pmax = dens->pmax;
+    sa.ns = s->ns;
     sa.fn = s->basis.fn;
     sa.nf = s->basis.nf;
     sa.P = dens->P;
@@ -918,9 +935,22 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device);
     // fixed grid (depends only on the device): the task -> warp assignment, and
     // so every per-warp ledger partial, is reproducible
-    const int sw = sym ? SCREEN_WARPS : screen2_warps<false>();
+    // HXF_SCREEN=flat selects the per-quartet screen (A/B reference)
+    const char* sv = getenv("HXF_SCREEN");
+    const bool flat = sv && !strcmp(sv, "flat");
+    const int sw = flat ? SCREEN_WARPS : (sym ? screen2_warps<true>() : screen2_warps<false>());
     const unsigned screen_grid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * (sym ? 12 : 8)));
+    auto launch_screen = [&](bool emit) {
+        if (flat) {
+            if (sym) { if (emit) k_screen<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
+            else { if (emit) k_screen<false, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<false, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
+        } else {
+            if (sym) { if (emit) k_screen2<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen2<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
+            else { if (emit) k_screen2<false, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen2<false, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
+        }
+        note_launch();
+    };
 
     // fixed-point scale for K: |K| <= 1/2 sum|P| max|(ij|kl)| <= 1/2 n ||P||_F maxQ
     const double kb = 2.0 * s->nfn * std::max(dens->frob, 1e-300) *
@@ -959,9 +989,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sa.fill = dfill;
             sa.counters = scount;
             sa.ledger = sledger;
-            // fourfold: the flat screen is faster (the triple bound is weaker with 4 slots)
-            if (sym) { k_screen<true, false><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
-            else { k_screen2<false, false><<<screen_grid, sw * 32, 0, st>>>(sa); note_launch(); }
+            launch_screen(false);
             HXF_CUDA(cudaGetLastError());
             long long c2[C_NCOUNTERS];
             unsigned long long l2[LEDGER_LIMBS];
@@ -1020,8 +1048,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sa.fill = dfill;
             sa.counters = scount;
             sa.ledger = sledger;
-            if (sym) { k_screen<true, true><<<screen_grid, SCREEN_WARPS * 32, 0, st>>>(sa); note_launch(); }
-            else { k_screen2<false, true><<<screen_grid, sw * 32, 0, st>>>(sa); note_launch(); }
+            launch_screen(true);
             HXF_CUDA(cudaGetLastError());
             unsigned long long fill = 0;
             HXF_CUDA(cudaMemcpyAsync(&fill, dfill, sizeof(fill), cudaMemcpyDeviceToHost, st));

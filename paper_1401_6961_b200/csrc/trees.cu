@@ -171,6 +171,31 @@ __global__ void k_diag_q(DevBasis B, int64_t n_pairs, const int* pi, const int* 
     }
 }
 
+// per pair: sqrt(Q) once (screening uses it for every quartet) and the class /
+// primitive-count byte of the survivor sort key
+__global__ void k_pair_meta(DevBasis B, int64_t n_pairs, const int* pi, const int* pj,
+                            const double* q, double* sq, uint8_t* meta) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_pairs) return;
+    const int i = pi[t], j = pj[t];
+    sq[t] = sqrt(q[t]);
+    const int np = (B.poff[i + 1] - B.poff[i]) * (B.poff[j + 1] - B.poff[j]);
+    meta[t] = (uint8_t)((B.l[i] << 1) | B.l[j] | ((np - 1) << 2));
+}
+
+// shell-level max |P| over each function block (|P_jk| for s shells): the
+// per-quartet density factor of the leaf test
+__global__ void k_shell_pmax(DevBasis B, const double* P, double* pmax) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)B.ns * B.ns) return;
+    const int s = (int)(t / B.ns), u = (int)(t % B.ns);
+    const int f0 = B.fn[s], g0 = B.fn[u];
+    double m = 0.0;
+    for (int x = 0; x < B.nf[s]; ++x)
+        for (int y = 0; y < B.nf[u]; ++y) m = fmax(m, fabs(P[(int64_t)(f0 + x) * B.nfn + g0 + y]));
+    pmax[t] = m;
+}
+
 // leaf pair node norms: diag_norm = sqrt(fsum(Q^2)), row/col sum maxima
 __global__ void k_leaf_norms(const int* lslo, const int* lshi, int nleaf, const int64_t* leaf_base,
                              const double* q, double* lnorm, double* lrow, double* lcol) {
@@ -418,6 +443,10 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     { k_diag_q<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
                                                      pr->pp, lt.leaf_of_shell, lt.lslo, lt.lshi, nl,
                                                      pr->leaf_base, pr->q); note_launch(); }
+    pr->sq = dalloc<double>(pr->n_pairs, st);
+    pr->meta = dalloc<uint8_t>(pr->n_pairs, st);
+    { k_pair_meta<<<nblk(pr->n_pairs), 256, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->q,
+                                                     pr->sq, pr->meta); note_launch(); }
     double* lnorm = dalloc<double>(nl2, st);
     double* lrow = dalloc<double>(nl2, st);
     double* lcol = dalloc<double>(nl2, st);
@@ -488,6 +517,8 @@ void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStr
     tmp.push_back(dmax);
     HXF_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
     { k_maxabs<<<256, 256, 0, st>>>(d->P, n2, dmax); note_launch(); }
+    d->pmax = dalloc<double>((int64_t)s->ns * s->ns, st);
+    { k_shell_pmax<<<nblk((int64_t)s->ns * s->ns), 256, 0, st>>>(s->basis, d->P, d->pmax); note_launch(); }
     unsigned long long hm = 0;
     HXF_CUDA(cudaMemcpyAsync(&hm, dmax, sizeof(hm), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaMemcpyAsync(&d->frob, d->norm, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -23,6 +23,6 @@ for _ in range(reps):
     print(name, mode, "quartets", c.eri_shell_quartets, "prim", c.prim_quartets,
           "stages_ms", [round(x, 2) for x in t], flush=True)
 for k in range(16):
-    if c.class_quartets[k]:
+    if c.class_quartets[k] and os.environ.get("ONE_BUILD_CLASSES"):
         print(f"class {k:2d} ({k >> 3}{(k >> 2) & 1}{(k >> 1) & 1}{k & 1}) quartets {c.class_quartets[k]:.3e} "
               f"prim {c.class_prim_quartets[k]:.3e} prim/q {c.class_prim_quartets[k] / c.class_quartets[k]:.2f}")
