@@ -3,18 +3,25 @@
 For each angular class (la, lb, lc, ld) in {0,1}^4 this emits
 
     struct Eri<la,lb,lc,ld> {
-        static constexpr int NI, NJ, NK, NL;
+        static constexpr int NI, NJ, NK, NL, L;
         __device__ static void eval(bra, nb, ket, nk, A, B, C, D, tab, out);
     };
 
 where bra[0:nb] / ket[0:nk] are the primitive pairs of the bra / ket shell
-pair (PrimPair tables of hxf_internal.cuh).  Per primitive quartet: Boys F_0..F_L, vertical
-recursion (electron 1 on P, electron 2 on Q, as in the CPU oracle's
-``eri_general``) onto [e0|f0]; contraction in registers; then the horizontal
-transfer (a,b+1_i| = (a+1_i,b| + AB_i (a,b| on the contracted values.
+pair (PrimPair tables of hxf_internal.cuh) and tab the Boys table of order L.
+Per primitive quartet: Boys F_0..F_L, vertical recursion (electron 1 on P,
+electron 2 on Q, as in the CPU oracle's ``eri_general``) onto [e0|f0];
+contraction in registers; then the horizontal transfer
+(a,b+1_i| = (a+1_i,b| + AB_i (a,b| on the contracted values.
 Output layout out[((i*NJ + j)*NK + k)*NL + l], p components ordered x,y,z.
 
-Run:  python gen_eri.py > eri_classes.cuh
+Light classes (L <= 1) get a compile-time ket primitive count: eval()
+dispatches on nk (warp-uniform, survivors are sorted by primitive counts) to
+core<NKC>, which caches the ket primitives in registers and fully unrolls the
+ket loop without branches, so the independent primitive-quartet chains can
+be interleaved (instruction-level parallelism).
+
+Run:  python gen_eri.py > eri_classes.cuh      (python gen_eri.py --flops: flop table)
 """
 
 import itertools
@@ -23,6 +30,7 @@ import sys
 UNIT = ((1, 0, 0), (0, 1, 0), (0, 0, 1))
 ZERO = (0, 0, 0)
 AX = "xyz"
+MAXK = 9
 
 
 def carts(l):
@@ -99,92 +107,97 @@ class Gen:
         return v
 
 
-def gen_class(la, lb, lc, ld):
+def prim_body(w, la, lb, lc, ld, accs, ind):
+    """Statements for one primitive quartet (bp, kp in scope)."""
     L = la + lb + lc + ld
-    es = carts_upto(la, la + lb)
-    fs = carts_upto(lc, lc + ld)
-    ni, nj, nk, nl = (len(carts(x)) for x in (la, lb, lc, ld))
-    out = []
-    w = out.append
-    w(f"template <> struct Eri<{la},{lb},{lc},{ld}> {{")
-    w(f"  static constexpr int NI = {ni}, NJ = {nj}, NK = {nk}, NL = {nl}, L = {L};")
-    w("  __device__ __forceinline__ static void eval(const PrimPair* __restrict__ bra, int nb,")
-    w("      const PrimPair* __restrict__ ket, int nk, const double3 A, const double3 B,")
-    w("      const double3 C, const double3 D, const double* __restrict__ tab,")
-    w("      double* __restrict__ out) {")
-    accs = [(e, f) for e in es for f in fs]
-    for e, f in accs:
-        w(f"    double acc_{name(e)}_{name(f)} = 0.0;")
-    # Light classes (L <= 1): the ket primitives of the quartet are loaded once
-    # into registers (inner loop fully unrolled to MAXK = 9; the primitive
-    # counts are warp-uniform because survivors are sorted by them), so each
-    # primitive quartet costs no global load.  Heavier classes reload them.
-    cached = L <= 1
-    if cached:
-        w("    constexpr int MK = 9;")
-        need_ip = lc + ld > 0
-        w("    double kqp[MK], kqc[MK], kqx[MK], kqy[MK], kqz[MK];")
-        if need_ip:
-            w("    double kqi[MK];")
-        w("#pragma unroll")
-        w("    for (int t = 0; t < MK; ++t)")
-        w("      if (t < nk) {")
-        w("        const PrimPair q = load_pp(ket + t);")
-        w("        kqp[t] = q.p; kqc[t] = q.c; kqx[t] = q.x; kqy[t] = q.y; kqz[t] = q.z;")
-        if need_ip:
-            w("        kqi[t] = q.ip;")
-        w("      }")
-    w("    for (int ib = 0; ib < nb; ++ib) {")
-    w("      const PrimPair bp = load_pp(bra + ib);")
-    if la + lb > 0:
-        w("      const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
-        w("      const double o2p = 0.5 * bp.ip;")
-    if cached:
-        w("#pragma unroll")
-        w("      for (int ik = 0; ik < MK; ++ik) {")
-        w("        if (ik >= nk) break;")
-        w("        PrimPair kp;")
-        w("        kp.p = kqp[ik]; kp.c = kqc[ik]; kp.x = kqx[ik]; kp.y = kqy[ik]; kp.z = kqz[ik];")
-        w("        kp.ip = %s;" % ("kqi[ik]" if need_ip else "0.0"))
-    else:
-        w("      PrimPair kn = load_pp(ket);")
-        w("      for (int ik = 0; ik < nk; ++ik) {")
-        w("        const PrimPair kp = kn;")
-        w("        if (ik + 1 < nk) kn = load_pp(ket + ik + 1);  // prefetch: hide the L1/L2 latency")
-    w("        const double ps = bp.p + kp.p;")
-    w("        const double r = rsqrt(ps);")
-    w("        const double r2 = r * r;")
-    w("        const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;")
-    w("        const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
-    w("        const double T = bp.p * kp.p * r2 * R2;")
-    w("        const double pref = bp.c * kp.c * r;")
+    p = " " * ind
+    w(p + "const double ps = bp.p + kp.p;")
+    w(p + "const double r = rsqrt(ps);")
+    w(p + "const double r2 = r * r;")
+    w(p + "const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;")
+    w(p + "const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
+    w(p + "const double T = bp.p * kp.p * r2 * R2;")
+    w(p + "const double pref = bp.c * kp.c * r;")
     if L == 0:
-        w("        const double bm0 = pref * boys_f0(T, tab);")
+        w(p + "const double bm0 = pref * boys_f0(T, tab);")
     else:
-        w(f"        double F[{L + 1}];")
-        w(f"        boys_fm<{L}>(T, F, tab);")
+        w(p + f"double F[{L + 1}];")
+        w(p + f"boys_fm<{L}>(T, F, tab);")
         for m in range(L + 1):
-            w(f"        const double bm{m} = pref * F[{m}];")
+            w(p + f"const double bm{m} = pref * F[{m}];")
         if la + lb > 0:
-            w("        const double rp = kp.p * r2;")
-            w("        const double WPx = -rp * PQx, WPy = -rp * PQy, WPz = -rp * PQz;")
+            w(p + "const double rp = kp.p * r2;")
+            w(p + "const double WPx = -rp * PQx, WPy = -rp * PQy, WPz = -rp * PQz;")
         if lc + ld > 0:
-            w("        const double rq = bp.p * r2;")
-            w("        const double WQx = rq * PQx, WQy = rq * PQy, WQz = rq * PQz;")
-            w("        const double QCx = kp.x - C.x, QCy = kp.y - C.y, QCz = kp.z - C.z;")
-            w("        const double o2q = 0.5 * kp.ip;")
+            w(p + "const double rq = bp.p * r2;")
+            w(p + "const double WQx = rq * PQx, WQy = rq * PQy, WQz = rq * PQz;")
+            w(p + "const double QCx = kp.x - C.x, QCy = kp.y - C.y, QCz = kp.z - C.z;")
+            w(p + "const double o2q = 0.5 * kp.ip;")
         if la + lb > 0 and lc + ld > 0:
-            w("        const double o2pq = 0.5 * r2;")
+            w(p + "const double o2pq = 0.5 * r2;")
     g = Gen()
     res = {}
     for e, f in accs:
         res[(e, f)] = g.vrr(e, f, 0)
     for line in g.lines:
-        w("        " + line)
+        w(p + line)
     for e, f in accs:
-        w(f"        acc_{name(e)}_{name(f)} += {res[(e, f)]};")
+        w(p + f"acc_{name(e)}_{name(f)} += {res[(e, f)]};")
+
+
+def gen_class(la, lb, lc, ld):
+    L = la + lb + lc + ld
+    es = carts_upto(la, la + lb)
+    fs = carts_upto(lc, lc + ld)
+    ni, nj, nk, nl = (len(carts(x)) for x in (la, lb, lc, ld))
+    accs = [(e, f) for e in es for f in fs]
+    cached = L <= 1
+    need_ip = lc + ld > 0
+    out = []
+    w = out.append
+    w(f"template <> struct Eri<{la},{lb},{lc},{ld}> {{")
+    w(f"  static constexpr int NI = {ni}, NJ = {nj}, NK = {nk}, NL = {nl}, L = {L};")
+    # ---- core<NKC>: NKC > 0 compile-time ket primitive count (register cache)
+    w("  template <int NKC>")
+    w("  __device__ __forceinline__ static void core(const PrimPair* __restrict__ bra, int nb,")
+    w("      const PrimPair* __restrict__ ket, int nk, const double3 A, const double3 B,")
+    w("      const double3 C, const double3 D, const double* __restrict__ tab,")
+    w("      double* __restrict__ out) {")
+    for e, f in accs:
+        w(f"    double acc_{name(e)}_{name(f)} = 0.0;")
+    if cached:
+        w("    if constexpr (NKC > 0) {")
+        w("      PrimPair kq[NKC > 0 ? NKC : 1];")
+        w("#pragma unroll")
+        w("      for (int t = 0; t < NKC; ++t) kq[t] = load_pp(ket + t);")
+        w("      PrimPair bn = load_pp(bra);")
+        w("      for (int ib = 0; ib < nb; ++ib) {")
+        w("        const PrimPair bp = bn;")
+        w("        if (ib + 1 < nb) bn = load_pp(bra + ib + 1);  // prefetch the next bra primitive")
+        if la + lb > 0:
+            w("        const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
+            w("        const double o2p = 0.5 * bp.ip;")
+        w("#pragma unroll")
+        w("        for (int ik = 0; ik < NKC; ++ik) {")
+        w("          const PrimPair& kp = kq[ik];")
+        prim_body(w, la, lb, lc, ld, accs, 10)
+        w("        }")
+        w("      }")
+        w("    } else {")
+    w("      for (int ib = 0; ib < nb; ++ib) {")
+    w("        const PrimPair bp = load_pp(bra + ib);")
+    if la + lb > 0:
+        w("        const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
+        w("        const double o2p = 0.5 * bp.ip;")
+    w("        PrimPair kn = load_pp(ket);")
+    w("        for (int ik = 0; ik < nk; ++ik) {")
+    w("          const PrimPair kp = kn;")
+    w("          if (ik + 1 < nk) kn = load_pp(ket + ik + 1);  // prefetch: hide the L1/L2 latency")
+    prim_body(w, la, lb, lc, ld, accs, 10)
+    w("        }")
     w("      }")
-    w("    }")
+    if cached:
+        w("    }")
     # horizontal recursion on contracted values
     memo = {}
     hl = []
@@ -228,7 +241,22 @@ def gen_class(la, lb, lc, ld):
     for idx, v in outs:
         w(f"    out[{idx}] = {v};")
     w("  }")
+    # ---- eval: dispatch on the (warp-uniform) ket primitive count
+    w("  __device__ __forceinline__ static void eval(const PrimPair* __restrict__ bra, int nb,")
+    w("      const PrimPair* __restrict__ ket, int nk, const double3 A, const double3 B,")
+    w("      const double3 C, const double3 D, const double* __restrict__ tab,")
+    w("      double* __restrict__ out) {")
+    if cached:
+        w("    switch (nk) {")
+        for k in range(1, MAXK + 1):
+            w(f"      case {k}: core<{k}>(bra, nb, ket, nk, A, B, C, D, tab, out); return;")
+        w("      default: core<0>(bra, nb, ket, nk, A, B, C, D, tab, out); return;")
+        w("    }")
+    else:
+        w("    core<0>(bra, nb, ket, nk, A, B, C, D, tab, out);")
+    w("  }")
     w("};")
+    del need_ip
     return "\n".join(out)
 
 

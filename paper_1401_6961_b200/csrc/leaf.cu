@@ -530,7 +530,7 @@ __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double
 }
 
 template <int LA, int LB, int LC, int LD>
-__global__ void __launch_bounds__(128, (LA + LB + LC + LD) <= 1 ? 4 : 2) k_eri(EriArgs e) {
+__global__ void __launch_bounds__(128, (LA + LB + LC + LD) <= 1 ? 3 : 2) k_eri(EriArgs e) {
     typedef Eri<LA, LB, LC, LD> E;
     constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL;
     extern __shared__ __align__(16) double s_tab[];
