@@ -48,13 +48,15 @@ def parse():
     return ap.parse_args()
 
 
-def make_config(args):
+def make_config(args, device_density=False):
     from paper_1401_6961_b200 import configs
     kw = {}
     if args.units is not None:
         if args.config in ("c1", "c2"):
             raise SystemExit("--units applies to the cube recipes c3-c5")
         kw["n_units"] = args.units
+    if args.config in ("c3", "c4", "c5") and device_density:
+        kw["host_density"] = False      # generated on the GPU below
     cfg = configs.make(args.config, **kw)
     if args.tau is not None:
         cfg.tau_2e = args.tau
@@ -203,7 +205,13 @@ def native_arm(args):
     dev = torch.device("cuda", local)
 
     t0 = time.perf_counter()
-    cfg = make_config(args)
+    cfg = make_config(args, device_density=True)
+    if cfg.P is None:
+        from paper_1401_6961_b200 import configs
+        P_gen = configs.decay_density_device(cfg.system, cfg.density_seed, dev)
+        torch.cuda.synchronize()
+    else:
+        P_gen = None
     gen_s = time.perf_counter() - t0
     sym = args.mode == "fourfold"
     part = hx.build_partition(cfg.system, leaf_size=cfg.leaf_size)
@@ -214,8 +222,13 @@ def native_arm(args):
     torch.cuda.synchronize()
     pair_ms = 1e3 * (time.perf_counter() - t0)
     n = cfg.n_functions
-    P_host = torch.from_numpy(cfg.P).pin_memory()
-    P_dev = P_host.to(dev)
+    if P_gen is None:
+        P_host = torch.from_numpy(cfg.P).pin_memory()
+        P_dev = P_host.to(dev)
+    else:
+        P_dev = P_gen
+        P_host = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        P_host.copy_(P_dev)
     K_dev = torch.empty((n, n), dtype=torch.float64, device=dev)
     K_host = torch.empty((n, n), dtype=torch.float64).pin_memory()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2

@@ -95,6 +95,15 @@ def counters_from_vector(v, symmetric):
     return out
 
 
+def allreduce_partials(K, counters_vec, group=None):
+    """Sum partial K and counter vectors over the job (NCCL on GPU, gloo on CPU)."""
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(K, group=group)
+        dist.all_reduce(counters_vec, group=group)
+    return K, counters_vec
+
+
 def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, shards=None):
     """One rank's share of a sharded build + the all-reduce of K and counters.
 
@@ -113,9 +122,7 @@ def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, sha
     _, c, _ = run_exchange(bra, ket, P, tau_2e, mode, symmetry, True, None, K_out=K_dev,
                            shard=(level, b, e), symmetrize=False)
     vec = torch.from_numpy(counters_vector(c)).to(K_dev.device)
-    if world > 1:
-        dist.all_reduce(K_dev, group=group)
-        dist.all_reduce(vec, group=group)
+    allreduce_partials(K_dev, vec, group)
     if symmetry:
         _native.check(_native.lib().hxf_symmetrize(ctypes.c_void_p(K_dev.data_ptr()), K_dev.shape[0],
                                                    1e-10, _native.current_stream()))

@@ -1,0 +1,173 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2).
+
+The device path shards the product-tree frontier at a cut level into
+contiguous cost-balanced ranges (distributed.split_by_cost), each rank runs
+its subtrees into a private K, work above the cut is counted by shard 0
+only, and K / counters are summed by one all-reduce
+(distributed.allreduce_partials).  Here the per-rank compute is the CPU
+oracle (the checker) driven over the same frontier order the device uses
+(parents in order, children in (a, cc, d, bb) order), so the sharding
+semantics and the reduction plumbing are verified without a GPU.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import hexfock_oracle as ho
+from paper_1401_6961_b200 import configs, distributed
+
+
+def test_split_by_cost_contiguous_balanced():
+    costs = np.array([5, 1, 1, 1, 1, 1, 5, 1, 1, 3], dtype=float)
+    for world in (1, 2, 3, 4, 7, 16):
+        r = distributed.split_by_cost(costs, world)
+        assert len(r) == world
+        assert r[0][0] == 0 and r[-1][1] == len(costs)
+        for (b0, e0), (b1, e1) in zip(r, r[1:]):
+            assert e0 == b1 and b0 <= e0
+    r = distributed.split_by_cost(np.ones(100), 4)
+    assert [e - b for b, e in r] == [25, 25, 25, 25]
+    assert distributed.split_by_cost(np.ones(0), 3) == [(0, 0), (0, 0), (0, 0)]
+
+
+def test_counters_vector_roundtrip():
+    class C:  # mimics the ctypes counters struct
+        pass
+    c = C()
+    for i, k in enumerate(("tasks_visited", "tasks_culled_screening", "tasks_culled_absent",
+                           "leaf_contractions", "eri_shell_quartets", "quartets_culled_leaf",
+                           "tasks_expanded", "children_spawned", "links_culled_screening",
+                           "links_culled_absent", "ties_task", "ties_leaf", "prim_quartets")):
+        setattr(c, k, 10 * i + 1)
+    c.case_tasks = list(range(9))
+    c.case_leaf_tasks = list(range(9, 18))
+    c.class_quartets = [0] * 16
+    c.class_prim_quartets = [0] * 16
+    c.culled_bound_ledger = 0.125
+    out = distributed.counters_from_vector(distributed.counters_vector(c), True)
+    assert out.tasks_visited == 1 and out.children_spawned == 71
+    assert out.case_tasks["SPARSE"] == 8 and out.case_leaf_tasks["A"] == 9
+    assert out.culled_bound_ledger == 0.125
+
+
+# ------------------------------------------------------------ sharded oracle
+
+def _frontier(st, tau, level, run):
+    """Naive BFS to `level` in device order; visits above the cut go to `run`."""
+    fr = [(st.pairs, st.Ptree, st.pairs)]
+    # the root visit
+    run.c.tasks_visited += 1
+    b, p, k = fr[0]
+    if _cull(run, b, p, k):
+        return []
+    if b.is_leaf and k.is_leaf:
+        run.c.leaf_contractions += 1
+        run.contract(b, p, k)
+        return []
+    run.c.tasks_expanded += 1
+    for _ in range(level):
+        nxt = []
+        for b, p, k in fr:
+            for a in range(len(b.row.kids())):
+                for cc in range(len(b.col.kids())):
+                    bch = b.child(a, cc)
+                    for d in range(len(k.row.kids())):
+                        pch = p.child(cc, d)
+                        for bb in range(len(k.col.kids())):
+                            kch = k.child(d, bb)
+                            run.c.children_spawned += 1
+                            run.c.tasks_visited += 1
+                            if _cull(run, bch, pch, kch):
+                                continue
+                            if bch.is_leaf and kch.is_leaf:
+                                run.c.leaf_contractions += 1
+                                run.contract(bch, pch, kch)
+                                continue
+                            run.c.tasks_expanded += 1
+                            nxt.append((bch, pch, kch))
+        fr = nxt
+    return fr
+
+
+def _cull(run, b, p, k):
+    c = run.c
+    if b is None or p is None or k is None or b.pruned or k.pruned:
+        c.tasks_culled_absent += 1
+        return True
+    import math
+    if ho.sorted_product(math.sqrt(b.diag_norm), p.norm, math.sqrt(k.diag_norm)) <= run.tau:
+        c.tasks_culled_screening += 1
+        c.culled_bound_ledger += ho.culled_task_bound(b, p.norm, k)
+        return True
+    return False
+
+
+def _expand_children(run, b, p, k):
+    for a in range(len(b.row.kids())):
+        for cc in range(len(b.col.kids())):
+            bch = b.child(a, cc)
+            for d in range(len(k.row.kids())):
+                pch = p.child(cc, d)
+                for bb in range(len(k.col.kids())):
+                    run.c.children_spawned += 1
+                    run.visit(bch, pch, k.child(d, bb))
+
+
+def _sharded_run(st, tau, level, world, rank):
+    top = ho._Naive(st.shells, st.P, st.P.shape[0], tau, "schwarz", True, False)
+    frontier = _frontier(st, tau, level, top)
+    ranges = distributed.split_by_cost(np.ones(len(frontier)), world)
+    mine = ho._Naive(st.shells, st.P, st.P.shape[0], tau, "schwarz", True, False)
+    for b, p, k in frontier[ranges[rank][0]:ranges[rank][1]]:
+        _expand_children(mine, b, p, k)
+    if rank == 0:
+        mine.K += top.K
+        mine.c.merge(top.c)
+    return mine
+
+
+def _vec(c):
+    return np.array([c.tasks_visited, c.tasks_culled_screening, c.tasks_culled_absent,
+                     c.leaf_contractions, c.eri_shell_quartets, c.quartets_culled_leaf,
+                     c.tasks_expanded, c.children_spawned, c.culled_bound_ledger], dtype=np.float64)
+
+
+def _worker(rank, world, port, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = configs.cube_cluster(4, 7, "tiny")
+    st = ho.Setup(cfg.system, cfg.P, tau_ovlp=1e-11, leaf_size=4)
+    run = _sharded_run(st, 1e-8, 2, world, rank)
+    K = torch.from_numpy(run.K.copy())
+    vec = torch.from_numpy(_vec(run.c))
+    distributed.allreduce_partials(K, vec)
+    if rank == 0:
+        np.savez(result_path, K=K.numpy(), vec=vec.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_sharded_build_equals_single_process(tmp_path, world):
+    path = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    res = np.load(path)
+    cfg = configs.cube_cluster(4, 7, "tiny")
+    st = ho.Setup(cfg.system, cfg.P, tau_ovlp=1e-11, leaf_size=4)
+    K, c = st.naive(1e-8)
+    assert np.abs(res["K"] - K).max() <= 1e-13
+    ref = _vec(c)
+    assert np.array_equal(res["vec"][:8], ref[:8])        # integer counters exact
+    assert res["vec"][8] == pytest.approx(ref[8], rel=1e-12)

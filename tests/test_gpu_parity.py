@@ -131,3 +131,31 @@ def test_repeated_builds_bitwise_identical():
         K2, c2 = f()
         assert np.array_equal(K1, K2)
         assert c1.to_dict() == c2.to_dict()
+
+
+@pytest.mark.parametrize("sym", [False, True])
+def test_sharded_shards_sum_to_full_build(sym):
+    """Multi-GPU semantics on one device: the shards of a frontier cut, run one
+    after another, sum (K and counters) to the unsharded build."""
+    from paper_1401_6961_b200 import distributed, exchange
+    cfg = configs.cube_cluster(8, 3, "tiny")
+    part = hx.build_partition(cfg.system, leaf_size=6)
+    pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
+    P_tree = hx.build_matrix_tree(cfg.P, part)
+    K_full, c_full, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-9, "schwarz", sym)
+    for world in (2, 3):
+        level, ranges = distributed.plan(pairs, pairs, P_tree, 1e-9, "schwarz", sym, world,
+                                         min_tasks_per_rank=4)
+        K = np.zeros_like(K_full)
+        vec = 0
+        for b, e in ranges:
+            Ks, c, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-9, "schwarz", sym,
+                                             shard=(level, b, e), symmetrize=False)
+            K += Ks
+            vec = vec + distributed.counters_vector(c)
+        if sym:
+            K = hx.symmetrize_final(K)
+        full = distributed.counters_vector(c_full)
+        assert np.array_equal(vec[:-1], full[:-1]), (world, level, ranges)
+        assert vec[-1] == pytest.approx(full[-1], rel=1e-12)
+        assert np.abs(K - K_full).max() <= 1e-13
