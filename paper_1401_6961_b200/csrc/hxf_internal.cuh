@@ -264,6 +264,27 @@ __host__ __device__ inline double fx_to_double(const unsigned long long* limb, i
 #define LEDGER_SCALE 160
 #define K_LIMBS 2
 
+// K accumulator (per element, 16 B): v = round(x 2^S) (|sums| < 2^98) is split
+// into non-overlapping parts hi = v >> 36 (signed) and lo = v & (2^36 - 1);
+// each is summed with a fire-and-forget 64-bit reduction (no returned value,
+// no dependent L2 round trip).  Integer sums are order independent, so K is
+// bitwise reproducible; exact while an element receives < 2^28 additions.
+#define K_LO_BITS 36
+
+__device__ __forceinline__ void k_fixed_add(unsigned long long* acc, double x, int S) {
+    unsigned long long v[2];
+    fx_from_double<2>(x, S, v);
+    const unsigned long long hi = (v[1] << (64 - K_LO_BITS)) | (v[0] >> K_LO_BITS);
+    const unsigned long long lo = v[0] & ((1ull << K_LO_BITS) - 1);
+    if (hi) atomicAdd(acc, hi);
+    if (lo) atomicAdd(acc + 1, lo);
+}
+
+__host__ __device__ inline double k_fixed_value(const unsigned long long* acc, int S) {
+    const long long hi = (long long)acc[0];
+    return ldexp((double)hi, K_LO_BITS - S) + ldexp((double)acc[1], -S);
+}
+
 // ---------------------------------------------------------------- warp utils
 
 __device__ __forceinline__ void atomic_add_ll(long long* p, long long v) {

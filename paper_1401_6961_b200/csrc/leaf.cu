@@ -524,9 +524,7 @@ struct EriArgs {
 
 __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double v) {
     if (v == 0.0) return;
-    unsigned long long limb[K_LIMBS];
-    fx_from_double<K_LIMBS>(v, e.S, limb);
-    fx_atomic_add<K_LIMBS>(e.K + 2 * ((int64_t)row * e.nfn + col), limb);
+    k_fixed_add(e.K + 2 * ((int64_t)row * e.nfn + col), v, e.S);
 }
 
 template <int LA, int LB, int LC, int LD>
@@ -709,6 +707,137 @@ __global__ void __launch_bounds__(256) k_eri_ssss(EriArgs e, const SegDesc* __re
 
 #endif
 
+// ---------------------------------------------------------------------------
+// Light classes (L <= 1): bra-primitive parallel.  Launched per sub-segment of
+// uniform bra primitive count G = nb (survivors are sorted by it): a group of
+// G lanes owns one shell quartet, lane g owns bra primitive g and loops over
+// the ket primitives (same address across the group -> broadcast loads).  The
+// group sum is a fixed shuffle tree over G lanes (depends only on G, so the
+// result is independent of where the quartet sits in the warp), then the
+// group leader applies the horizontal transfer and contracts into K.  Few
+// registers per lane -> high occupancy.
+
+template <int LA, int LB, int LC, int LD>
+__global__ void __launch_bounds__(256) k_eri_bp(EriArgs e, int G) {
+    typedef Eri<LA, LB, LC, LD> E;
+    typedef EriBP<LA, LB, LC, LD> BP;
+    constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL, NACC = BP::NACC;
+    extern __shared__ __align__(16) double s_tab[];
+    boys_table_to_smem(s_tab, E::L);
+    const int lane = threadIdx.x & 31;
+    const int RW = 32 / G;                 // groups per warp
+    const int grp = lane / G, g = lane - grp * G;
+    const int64_t nwt = (e.n + RW - 1) / RW;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    long long nprim = 0, nq = 0;
+    for (int64_t wt = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); wt < nwt;
+         wt += nwarps) {
+        const int64_t r = wt * RW + grp;
+        bool act = grp < RW && r < e.n;
+        int mask = 0;
+        int4 ib = make_int4(0, 0, 0, 0), ik = make_int4(0, 0, 0, 0);
+        int64_t pb = 0, pk = 0;
+        double acc[NACC];
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+        double3 A{0, 0, 0}, C{0, 0, 0};
+        if (act) {
+            const uint64_t rec = e.rec[r];
+            mask = (int)((rec >> 56) & 0xf);
+            act = mask != 0;
+            pb = (int64_t)(rec & 0xfffffff);
+            pk = (int64_t)((rec >> 28) & 0xfffffff);
+        }
+        if (act) {
+            ib = __ldg(e.binfo + pb);
+            ik = __ldg(e.kinfo + pk);
+            if (LA | LB) A = e.ctr[e.bpi[pb]];
+            if (LC | LD) C = e.ctr[e.kpi[pk]];
+            const PrimPair bp = load_pp(e.bpp + ib.z + g);
+            const PrimPair* kq = e.kpp + ik.z;
+            for (int t = 0; t < ik.w; ++t) BP::prim(bp, load_pp(kq + t), A, C, s_tab, acc);
+        }
+#pragma unroll
+        for (int k = 0; k < NACC; ++k) {
+#pragma unroll
+            for (int off = 8; off > 0; off >>= 1) {
+                const double o = __shfl_down_sync(0xffffffffu, acc[k], off);
+                if (g + off < G) acc[k] += o;
+            }
+        }
+        if (act && g == 0) {
+            nq += 1;
+            nprim += (long long)ib.w * ik.w;
+            double3 B{0, 0, 0}, D{0, 0, 0};
+            if (LB) B = e.ctr[e.bpj[pb]];
+            if (LD) D = e.ctr[e.kpj[pk]];
+            double out[NI * NJ * NK * NL];
+            BP::hrr(acc, A, B, C, D, out);
+            const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
+            const int64_t n = e.nfn;
+            const double* P = e.P;
+#define OUT(x, y, z, w) out[(((x) * NJ + (y)) * NK + (z)) * NL + (w)]
+            if (mask & 1)
+                for (int x = 0; x < NI; ++x)
+                    for (int w = 0; w < NL; ++w) {
+                        double s = 0.0;
+                        for (int y = 0; y < NJ; ++y)
+                            for (int z = 0; z < NK; ++z) s += __ldg(P + (fj + y) * n + fk + z) * OUT(x, y, z, w);
+                        k_add(e, fi + x, fl + w, -0.5 * s);
+                    }
+            if (mask & 2)
+                for (int y = 0; y < NJ; ++y)
+                    for (int w = 0; w < NL; ++w) {
+                        double s = 0.0;
+                        for (int x = 0; x < NI; ++x)
+                            for (int z = 0; z < NK; ++z) s += __ldg(P + (fi + x) * n + fk + z) * OUT(x, y, z, w);
+                        k_add(e, fj + y, fl + w, -0.5 * s);
+                    }
+            if (mask & 4)
+                for (int x = 0; x < NI; ++x)
+                    for (int z = 0; z < NK; ++z) {
+                        double s = 0.0;
+                        for (int y = 0; y < NJ; ++y)
+                            for (int w = 0; w < NL; ++w) s += __ldg(P + (fj + y) * n + fl + w) * OUT(x, y, z, w);
+                        k_add(e, fi + x, fk + z, -0.5 * s);
+                    }
+            if (mask & 8)
+                for (int y = 0; y < NJ; ++y)
+                    for (int z = 0; z < NK; ++z) {
+                        double s = 0.0;
+                        for (int x = 0; x < NI; ++x)
+                            for (int w = 0; w < NL; ++w) s += __ldg(P + (fi + x) * n + fl + w) * OUT(x, y, z, w);
+                        k_add(e, fj + y, fk + z, -0.5 * s);
+                    }
+#undef OUT
+        }
+    }
+    constexpr int CLS = (LA << 3) | (LB << 2) | (LC << 1) | LD;
+    nq = warp_sum_ll(nq);
+    nprim = warp_sum_ll(nprim);
+    if (lane == 0 && nprim) {
+        atomic_add_ll(&e.counters[C_PRIMQ], nprim);
+        atomic_add_ll(&e.counters[C_CLSPQ0 + CLS], nprim);
+        atomic_add_ll(&e.counters[C_CLSQ0 + CLS], nq);
+    }
+}
+
+template <int A, int B, int C, int D>
+void launch_eri_bp(const EriArgs& e, int G, cudaStream_t st) {
+    static int per_sm = -1, sms = 0;
+    if (per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri_bp<A, B, C, D>, 256, BOYS_TAB_BYTES);
+        per_sm = std::max(per_sm, 1);
+    }
+    const int64_t warps = (e.n + (32 / G) - 1) / (32 / G);
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)sms * per_sm));
+    k_eri_bp<A, B, C, D><<<g, 256, BOYS_TAB_BYTES, st>>>(e, G);
+    note_launch();
+}
+
 // lower bounds of every 12-bit key value in the sorted key array
 __global__ void k_key_bounds(const uint16_t* keys, int64_t n, int64_t* bounds) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -753,7 +882,7 @@ __global__ void k_log(const uint64_t* rec, int64_t n, const int* bpi, const int*
 __global__ void k_fx_to_double(const unsigned long long* Kfx, int64_t n2, int S, double* K) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2;
          t += (int64_t)gridDim.x * blockDim.x)
-        K[t] = fx_to_double<K_LIMBS>(Kfx + 2 * t, S);
+        K[t] = k_fixed_value(Kfx + 2 * t, S);
 }
 
 __global__ void k_asym(const double* K, int n, unsigned long long* out) {
@@ -938,6 +1067,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     // HXF_SCREEN=flat selects the per-quartet screen (A/B reference)
     const char* sv = getenv("HXF_SCREEN");
     const bool flat = sv && !strcmp(sv, "flat");
+    // HXF_ERI=bp enables the bra-primitive-parallel light-class kernels (measured
+    // slower than thread-per-quartet on c3/c4; kept as an A/B variant)
+    const char* ev = getenv("HXF_ERI");
+    const bool use_bp = ev && !strcmp(ev, "bp");
     const int sw = flat ? SCREEN_WARPS : (sym ? screen2_warps<true>() : screen2_warps<false>());
     const unsigned screen_grid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * (sym ? 12 : 8)));
@@ -955,7 +1088,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     // fixed-point scale for K: |K| <= 1/2 sum|P| max|(ij|kl)| <= 1/2 n ||P||_F maxQ
     const double kb = 2.0 * s->nfn * std::max(dens->frob, 1e-300) *
                       std::max(std::sqrt(bra->maxq * ket->maxq), 1e-300);
-    int S = 124 - (int)std::ceil(std::log2(kb));
+    int S = 97 - (int)std::ceil(std::log2(kb));  // |sums of v| < 2^98 (k_fixed_add)
     S = std::max(-900, std::min(S, 400));
 
     unsigned long long* Kfx = nullptr;
@@ -1005,7 +1138,9 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         HXF_CUDA(cudaMemsetAsync(Kfx, 0, 2 * n2 * sizeof(unsigned long long), st));
         size_t freeb = 0, totb = 0;
         cudaMemGetInfo(&freeb, &totb);
-        int64_t cap = std::min<int64_t>(1ll << 27, std::max<int64_t>(1 << 16, (int64_t)(freeb / 40)));
+        // survivor chunk capacity: ~40 B of device memory per record (two record
+        // buffers, two key buffers, radix-sort scratch); up to 2^29 records
+        int64_t cap = std::min<int64_t>(1ll << 29, std::max<int64_t>(1 << 16, (int64_t)(freeb / 160)));
         uint64_t* rec = lalloc<uint64_t>(cap, st);
         uint64_t* rec2 = lalloc<uint64_t>(cap, st);
         uint16_t* keys = lalloc<uint16_t>(cap, st);
@@ -1070,6 +1205,23 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                 HXF_CUDA(cudaStreamSynchronize(st));
                 Timer tk(st);
                 for (int c = 0; c < 16; ++c) {
+                    if (use_bp && __builtin_popcount(c) <= 1) {
+                        // light class: one launch per bra primitive count (group size)
+                        for (int nb = 1; nb <= 16; ++nb) {
+                            const int64_t b0 = kbnd[(c << 8) | ((nb - 1) << 4)], b1 = kbnd[(c << 8) + (nb << 4)];
+                            if (b1 <= b0) continue;
+                            e.rec = rec2 + b0;
+                            e.n = b1 - b0;
+                            switch (c) {
+                                case 0: launch_eri_bp<0, 0, 0, 0>(e, nb, st); break;
+                                case 1: launch_eri_bp<0, 0, 0, 1>(e, nb, st); break;
+                                case 2: launch_eri_bp<0, 0, 1, 0>(e, nb, st); break;
+                                case 4: launch_eri_bp<0, 1, 0, 0>(e, nb, st); break;
+                                case 8: launch_eri_bp<1, 0, 0, 0>(e, nb, st); break;
+                            }
+                        }
+                        continue;
+                    }
                     e.rec = rec2 + kbnd[c << 8];
                     e.n = kbnd[(c + 1) << 8] - kbnd[c << 8];
                     launch_eri_class(c, e, st);
