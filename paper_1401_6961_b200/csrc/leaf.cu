@@ -84,6 +84,51 @@ __device__ __forceinline__ double pblock_max(const ScreenArgs& a, int s, int t) 
     return m;
 }
 
+// Survivor emission through per-warp slabs: one global atomic reserves SLAB
+// record slots; a slab that cannot take the next ballot is padded with
+// sentinel records (key 0xFFFF sorts after every real 12-bit key and is
+// excluded by the key bounds), so no emitting iteration waits for an atomic.
+#define SLAB 256
+#define SENTINEL_REC (~0ull)
+#define SENTINEL_KEY ((uint16_t)0xFFFF)
+
+struct Slab {
+    unsigned long long base;
+    int used;
+};
+
+template <typename Args>
+__device__ __forceinline__ void slab_pad(const Slab& s, const Args& a, int lane) {
+    for (int i = s.used + lane; i < SLAB; i += 32) {
+        const unsigned long long pos = s.base + i;
+        if ((int64_t)pos < a.cap) {
+            a.rec[pos] = SENTINEL_REC;
+            a.keys[pos] = SENTINEL_KEY;
+        }
+    }
+}
+
+template <typename Args>
+__device__ __forceinline__ void slab_emit(Slab& s, const Args& a, unsigned bal, bool keep, uint64_t rec,
+                                          uint16_t key, int lane) {
+    const int cnt = __popc(bal);
+    if (s.used + cnt > SLAB) {  // warp-uniform
+        slab_pad(s, a, lane);
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(a.fill, (unsigned long long)SLAB);
+        s.base = __shfl_sync(0xffffffffu, b, 0);
+        s.used = 0;
+    }
+    if (keep) {
+        const unsigned long long pos = s.base + s.used + __popc(bal & ((1u << lane) - 1u));
+        if ((int64_t)pos < a.cap) {
+            a.rec[pos] = rec;
+            a.keys[pos] = key;
+        }
+    }
+    s.used += cnt;
+}
+
 // canonical (x <= y) enumeration of a diagonal node's pairs
 __device__ __forceinline__ void tri_decode(int a, int n, int* x, int* y) {
     int r = 0;
@@ -103,6 +148,7 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
     const int64_t gw = blockIdx.x * (int64_t)SCREEN_WARPS + wid;
     const int64_t W = (int64_t)gridDim.x * SCREEN_WARPS;
     long long n_eri = 0, n_cull = 0, n_tie = 0;
+    Slab slab{0ull, SLAB};
     double ledger = 0.0;
     const bool schwarz = a.mode == HXF_MODE_SCHWARZ;
     for (int64_t t = a.t0 + gw; t < a.t1; t += W) {
@@ -196,26 +242,19 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
             if (EMIT) {
                 const unsigned bal = __ballot_sync(0xffffffffu, keep_any);
                 if (bal) {
-                    unsigned long long base = 0;
-                    if (lane == 0) base = atomicAdd(a.fill, (unsigned long long)__popc(bal));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (keep_any) {
-                        const uint64_t pos = base + __popc(bal & ((1u << lane) - 1u));
-                        if ((int64_t)pos < a.cap) {
-                            const uint64_t pb = (uint64_t)(bb + sm.apl[ia]);
-                            const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
-                            const int ca = sm.acl[ia], cb = sm.bcl[ib];
-                            const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
-                            a.rec[pos] = pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60);
-                            // sort key: class, bra / ket primitive-pair counts (uniform warps)
-                            a.keys[pos] = (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2));
-                        }
-                    }
+                    const uint64_t pb = (uint64_t)(bb + sm.apl[ia]);
+                    const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
+                    const int ca = sm.acl[ia], cb = sm.bcl[ib];
+                    const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
+                    // sort key: class, bra / ket primitive-pair counts (uniform warps)
+                    slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60),
+                              (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2)), lane);
                 }
             }
         }
         __syncwarp();
     }
+    if (EMIT) slab_pad(slab, a, lane);
     // per-lane totals; counters are integers (order independent); the warp's
     // ledger partial has a fixed task->warp assignment and a fixed shuffle tree
     n_eri = warp_sum_ll(n_eri);
@@ -275,6 +314,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
     const int64_t gw = blockIdx.x * (int64_t)NW + wid;
     const int64_t Wt = (int64_t)gridDim.x * NW;
     long long n_eri = 0, n_cull = 0, n_tie = 0;
+    Slab slab{0ull, SLAB};
     double ledger = 0.0;
     const bool schwarz = a.mode == HXF_MODE_SCHWARZ;
     const double tau = a.tau;
@@ -418,20 +458,12 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
                 if (EMIT) {
                     const unsigned bal = __ballot_sync(0xffffffffu, keep_any);
                     if (bal) {
-                        unsigned long long base = 0;
-                        if (lane == 0) base = atomicAdd(a.fill, (unsigned long long)__popc(bal));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (keep_any) {
-                            const uint64_t pos = base + __popc(bal & ((1u << lane) - 1u));
-                            if ((int64_t)pos < a.cap) {
-                                const uint64_t pb = (uint64_t)(bb + sm.apl[ia]);
-                                const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
-                                const int ca = sm.acl[ia], cb = sm.bcl[ib];
-                                const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
-                                a.rec[pos] = pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60);
-                                a.keys[pos] = (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2));
-                            }
-                        }
+                        const uint64_t pb = (uint64_t)(bb + sm.apl[ia]);
+                        const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
+                        const int ca = sm.acl[ia], cb = sm.bcl[ib];
+                        const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
+                        slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60),
+                                  (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2)), lane);
                     }
                 }
             }
@@ -484,6 +516,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
         if (qn) flush(qn);
         __syncwarp();
     }
+    if (EMIT) slab_pad(slab, a, lane);
     n_eri = warp_sum_ll(n_eri);
     n_cull = warp_sum_ll(n_cull);
     n_tie = warp_sum_ll(n_tie);
@@ -869,6 +902,7 @@ __global__ void k_log(const uint64_t* rec, int64_t n, const int* bpi, const int*
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= n) return;
     const uint64_t r = rec[t];
+    if (r == SENTINEL_REC) return;  // slab padding
     const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
     const unsigned long long pos = atomicAdd(fill, 1ull);
     if ((int64_t)pos < cap) {
