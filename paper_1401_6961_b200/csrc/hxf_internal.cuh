@@ -308,7 +308,7 @@ enum {
     C_VISITED = 0, C_CULL_SCREEN, C_CULL_ABSENT, C_LEAF, C_ERIQ, C_CULL_LEAF, C_EXPANDED,
     C_SPAWNED, C_LINK_SCREEN, C_LINK_ABSENT, C_CASE0, C_CASELEAF0 = C_CASE0 + HXF_NCASES,
     C_TIE_TASK = C_CASELEAF0 + HXF_NCASES, C_TIE_LEAF, C_PRIMQ, C_OVERFLOW, C_CLSQ0,
-    C_CLSPQ0 = C_CLSQ0 + 16, C_NCOUNTERS = C_CLSPQ0 + 16
+    C_CLSPQ0 = C_CLSQ0 + 16, C_DBG0 = C_CLSPQ0 + 16, C_NCOUNTERS = C_DBG0 + 4
 };
 
 // kernels launched by the library (evidence that the device path ran)

@@ -319,7 +319,14 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
     const bool schwarz = a.mode == HXF_MODE_SCHWARZ;
     const double tau = a.tau;
     const double tau_skip = tau * (1.0 - 1e-12);
+#ifdef HXF_PROF_SCREEN
+    long long cyc[4] = {0, 0, 0, 0};  // staging, tables, phase 1, phase 2
+#define PROF_MARK(v) const long long v = clock64()
+#else
+#define PROF_MARK(v)
+#endif
     for (int64_t t = a.t0 + gw; t < a.t1; t += Wt) {
+        PROF_MARK(c_start);
         const uint64_t task = a.tasks[t];
         const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
                   sig = (task >> 45) & 0x7fff;
@@ -372,6 +379,8 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
                 sm.pm[g][i] = a.pmax[(int64_t)(rs[g] + x) * a.ns + cs[g] + y];
             }
         }
+        __syncwarp();
+        PROF_MARK(c_staged);
         // ket rows: L_k = ket pairs with row shell k (contiguous in the pair order)
         if (lane < nlam) {
             const int k = lane;
@@ -413,6 +422,10 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
             }
         }
         __syncwarp();
+        PROF_MARK(c_tables);
+#ifdef HXF_PROF_SCREEN
+        long long c_flush = 0;
+#endif
         // ---- phase 1: triples (a, k); phase 2: queued triples x l, exact tests
         int qn = 0;
         const int ntrip = ma * nlam;
@@ -508,13 +521,28 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
             qn += __popc(bal);
             __syncwarp();
             if (qn >= 32) {
+                PROF_MARK(f0);
                 flush(qn);
                 qn = 0;
                 __syncwarp();
+#ifdef HXF_PROF_SCREEN
+                c_flush += clock64() - f0;
+#endif
             }
         }
-        if (qn) flush(qn);
-        __syncwarp();
+        {
+            PROF_MARK(f1);
+            if (qn) flush(qn);
+            __syncwarp();
+#ifdef HXF_PROF_SCREEN
+            c_flush += clock64() - f1;
+            const long long c_end = clock64();
+            cyc[0] += c_staged - c_start;
+            cyc[1] += c_tables - c_staged;
+            cyc[2] += c_end - c_tables - c_flush;
+            cyc[3] += c_flush;
+#endif
+        }
     }
     if (EMIT) slab_pad(slab, a, lane);
     n_eri = warp_sum_ll(n_eri);
@@ -522,6 +550,9 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
     n_tie = warp_sum_ll(n_tie);
     ledger = warp_sum(ledger);
     if (lane == 0) {
+#ifdef HXF_PROF_SCREEN
+        for (int k = 0; k < 4; ++k) atomic_add_ll(&a.counters[C_DBG0 + k], cyc[k]);
+#endif
         if (n_eri) atomic_add_ll(&a.counters[C_ERIQ], n_eri);
         if (n_cull) atomic_add_ll(&a.counters[C_CULL_LEAF], n_cull);
         if (n_tie) atomic_add_ll(&a.counters[C_TIE_LEAF], n_tie);
@@ -557,6 +588,10 @@ struct EriArgs {
 
 __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double v) {
     if (v == 0.0) return;
+#ifdef HXF_EXP_NOATOM  // timing experiment: no K traffic (results wrong)
+    if (v == 1.2345) e.K[0] = 1;
+    return;
+#endif
     k_fixed_add(e.K + 2 * ((int64_t)row * e.nfn + col), v, e.S);
 }
 
@@ -582,7 +617,11 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) <= 1 ? 3 : 2) k_eri(E
             double3 A{0, 0, 0}, B{0, 0, 0}, C{0, 0, 0}, D{0, 0, 0};
             if (LA | LB) { A = e.ctr[e.bpi[pb]]; B = e.ctr[e.bpj[pb]]; }
             if (LC | LD) { C = e.ctr[e.kpi[pk]]; D = e.ctr[e.kpj[pk]]; }
+#ifdef HXF_EXP_NOPRIM  // timing experiment: skip the primitive loops (results wrong)
+            for (int q = 0; q < NI * NJ * NK * NL; ++q) out[q] = e.bpp[ib.z].c * e.kpp[ik.z].c;
+#else
             E::eval(e.bpp + ib.z, nb, e.kpp + ik.z, nk, A, B, C, D, s_tab, out);
+#endif
             const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
             const int64_t n = e.nfn;
             const double* P = e.P;
@@ -1356,6 +1395,11 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         c.class_prim_quartets[k] = acc_c[C_CLSPQ0 + k];
     }
     c.culled_bound_ledger = fx_to_double<LEDGER_LIMBS>(acc_l, LEDGER_SCALE);
+#ifdef HXF_PROF_SCREEN
+    fprintf(stderr, "screen cycles (warp-summed): staging %.3e tables %.3e phase1 %.3e phase2 %.3e\n",
+            (double)acc_c[C_DBG0], (double)acc_c[C_DBG0 + 1], (double)acc_c[C_DBG0 + 2],
+            (double)acc_c[C_DBG0 + 3]);
+#endif
     return HXF_OK;
 }
 
