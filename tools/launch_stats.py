@@ -18,7 +18,8 @@ for r in rows:
     name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
     v = float(d["Metric Value"].replace(",", ""))
     unit = d["Metric Unit"]
-    v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1.0)
+    v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+          "second": 1e3, "s": 1e3}.get(unit, 1.0)
     agg[name][0] += 1
     agg[name][1] += v
 tot = sum(v[1] for v in agg.values())
