@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
         const int mb = kdiag ? nlam * (nlam + 1) / 2 : nlam * nsig;
         const float inv_nnu = 1.0f / nnu, inv_nsig = 1.0f / nsig, inv_nlam = 1.0f / nlam;
         // ---- stage pair factors
+#pragma unroll 1
         for (int i = lane; i < ma; i += 32) {
             int x, y;
             if (bdiag) tri_decode(i, nmu, &x, &y);
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
             sm.apl[i] = x * nnu + y;
             sm.acl[i] = a.metab[pid];
         }
+#pragma unroll 1
         for (int i = lane; i < mb; i += 32) {
             int x, y;
             if (kdiag) tri_decode(i, nlam, &x, &y);
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
         for (int g = 0; g < Smem2<SYM>::NG; ++g) {
             if (!((live >> g) & 1)) continue;
             const float inv = 1.0f / cn[g];
+#pragma unroll 1
             for (int i = lane; i < rn[g] * cn[g]; i += 32) {
                 const int x = fdiv(i, cn[g], inv), y = i - x * cn[g];
                 sm.pm[g][i] = a.pmax[(int64_t)(rs[g] + x) * a.ns + cs[g] + y];
@@ -406,11 +409,13 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
             for (int h = 0; h < 2; ++h) {
                 const int g = 2 + h;
                 if (!((live >> g) & 1)) continue;
+#pragma unroll 1
                 for (int i = lane; i < rn[g] * nlam; i += 32) {
                     const int r = fdiv(i, nlam, inv_nlam), k = i - r * nlam;
                     const int st = kdiag ? k * nlam - k * (k - 1) / 2 : k * nsig;
                     const int n = kdiag ? nlam - k : nsig;
                     double s = 0.0, zm = 0.0;
+#pragma unroll 1
                     for (int b = st; b < st + n; ++b) {
                         const double pv = sm.pm[g][r * nsig + sm.by[b]];
                         s += pv * sm.sb[b];
@@ -433,6 +438,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
         const int per = 32 / Wl;                  // triples per phase-2 pass
         const int my_e = lane / Wl, my_l = lane - my_e * Wl;
         auto flush = [&](int count) {
+#pragma unroll 1
             for (int e0 = 0; e0 < count; e0 += per) {
                 const int e = e0 + my_e;
                 bool keep_any = false;
@@ -481,11 +487,13 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
                 }
             }
         };
-        for (int t0 = 0; t0 < ntrip; t0 += 32) {
+        // one flush call site keeps the kernel's code small (instruction cache)
+        for (int t0 = 0;; t0 += 32) {
+            const bool more = t0 < ntrip;
             const int tt = t0 + lane;
             bool pass = false;
             int ia = 0, k = 0;
-            if (tt < ntrip) {
+            if (more && tt < ntrip) {
                 ia = fdiv(tt, nlam, inv_nlam);
                 k = tt - ia * nlam;
                 const double fa = sm.fa[ia], sa = sm.sa[ia], fm = sm.fbmax[k];
@@ -520,7 +528,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
             if (pass) sm.queue[qn + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)((ia << 4) | k);
             qn += __popc(bal);
             __syncwarp();
-            if (qn >= 32) {
+            if (qn >= 32 || (!more && qn > 0)) {
                 PROF_MARK(f0);
                 flush(qn);
                 qn = 0;
@@ -529,13 +537,10 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
                 c_flush += clock64() - f0;
 #endif
             }
+            if (!more) break;
         }
         {
-            PROF_MARK(f1);
-            if (qn) flush(qn);
-            __syncwarp();
 #ifdef HXF_PROF_SCREEN
-            c_flush += clock64() - f1;
             const long long c_end = clock64();
             cyc[0] += c_staged - c_start;
             cyc[1] += c_tables - c_staged;
