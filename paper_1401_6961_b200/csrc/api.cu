@@ -115,8 +115,10 @@ int hxf_system_create(int device, int ns, const double* centers, const int* l, c
             if (n > 32767) throw HxfError{HXF_EINVAL, "more than 32767 spans on one partition level"};
         }
         s->n_leaves = s->h_off[D + 1] - s->h_off[D];
+        s->max_leaf_shells = 0;
         for (int k = s->h_off[D]; k < s->h_off[D + 1]; ++k) {
             s->h_leaf_id[k] = k - s->h_off[D];
+            s->max_leaf_shells = std::max(s->max_leaf_shells, s->h_shi[k] - s->h_slo[k]);
             if (s->h_shi[k] - s->h_slo[k] > 10)
                 throw HxfError{HXF_EINVAL, "leaf spans hold at most 10 shells on the device path"};
         }

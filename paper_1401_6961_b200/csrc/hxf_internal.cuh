@@ -68,7 +68,7 @@ struct DevBasis {
 // Device state handles (opaque to C callers).
 struct hxf_system {
     int device;
-    int ns, nfn, n_levels, n_leaves, max_span;
+    int ns, nfn, n_levels, n_leaves, max_span, max_leaf_shells;
     std::vector<int> h_off, h_slo, h_shi, h_flo, h_fhi, h_kid0, h_kid1, h_leaf_id, h_l, h_poff,
         h_fn, h_nf;
     std::vector<int64_t> node_off;  // per level offset of dense node arrays (n_L^2)

@@ -284,33 +284,38 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
 // per-quartet sum).  Passing triples go to a per-warp queue whose entries
 // are expanded lane-parallel into exact per-quartet tests.
 
-template <bool SYM>
+// MS = max shells per leaf span of the system (8 for every BASELINE p-shell
+// config, 10 for all-s systems at leaf size 10): smaller per-warp staging
+// means more resident warps to hide the staging loads.
+template <bool SYM, int MS>
 struct Smem2 {
-    static constexpr int NG = SYM ? 4 : 1;
-    double fa[MAXP], sa[MAXP], fb[MAXP], sb[MAXP];
-    double pm[NG][MAXP];
-    double w[SYM ? 2 : 1][SYM ? MAXP : 1];    // g2/g3 row ledgers: sum_{b in L_k} pm_g[r, l(b)] sb[b]
-    double fbmax[MAXS], sbsum[MAXS];
-    double z[SYM ? 2 : 1][SYM ? MAXP : 1];    // g2/g3: max_{b in L_k} pm_g[r, l(b)] f_b
-    unsigned char ax[MAXP], ay[MAXP], acl[MAXP], bx[MAXP], by[MAXP], bcl[MAXP];
-    unsigned short apl[MAXP], bpl[MAXP];
-    unsigned char bstart[MAXS], nl[MAXS];
+    static constexpr int NG = SYM ? 4 : 1, MP = MS * MS;
+    double fa[MP], sa[MP], fb[MP], sb[MP];
+    double pm[NG][MP];
+    double w[SYM ? 2 : 1][SYM ? MP : 1];    // g2/g3 row ledgers: sum_{b in L_k} pm_g[r, l(b)] sb[b]
+    double fbmax[MS], sbsum[MS];
+    double z[SYM ? 2 : 1][SYM ? MP : 1];    // g2/g3: max_{b in L_k} pm_g[r, l(b)] f_b
+    unsigned char ax[MP], ay[MP], acl[MP], bx[MP], by[MP], bcl[MP];
+    unsigned short apl[MP], bpl[MP];
+    unsigned char bstart[MS], nl[MS];
     unsigned short queue[64];
 };
 
-template <bool SYM>
-constexpr int screen2_warps() { return SYM ? 4 : 8; }  // static smem <= 48 KB
+template <bool SYM, int MS>
+constexpr int screen2_warps() {  // static smem <= 48 KB per block
+    return MS <= 8 ? (SYM ? 6 : 12) : (SYM ? 4 : 8);
+}
 
 __device__ __forceinline__ int fdiv(int a, int n, float inv) {
     return __float2int_rz(((float)a + 0.5f) * inv);  // exact for a < 2^20, n <= 32
 }
 
-template <bool SYM, bool EMIT>
-__global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArgs a) {
-    constexpr int NW = screen2_warps<SYM>();
-    __shared__ Smem2<SYM> sm_all[NW];
+template <bool SYM, bool EMIT, int MS>
+__global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(ScreenArgs a) {
+    constexpr int NW = screen2_warps<SYM, MS>();
+    __shared__ Smem2<SYM, MS> sm_all[NW];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    Smem2<SYM>& sm = sm_all[wid];
+    Smem2<SYM, MS>& sm = sm_all[wid];
     const int64_t gw = blockIdx.x * (int64_t)NW + wid;
     const int64_t Wt = (int64_t)gridDim.x * NW;
     long long n_eri = 0, n_cull = 0, n_tie = 0;
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
         const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
         const int cs[4] = {slam, slam, ssig, ssig}, cn[4] = {nlam, nlam, nsig, nsig};
 #pragma unroll
-        for (int g = 0; g < Smem2<SYM>::NG; ++g) {
+        for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
             if (!((live >> g) & 1)) continue;
             const float inv = 1.0f / cn[g];
 #pragma unroll 1
@@ -453,7 +458,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
                         const int x = sm.ax[ia], y = sm.ay[ia], z = sm.bx[ib], w = sm.by[ib];
                         const int rowv[4] = {y, x, y, x}, colv[4] = {z, z, w, w};
 #pragma unroll
-                        for (int g = 0; g < Smem2<SYM>::NG; ++g) {
+                        for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
                             if (!((live >> g) & 1)) continue;
                             const double pm = sm.pm[g][rowv[g] * cn[g] + colv[g]];
                             const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
@@ -501,7 +506,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM>() * 32) k_screen2(ScreenArg
                 double lsum = 0.0;
                 int ncul = 0;
 #pragma unroll
-                for (int g = 0; g < Smem2<SYM>::NG; ++g) {
+                for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
                     if (!((live >> g) & 1)) continue;
                     double ub, led;
                     if (g < 2) {
@@ -1149,7 +1154,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     // slower than thread-per-quartet on c3/c4; kept as an A/B variant)
     const char* ev = getenv("HXF_ERI");
     const bool use_bp = ev && !strcmp(ev, "bp");
-    const int sw = flat ? SCREEN_WARPS : (sym ? screen2_warps<true>() : screen2_warps<false>());
+    const bool ms8 = s->max_leaf_shells <= 8;
+    const int sw = flat ? SCREEN_WARPS
+                        : (ms8 ? (sym ? screen2_warps<true, 8>() : screen2_warps<false, 8>())
+                               : (sym ? screen2_warps<true, 10>() : screen2_warps<false, 10>()));
     const unsigned screen_grid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * (sym ? 12 : 8)));
     auto launch_screen = [&](bool emit) {
@@ -1157,8 +1165,14 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             if (sym) { if (emit) k_screen<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
             else { if (emit) k_screen<false, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<false, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
         } else {
-            if (sym) { if (emit) k_screen2<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen2<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
-            else { if (emit) k_screen2<false, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen2<false, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
+            const dim3 g(screen_grid), b(sw * 32);
+            if (ms8) {
+                if (sym) { if (emit) k_screen2<true, true, 8><<<g, b, 0, st>>>(sa); else k_screen2<true, false, 8><<<g, b, 0, st>>>(sa); }
+                else { if (emit) k_screen2<false, true, 8><<<g, b, 0, st>>>(sa); else k_screen2<false, false, 8><<<g, b, 0, st>>>(sa); }
+            } else {
+                if (sym) { if (emit) k_screen2<true, true, 10><<<g, b, 0, st>>>(sa); else k_screen2<true, false, 10><<<g, b, 0, st>>>(sa); }
+                else { if (emit) k_screen2<false, true, 10><<<g, b, 0, st>>>(sa); else k_screen2<false, false, 10><<<g, b, 0, st>>>(sa); }
+            }
         }
         note_launch();
     };
