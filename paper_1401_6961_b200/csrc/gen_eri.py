@@ -112,19 +112,17 @@ def prim_body(w, la, lb, lc, ld, accs, ind):
     L = la + lb + lc + ld
     p = " " * ind
     w(p + "const double ps = bp.p + kp.p;")
-    w(p + "const double r = rsqrt(ps);")
+    w(p + "const double r = rsqrt_pos(ps);")
     w(p + "const double r2 = r * r;")
     w(p + "const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;")
     w(p + "const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
     w(p + "const double T = bp.p * kp.p * r2 * R2;")
     w(p + "const double pref = bp.c * kp.c * r;")
-    if L == 0:
-        w(p + "const double bm0 = pref * boys_f0(T, tab);")
-    else:
-        w(p + f"double F[{L + 1}];")
-        w(p + f"boys_fm<{L}>(T, F, tab);")
-        for m in range(L + 1):
-            w(p + f"const double bm{m} = pref * F[{m}];")
+    w(p + f"double F[{L + 1}];")
+    w(p + f"boys_bf<{L}>(T, F, tab);")
+    for m in range(L + 1):
+        w(p + f"const double bm{m} = pref * F[{m}];")
+    if L > 0:
         if la + lb > 0:
             w(p + "const double rp = kp.p * r2;")
             w(p + "const double WPx = -rp * PQx, WPy = -rp * PQy, WPz = -rp * PQz;")

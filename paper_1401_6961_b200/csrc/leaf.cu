@@ -911,6 +911,7 @@ void launch_eri_bp(const EriArgs& e, int G, cudaStream_t st) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_eri_bp<A, B, C, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BOYS_TAB_BYTES);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri_bp<A, B, C, D>, 256, BOYS_TAB_BYTES);
         per_sm = std::max(per_sm, 1);
     }
@@ -1011,6 +1012,7 @@ void launch_eri(const EriArgs& e, cudaStream_t st) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_eri<A, B, C, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BOYS_TAB_BYTES);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri<A, B, C, D>, 128, BOYS_TAB_BYTES);
         per_sm = std::max(per_sm, 1);
     }
