@@ -107,10 +107,20 @@ class Gen:
         return v
 
 
-def prim_body(w, la, lb, lc, ld, accs, ind):
+def prim_body(w, la, lb, lc, ld, accs, ind, fold=False):
     """Statements for one primitive quartet (bp, kp in scope)."""
     L = la + lb + lc + ld
     p = " " * ind
+    if L == 0 and fold:  # (ss|ss): bra coefficient applied once per bra primitive (accb)
+        w(p + "const double ps = bp.p + kp.p;")
+        w(p + "const double r = rsqrt_pos(ps);")
+        w(p + "const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;")
+        w(p + "const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
+        w(p + "const double T = bp.p * kp.p * (r * r) * R2;")
+        w(p + "double F[1];")
+        w(p + "boys_bf<0>(T, F, tab);")
+        w(p + "accb = fma(kp.c * r, F[0], accb);")
+        return
     w(p + "const double ps = bp.p + kp.p;")
     w(p + "const double r = rsqrt_pos(ps);")
     w(p + "const double r2 = r * r;")
@@ -175,11 +185,15 @@ def gen_class(la, lb, lc, ld):
         if la + lb > 0:
             w("        const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
             w("        const double o2p = 0.5 * bp.ip;")
+        if L == 0:
+            w("        double accb = 0.0;")
         w("#pragma unroll")
         w("        for (int ik = 0; ik < NKC; ++ik) {")
         w("          const PrimPair& kp = kq[ik];")
-        prim_body(w, la, lb, lc, ld, accs, 10)
+        prim_body(w, la, lb, lc, ld, accs, 10, fold=True)
         w("        }")
+        if L == 0:
+            w("        acc_000_000 = fma(bp.c, accb, acc_000_000);")
         w("      }")
         w("    } else {")
     w("      for (int ib = 0; ib < nb; ++ib) {")
@@ -188,11 +202,15 @@ def gen_class(la, lb, lc, ld):
         w("        const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
         w("        const double o2p = 0.5 * bp.ip;")
     w("        PrimPair kn = load_pp(ket);")
+    if L == 0:
+        w("        double accb = 0.0;")
     w("        for (int ik = 0; ik < nk; ++ik) {")
     w("          const PrimPair kp = kn;")
     w("          if (ik + 1 < nk) kn = load_pp(ket + ik + 1);  // prefetch: hide the L1/L2 latency")
-    prim_body(w, la, lb, lc, ld, accs, 10)
+    prim_body(w, la, lb, lc, ld, accs, 10, fold=True)
     w("        }")
+    if L == 0:
+        w("        acc_000_000 = fma(bp.c, accb, acc_000_000);")
     w("      }")
     if cached:
         w("    }")

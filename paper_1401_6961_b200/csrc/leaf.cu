@@ -606,7 +606,7 @@ __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double
 }
 
 template <int LA, int LB, int LC, int LD>
-__global__ void __launch_bounds__(128, (LA + LB + LC + LD) <= 1 ? 3 : 2) k_eri(EriArgs e) {
+__global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? 3 : 2) k_eri(EriArgs e) {
     typedef Eri<LA, LB, LC, LD> E;
     constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL;
     extern __shared__ __align__(16) double s_tab[];
@@ -684,110 +684,6 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) <= 1 ? 3 : 2) k_eri(E
         atomic_add_ll(&e.counters[C_CLSQ0 + CLS], nq);
     }
 }
-
-// ---------------------------------------------------------------------------
-// Experimental, disabled: measured 1.6x slower than the register-cached
-// thread-per-quartet kernel on c3 (integer index overhead, IPC-bound).
-#if 0
-// (ss|ss): primitive-parallel.  Survivors are sorted by (class, nb, nk), so a
-// segment has a uniform primitive-quartet count S = nb*nk.  A group of
-// G = min(S, 32) lanes owns one shell quartet, each lane one (or, for S > 32,
-// every 32nd) primitive quartet; loads of the pair's primitive records are
-// near-coalesced and every lane holds little state (high occupancy).  The
-// group sum uses a fixed shuffle tree that depends only on G, so results do
-// not depend on where the quartet lands in the warp (bitwise reproducible).
-
-struct SegDesc {
-    int64_t begin, end, wbegin;
-    int nb, nk;
-};
-
-__global__ void __launch_bounds__(256) k_eri_ssss(EriArgs e, const SegDesc* __restrict__ segs,
-                                                  int nseg, int64_t total_w) {
-    extern __shared__ __align__(16) double s_tab[];
-    boys_table_to_smem(s_tab, 0);
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    long long nprim = 0, nq = 0;
-    for (int64_t wt = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); wt < total_w;
-         wt += nwarps) {
-        int lo = 0, hi = nseg - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (segs[mid].wbegin <= wt) lo = mid;
-            else hi = mid - 1;
-        }
-        const SegDesc sd = segs[lo];
-        const int nk = sd.nk, S = sd.nb * sd.nk;
-        int G, g, rounds;
-        int64_t r;
-        if (S <= 32) {
-            G = S;
-            const int RW = 32 / G;
-            g = lane % G;
-            r = (lane < RW * G) ? sd.begin + (wt - sd.wbegin) * RW + lane / G : sd.end;
-            rounds = 1;
-        } else {
-            G = 32;
-            g = lane;
-            r = sd.begin + (wt - sd.wbegin);
-            rounds = (S + 31) >> 5;
-        }
-        const bool act = r < sd.end;
-        double v = 0.0;
-        int mask = 0;
-        int4 ib = make_int4(0, 0, 0, 0), ik = make_int4(0, 0, 0, 0);
-        if (act) {
-            const uint64_t rec = e.rec[r];
-            mask = (int)((rec >> 56) & 0xf);
-            ib = __ldg(e.binfo + (int64_t)(rec & 0xfffffff));
-            ik = __ldg(e.kinfo + (int64_t)((rec >> 28) & 0xfffffff));
-            for (int rd = 0; rd < rounds; ++rd) {
-                const int p = g + 32 * rd;
-                if (p < S) {
-                    const int a = p / nk, k = p - a * nk;
-                    const PrimPair bp = load_pp(e.bpp + ib.z + a), kp = load_pp(e.kpp + ik.z + k);
-                    const double ps = bp.p + kp.p;
-                    const double rr = rsqrt(ps);
-                    const double r2 = rr * rr;
-                    const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;
-                    const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;
-                    const double T = bp.p * kp.p * r2 * R2;
-                    v += bp.c * kp.c * rr * boys_f0(T, s_tab);
-                }
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double o = __shfl_down_sync(0xffffffffu, v, off);
-            if (g + off < G) v += o;
-        }
-        const double eri = __shfl_sync(0xffffffffu, v, lane - g);
-        if (act) {
-            if (g == 0) {
-                nq += 1;
-                nprim += S;
-            }
-            // slot s (exchange_symmetry.py:345-361; naive = slot 0):
-            //   0 K[i,l] P[j,k]   1 K[j,l] P[i,k]   2 K[i,k] P[j,l]   3 K[j,k] P[i,l]
-            for (int s = g; s < 4; s += G) {
-                if (!((mask >> s) & 1)) continue;
-                const int row = (s & 1) ? ib.y : ib.x, col = (s & 2) ? ik.x : ik.y;
-                const int pr = (s & 1) ? ib.x : ib.y, pc = (s & 2) ? ik.y : ik.x;
-                k_add(e, row, col, -0.5 * (__ldg(e.P + (int64_t)pr * e.nfn + pc) * eri));
-            }
-        }
-    }
-    nq = warp_sum_ll(nq);
-    nprim = warp_sum_ll(nprim);
-    if (lane == 0 && nprim) {
-        atomic_add_ll(&e.counters[C_PRIMQ], nprim);
-        atomic_add_ll(&e.counters[C_CLSPQ0], nprim);
-        atomic_add_ll(&e.counters[C_CLSQ0], nq);
-    }
-}
-
-#endif
 
 // ---------------------------------------------------------------------------
 // Light classes (L <= 1): bra-primitive parallel.  Launched per sub-segment of
