@@ -88,6 +88,15 @@ typedef struct hxf_exchange_opts {
     int32_t* quartet_log;   /* NULL or 4*capacity int32 (host) */
     int64_t log_capacity;
     int64_t* log_count;     /* out: quartets logged (may exceed capacity) */
+    /* Order-independent digest of the evaluated quartet set (SURVEY.md 8(c)
+       item 2: full-size parity without a materialised log).  NULL, or host
+       uint64[3] = {count, sum h(q), sum h(h(q))} mod 2^64 over the evaluated
+       tuples q = (i,j,k,l) (the quartet_log tuples) with i % digest_mod ==
+       digest_rem; h = SplitMix64 finaliser of ((i*ns + j)*ns + k)*ns + l.
+       Filled only when evaluate != 0. */
+    uint64_t* digest;
+    int digest_mod;    /* <= 1: every quartet */
+    int digest_rem;
 } hxf_exchange_opts;
 
 const char* hxf_last_error(void);
@@ -122,6 +131,9 @@ int hxf_density_build(hxf_system* sys, const double* P, int P_on_device, double 
 void hxf_density_destroy(hxf_density* dens);
 /* node norms of one level, -1 where the node is absent. */
 int hxf_density_download(const hxf_density* dens, int level, double* norm);
+/* max |P| over each shell block (the per-quartet bound's density factor for
+ * p shells), n_shells^2 row-major. */
+int hxf_density_download_pmax(const hxf_density* dens, double* pmax);
 
 int hxf_exchange(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* opts,
                  double* K_out, hxf_counters* counters, void* stream);

@@ -21,7 +21,7 @@ NCASES = 9
 EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_destroy",
             "hxf_system_info", "hxf_pairs_build", "hxf_pairs_destroy", "hxf_pairs_download",
             "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
-            "hxf_density_destroy", "hxf_density_download", "hxf_exchange", "hxf_frontier",
+            "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_frontier",
             "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count")
 
 
@@ -62,7 +62,10 @@ class ExchangeOpts(ctypes.Structure):
                 ("shard_end", ctypes.c_int64),
                 ("quartet_log", ctypes.POINTER(ctypes.c_int32)),
                 ("log_capacity", ctypes.c_int64),
-                ("log_count", ctypes.POINTER(ctypes.c_int64))]
+                ("log_count", ctypes.POINTER(ctypes.c_int64)),
+                ("digest", ctypes.POINTER(ctypes.c_uint64)),
+                ("digest_mod", ctypes.c_int),
+                ("digest_rem", ctypes.c_int)]
 
 
 _lib = None
@@ -95,6 +98,7 @@ def lib():
     L.hxf_density_destroy.argtypes = [vp]
     L.hxf_density_destroy.restype = None
     L.hxf_density_download.argtypes = [vp, i32, vp]
+    L.hxf_density_download_pmax.argtypes = [vp, vp]
     L.hxf_exchange.argtypes = [vp, vp, vp, P(ExchangeOpts), vp, P(Counters), vp]
     L.hxf_frontier.argtypes = [vp, vp, vp, dbl, i32, i32, i32, P(i64), vp, i64, vp]
     L.hxf_last_timings.argtypes = [vp, i32]

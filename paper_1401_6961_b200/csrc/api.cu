@@ -292,6 +292,15 @@ int hxf_density_download(const hxf_density* d, int level, double* norm) {
     })
 }
 
+int hxf_density_download_pmax(const hxf_density* d, double* pmax) {
+    HXF_TRY({
+        if (!d || !pmax) throw HxfError{HXF_EINVAL, "NULL argument"};
+        const hxf_system* s = d->sys;
+        set_device(s->device);
+        HXF_CUDA(cudaMemcpy(pmax, d->pmax, (size_t)s->ns * s->ns * sizeof(double), cudaMemcpyDeviceToHost));
+    })
+}
+
 int hxf_exchange(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* opts,
                  double* K_out, hxf_counters* counters, void* stream) {
     HXF_TRY({

@@ -859,6 +859,40 @@ __global__ void k_log(const uint64_t* rec, int64_t n, const int* bpi, const int*
     }
 }
 
+// SplitMix64 finaliser (basis.py:112-136 mixes the same way)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// order-independent digest of the evaluated tuples (the k_log tuples)
+__global__ void k_digest(const uint64_t* rec, int64_t n, const int* bpi, const int* bpj, const int* kpi,
+                         const int* kpj, uint64_t ns, int mod, int rem, unsigned long long* dg) {
+    unsigned long long c = 0, h1 = 0, h2 = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = rec[t];
+        if (r == SENTINEL_REC) continue;
+        const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
+        const uint64_t i = bpi[pb];
+        if (mod > 1 && (int)(i % (uint64_t)mod) != rem) continue;
+        const uint64_t h = mix64(((i * ns + (uint64_t)bpj[pb]) * ns + (uint64_t)kpi[pk]) * ns + (uint64_t)kpj[pk]);
+        c += 1;
+        h1 += h;
+        h2 += mix64(h);
+    }
+    c = (unsigned long long)warp_sum_ll((long long)c);
+    h1 = (unsigned long long)warp_sum_ll((long long)h1);
+    h2 = (unsigned long long)warp_sum_ll((long long)h2);
+    if ((threadIdx.x & 31) == 0 && c) {
+        atomicAdd(dg + 0, c);
+        atomicAdd(dg + 1, h1);
+        atomicAdd(dg + 2, h2);
+    }
+}
+
 __global__ void k_fx_to_double(const unsigned long long* Kfx, int64_t n2, int S, double* K) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2;
          t += (int64_t)gridDim.x * blockDim.x)
@@ -1092,6 +1126,13 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         HXF_CUDA(cudaMemsetAsync(dlogfill, 0, sizeof(unsigned long long), st));
     }
 
+    unsigned long long* ddigest = nullptr;
+    const bool want_digest = o->digest != nullptr && o->evaluate;
+    if (want_digest) {
+        ddigest = lalloc<unsigned long long>(3, st);
+        HXF_CUDA(cudaMemsetAsync(ddigest, 0, 3 * sizeof(unsigned long long), st));
+    }
+
     long long* scount = lalloc<long long>(C_NCOUNTERS, st);
     unsigned long long* sledger = lalloc<unsigned long long>(LEDGER_LIMBS, st);
     unsigned long long* dfill = lalloc<unsigned long long>(1, st);
@@ -1221,6 +1262,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                 if (want_log)
                     { k_log<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(rec2, nrec, bra->pi, bra->pj, ket->pi,
                                                                         ket->pj, dlog, o->log_capacity, dlogfill); note_launch(); }
+                if (want_digest)
+                    { k_digest<<<(unsigned)std::min<int64_t>((nrec + 255) / 256, 4096), 256, 0, st>>>(
+                          rec2, nrec, bra->pi, bra->pj, ket->pi, ket->pj, (uint64_t)s->ns, o->digest_mod,
+                          o->digest_rem, ddigest); note_launch(); }
             }
             long long c2[C_NCOUNTERS];
             unsigned long long l2[LEDGER_LIMBS];
@@ -1280,6 +1325,15 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         cudaFreeAsync(dlogfill, st);
     }
     if (o->log_count) *o->log_count = logged;
+    if (o->digest) {
+        unsigned long long hd[3] = {0, 0, 0};
+        if (want_digest) {
+            HXF_CUDA(cudaMemcpyAsync(hd, ddigest, sizeof(hd), cudaMemcpyDeviceToHost, st));
+            HXF_CUDA(cudaStreamSynchronize(st));
+            cudaFreeAsync(ddigest, st);
+        }
+        for (int k = 0; k < 3; ++k) o->digest[k] = hd[k];
+    }
     for (void* p : {(void*)Kfx, (void*)scount, (void*)sledger, (void*)dfill, (void*)dcount,
                     (void*)dledger, (void*)d_lslo, (void*)d_lshi, (void*)tr.leaf})
         if (p) cudaFreeAsync(p, st);

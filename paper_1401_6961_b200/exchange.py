@@ -225,11 +225,14 @@ def _require_root(node, what):
 
 
 def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log=None,
-                 K_out=None, shard=None, symmetrize=True):
+                 K_out=None, shard=None, symmetrize=True, digest=None, digest_sample=(1, 0)):
     """Low-level call of hxf_exchange.
 
     K_out: None (return a new host array), or a CUDA tensor (n x n float64)
     written in place on the device.  shard: None or (level, begin, end).
+    digest: None, or a caller-owned numpy uint64[3] filled with the
+    order-independent digest (count, sum h, sum h(h)) of the evaluated quartet
+    tuples with i % digest_sample[0] == digest_sample[1] (include/hxf.h).
     Returns (K or None, hxf counters struct, list of logged quartets or None).
     """
     if not (tau_2e >= 0.0):
@@ -253,6 +256,12 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
         opts.shard_level, opts.shard_begin, opts.shard_end = -1, 0, 0
     else:
         opts.shard_level, opts.shard_begin, opts.shard_end = shard
+    if digest is not None:
+        if not (isinstance(digest, np.ndarray) and digest.dtype == np.uint64 and digest.shape == (3,)
+                and digest.flags.c_contiguous):
+            raise InvalidArgumentError("digest must be a contiguous numpy uint64[3]")
+        opts.digest = digest.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+        opts.digest_mod, opts.digest_rem = int(digest_sample[0]), int(digest_sample[1])
     log_count = ctypes.c_int64(0)
     cap = 0
     if quartet_log is not None and evaluate:

@@ -224,6 +224,13 @@ class _DensityTree:
             self._norms[level] = v
         return v
 
+    def pmax(self):
+        """max |P| over each shell block (n_shells x n_shells)."""
+        ns = self.ds.n_shells
+        v = np.empty(ns * ns)
+        _native.check(_native.lib().hxf_density_download_pmax(self.handle, _native.ptr(v)))
+        return v.reshape(ns, ns)
+
     def view(self, level, r, c):
         key = (level, r, c)
         v = self._views.get(key)
