@@ -31,10 +31,25 @@ def test_library_exports_every_symbol():
         assert hasattr(lib, name), name
 
 
-def test_struct_layouts_match_header():
-    # hxf_counters: 10 + 2*9 + 3 + 2*16 int64 + 1 double
-    assert ctypes.sizeof(_native.Counters) == (10 + 18 + 3 + 32) * 8 + 8
-    assert ctypes.sizeof(_native.ExchangeOpts) == 8 + 5 * 4 + 4 + 8 + 8 + 8 + 8 + 8
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of hxf_counters / hxf_exchange_opts == the C compiler's layout."""
+    import subprocess
+    src = tmp_path / "layout.c"
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "hxf.h"', "int main(void) {"]
+    for cname, py in (("hxf_counters", _native.Counters), ("hxf_exchange_opts", _native.ExchangeOpts)):
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                 check=True).stdout.splitlines())
+    for cname, py in (("hxf_counters", _native.Counters), ("hxf_exchange_opts", _native.ExchangeOpts)):
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, (cname, f)
 
 
 def test_version():
