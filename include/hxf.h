@@ -138,6 +138,17 @@ int hxf_density_download_pmax(const hxf_density* dens, double* pmax);
 int hxf_exchange(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* opts,
                  double* K_out, hxf_counters* counters, void* stream);
 
+/* Direct-SCF twin (dense_exchange_screened, oracle.py:69-108; SURVEY.md 8(f)
+ * f1): every ordered shell quartet of live pairs with
+ * (f(Q_ij) |P|_jk) f(Q_kl) > tau_2e, enumerated without the hierarchy and
+ * evaluated by the same ERI stage into the same fixed-point K, so its K equals
+ * the naive hierarchical K bit for bit when the evaluated sets agree.  Uses
+ * opts->tau_2e, mode, evaluate, K_on_device, digest; digest_mod/digest_rem
+ * restrict the EVALUATED quartets to first shells i % mod == rem (sampled K
+ * rows).  Counters: eri_shell_quartets, prim_quartets and the class arrays. */
+int hxf_exchange_direct(hxf_pairs* pairs, hxf_density* P, const hxf_exchange_opts* opts,
+                        double* K_out, hxf_counters* counters, void* stream);
+
 /* Frontier size of the product tree at `level` (for multi-GPU shard
  * planning); also returns per-task cost estimates (descendant leaf count
  * proxy) when `cost` is non-NULL (host buffer of that size). */

@@ -21,7 +21,7 @@ NCASES = 9
 EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_destroy",
             "hxf_system_info", "hxf_pairs_build", "hxf_pairs_destroy", "hxf_pairs_download",
             "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
-            "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_frontier",
+            "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_exchange_direct", "hxf_frontier",
             "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count")
 
 
@@ -100,6 +100,7 @@ def lib():
     L.hxf_density_download.argtypes = [vp, i32, vp]
     L.hxf_density_download_pmax.argtypes = [vp, vp]
     L.hxf_exchange.argtypes = [vp, vp, vp, P(ExchangeOpts), vp, P(Counters), vp]
+    L.hxf_exchange_direct.argtypes = [vp, vp, P(ExchangeOpts), vp, P(Counters), vp]
     L.hxf_frontier.argtypes = [vp, vp, vp, dbl, i32, i32, i32, P(i64), vp, i64, vp]
     L.hxf_last_timings.argtypes = [vp, i32]
     L.hxf_symmetrize.argtypes = [vp, i32, dbl, vp]

@@ -311,6 +311,16 @@ int hxf_exchange(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_excha
     })
 }
 
+int hxf_exchange_direct(hxf_pairs* pairs, hxf_density* P, const hxf_exchange_opts* opts, double* K_out,
+                        hxf_counters* counters, void* stream) {
+    HXF_TRY({
+        if (!pairs || !P || !opts || !counters) throw HxfError{HXF_EINVAL, "NULL argument"};
+        set_device(pairs->sys->device);
+        memset(counters, 0, sizeof(*counters));
+        direct_run(pairs, P, opts, K_out, counters, (cudaStream_t)stream);
+    })
+}
+
 int hxf_frontier(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, double tau_2e, int mode, int symmetry,
                  int level, int64_t* n_tasks, double* cost, int64_t cost_capacity, void* stream) {
     HXF_TRY({

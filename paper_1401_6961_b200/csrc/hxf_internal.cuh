@@ -322,6 +322,8 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st);
 void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStream_t st);
 
 struct ExchangeCtx;
+int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, double* K_out,
+               hxf_counters* out, cudaStream_t st);
 int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* o,
                  double* K_out, hxf_counters* c, cudaStream_t st);
 int symmetrize_device(double* K, int n, double tol, cudaStream_t st);

@@ -965,6 +965,21 @@ void launch_eri_class(int cls, const EriArgs& e, cudaStream_t st) {
     }
 }
 
+thread_local double g_timings[8];
+
+struct SurvivorBufs {
+    uint64_t *rec, *rec2;
+    uint16_t *keys, *keys2;
+    void* sort_tmp;
+    size_t sort_tb;
+    int64_t* dbounds;
+};
+
+struct Timer;
+// sort one chunk of survivors by (class, nb, nk) and run the per-class ERI
+// kernels over rec2 (the sorted copy)
+void eri_sorted_stage(EriArgs e, const SurvivorBufs& b, int64_t nrec, bool use_bp, cudaStream_t st);
+
 struct Timer {
     cudaEvent_t a, b;
     cudaStream_t st;
@@ -984,7 +999,39 @@ struct Timer {
     }
 };
 
-thread_local double g_timings[8];
+void eri_sorted_stage(EriArgs e, const SurvivorBufs& b, int64_t nrec, bool use_bp, cudaStream_t st) {
+    size_t tb = b.sort_tb;
+    cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, 12, st);
+    { k_key_bounds<<<17, 256, 0, st>>>(b.keys2, nrec, b.dbounds); note_launch(); }
+    std::vector<int64_t> kbnd(4097);
+    HXF_CUDA(cudaMemcpyAsync(kbnd.data(), b.dbounds, 4097 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+    Timer tk(st);
+    for (int c = 0; c < 16; ++c) {
+        if (use_bp && __builtin_popcount(c) <= 1) {
+            // light class: one launch per bra primitive count (group size)
+            for (int nb = 1; nb <= 16; ++nb) {
+                const int64_t b0 = kbnd[(c << 8) | ((nb - 1) << 4)], b1 = kbnd[(c << 8) + (nb << 4)];
+                if (b1 <= b0) continue;
+                e.rec = b.rec2 + b0;
+                e.n = b1 - b0;
+                switch (c) {
+                    case 0: launch_eri_bp<0, 0, 0, 0>(e, nb, st); break;
+                    case 1: launch_eri_bp<0, 0, 0, 1>(e, nb, st); break;
+                    case 2: launch_eri_bp<0, 0, 1, 0>(e, nb, st); break;
+                    case 4: launch_eri_bp<0, 1, 0, 0>(e, nb, st); break;
+                    case 8: launch_eri_bp<1, 0, 0, 0>(e, nb, st); break;
+                }
+            }
+            continue;
+        }
+        e.rec = b.rec2 + kbnd[c << 8];
+        e.n = kbnd[(c + 1) << 8] - kbnd[c << 8];
+        launch_eri_class(c, e, st);
+    }
+    g_timings[5] += tk.stop();
+    HXF_CUDA(cudaGetLastError());
+}
 
 void host_ledger_add(unsigned long long* acc, const unsigned long long* v) {
     unsigned long long carry = 0;
@@ -1228,37 +1275,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             Timer teri(st);
             const int64_t nrec = (int64_t)fill;
             if (nrec) {
-                size_t tb = sort_tb;
-                cub::DeviceRadixSort::SortPairs(sort_tmp, tb, keys, keys2, rec, rec2, nrec, 0, 12, st);
-                { k_key_bounds<<<17, 256, 0, st>>>(keys2, nrec, dbounds); note_launch(); }
-                std::vector<int64_t> kbnd(4097);
-                HXF_CUDA(cudaMemcpyAsync(kbnd.data(), dbounds, 4097 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-                HXF_CUDA(cudaStreamSynchronize(st));
-                Timer tk(st);
-                for (int c = 0; c < 16; ++c) {
-                    if (use_bp && __builtin_popcount(c) <= 1) {
-                        // light class: one launch per bra primitive count (group size)
-                        for (int nb = 1; nb <= 16; ++nb) {
-                            const int64_t b0 = kbnd[(c << 8) | ((nb - 1) << 4)], b1 = kbnd[(c << 8) + (nb << 4)];
-                            if (b1 <= b0) continue;
-                            e.rec = rec2 + b0;
-                            e.n = b1 - b0;
-                            switch (c) {
-                                case 0: launch_eri_bp<0, 0, 0, 0>(e, nb, st); break;
-                                case 1: launch_eri_bp<0, 0, 0, 1>(e, nb, st); break;
-                                case 2: launch_eri_bp<0, 0, 1, 0>(e, nb, st); break;
-                                case 4: launch_eri_bp<0, 1, 0, 0>(e, nb, st); break;
-                                case 8: launch_eri_bp<1, 0, 0, 0>(e, nb, st); break;
-                            }
-                        }
-                        continue;
-                    }
-                    e.rec = rec2 + kbnd[c << 8];
-                    e.n = kbnd[(c + 1) << 8] - kbnd[c << 8];
-                    launch_eri_class(c, e, st);
-                }
-                g_timings[5] += tk.stop();
-                HXF_CUDA(cudaGetLastError());
+                SurvivorBufs sb{rec, rec2, keys, keys2, sort_tmp, sort_tb, dbounds};
+                eri_sorted_stage(e, sb, nrec, use_bp, st);
                 if (want_log)
                     { k_log<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(rec2, nrec, bra->pi, bra->pj, ket->pi,
                                                                         ket->pj, dlog, o->log_capacity, dlogfill); note_launch(); }
@@ -1371,6 +1389,324 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             (double)acc_c[C_DBG0], (double)acc_c[C_DBG0 + 1], (double)acc_c[C_DBG0 + 2],
             (double)acc_c[C_DBG0 + 3]);
 #endif
+    return HXF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Direct-SCF twin (the semantics of dense_exchange_screened,
+// oracle.py:69-108): every ordered shell quartet (i,j,k,l) of live pairs with
+// (f(Q_ij) |P|_jk) f(Q_kl) > tau, found without the hierarchy, evaluated by
+// the same sorted ERI stage into the same fixed-point K.  Because the K
+// accumulation is order-independent, the twin's K equals the hierarchical
+// naive K bit for bit exactly when both evaluate the same quartet set: the
+// full-size K parity check of SURVEY.md 8(c) item 2.
+//
+// Enumeration: per shell j the ket rows k sorted by |P|_jk descending, per
+// shell k the columns l sorted by f(Q_kl) descending (segmented radix sorts
+// of the dense n_shells^2 tables); one warp per bra pair walks its k list 32
+// at a time, each lane binary-searches the passing prefix of its l list
+// (binary64 products are monotone), and the walk stops at the first k whose
+// bound with max f(Q) cannot pass.  A count pass and an exclusive scan give
+// every bra pair its record range, so the emit pass writes without atomics.
+
+namespace {
+
+__global__ void k_direct_tables(int64_t n_pairs, const int* pi, const int* pj, const double* q,
+                                const double* sq, int schwarz, int ns, double* fq, int* pidm) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_pairs) return;
+    const int64_t x = (int64_t)pi[t] * ns + pj[t];
+    fq[x] = schwarz ? sq[t] : q[t];
+    pidm[x] = (int)t;
+}
+
+__global__ void k_iota_cols(int64_t n2, int ns, int* col, int64_t* row_off) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < n2) col[t] = (int)(t % ns);
+    if (t <= ns) row_off[t] = t * ns;
+}
+
+// entries > 0 per row of a row-wise descending-sorted table
+__global__ void k_row_nnz(const double* sorted, int ns, int* cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= ns) return;
+    const double* row = sorted + (int64_t)r * ns;
+    int lo = 0, hi = ns;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (row[mid] > 0.0) lo = mid + 1;
+        else hi = mid;
+    }
+    cnt[r] = lo;
+}
+
+struct DirectArgs {
+    int64_t n_pairs;
+    const int* pi;
+    const int* pj;
+    const uint8_t* meta;
+    const double* fq;   // n_shells^2, f(Q), 0 where absent
+    const int* pidm;    // n_shells^2, pair id, -1 where absent
+    const double* pm;   // n_shells^2, block max |P|
+    const int* lq;      // per k: l sorted by f(Q_kl) descending
+    const int* nq;
+    const int* lp;      // per j: k sorted by |P|_jk descending
+    const int* np;
+    int ns;
+    int mod, rem;
+    double tau, fqmax;
+    int64_t* count;        // count pass: records per bra pair
+    const int64_t* off;    // emit pass: record offsets (exclusive scan of count)
+    uint64_t* rec;
+    uint16_t* keys;
+};
+
+template <bool EMIT>
+__global__ void __launch_bounds__(256) k_direct(DirectArgs a, int64_t p0, int64_t p1) {
+    const int lane = threadIdx.x & 31;
+    const int64_t p = p0 + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+    if (p >= p1) return;
+    const int ia = a.pi[p], ib = a.pj[p];
+    int64_t wcount = 0;
+    if (a.mod <= 1 || ia % a.mod == a.rem) {
+        const int64_t ns = a.ns;
+        const double fab = a.fq[ia * ns + ib];
+        const int* krow = a.lp + ib * ns;
+        const int nk = a.np[ib];
+        const int ca = a.meta[p];
+        const int64_t base = EMIT ? a.off[p] - a.off[p0] : 0;
+        for (int c0 = 0; c0 < nk; c0 += 32) {
+            const int idx = c0 + lane;
+            int k = -1, n = 0;
+            double x = 0.0;
+            bool stop = idx >= nk;
+            if (!stop) {
+                k = krow[idx];
+                x = __dmul_rn(fab, a.pm[ib * ns + k]);
+                if (!(__dmul_rn(x, a.fqmax) > a.tau)) {
+                    stop = true;
+                    k = -1;
+                }
+            }
+            const int* lrow = a.lq + (int64_t)(k < 0 ? 0 : k) * ns;
+            if (k >= 0) {
+                int lo = 0, hi = a.nq[k];
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (__dmul_rn(x, a.fq[(int64_t)k * ns + lrow[mid]]) > a.tau) lo = mid + 1;
+                    else hi = mid;
+                }
+                n = lo;
+            }
+            int incl = n;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (EMIT) {
+                int64_t pos = base + wcount + incl - n;
+                for (int t = 0; t < n; ++t, ++pos) {
+                    const int pk = a.pidm[(int64_t)k * ns + lrow[t]];
+                    const int cb = a.meta[pk];
+                    const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
+                    a.rec[pos] = (uint64_t)p | ((uint64_t)pk << 28) | (1ull << 56) | (cls << 60);
+                    a.keys[pos] = (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2));
+                }
+            }
+            wcount += __shfl_sync(0xffffffffu, incl, 31);
+            if (__any_sync(0xffffffffu, stop)) break;
+        }
+    }
+    if (!EMIT && lane == 0) a.count[p] = wcount;
+}
+
+}  // namespace
+
+int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, double* K_out,
+               hxf_counters* out, cudaStream_t st) {
+    hxf_system* s = pairs->sys;
+    if (dens->sys != s) throw HxfError{HXF_EINVAL, "pairs and P must be built over the same partition"};
+    if (!(o->tau_2e >= 0.0)) throw HxfError{HXF_EINVAL, "tau_2e must be non-negative"};
+    if (o->mode != HXF_MODE_SCHWARZ && o->mode != HXF_MODE_LITERAL)
+        throw HxfError{HXF_EINVAL, "unknown screening mode"};
+    for (int k = 0; k < 8; ++k) g_timings[k] = 0.0;
+    Timer ttot(st);
+    const int ns = s->ns;
+    const int64_t n2 = (int64_t)ns * ns, nfn2 = (int64_t)s->nfn * s->nfn;
+    const int schwarz = o->mode == HXF_MODE_SCHWARZ;
+    const int mod = std::max(1, o->digest_mod), rem = o->digest_rem;
+
+    // ---- dense f(Q) / pair-id tables and the two row-sorted lists
+    Timer tprep(st);
+    double* fq = lalloc<double>(n2, st);
+    int* pidm = lalloc<int>(n2, st);
+    HXF_CUDA(cudaMemsetAsync(fq, 0, n2 * sizeof(double), st));
+    HXF_CUDA(cudaMemsetAsync(pidm, 0xff, n2 * sizeof(int), st));
+    { k_direct_tables<<<(unsigned)((pairs->n_pairs + 255) / 256), 256, 0, st>>>(
+          pairs->n_pairs, pairs->pi, pairs->pj, pairs->q, pairs->sq, schwarz, ns, fq, pidm); note_launch(); }
+    int* iota = lalloc<int>(n2, st);
+    int64_t* roff = lalloc<int64_t>(ns + 1, st);
+    { k_iota_cols<<<(unsigned)((std::max<int64_t>(n2, ns + 1) + 255) / 256), 256, 0, st>>>(n2, ns, iota, roff); note_launch(); }
+    double* skeys = lalloc<double>(n2, st);
+    int* lq = lalloc<int>(n2, st);
+    int* lp = lalloc<int>(n2, st);
+    int* nq = lalloc<int>(ns, st);
+    int* np = lalloc<int>(ns, st);
+    size_t tb = 0;
+    cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, fq, skeys, iota, lq, n2, ns, roff, roff + 1, 0, 64, st);
+    void* stmp = lalloc<char>(tb, st);
+    size_t tb2 = tb;
+    cub::DeviceSegmentedRadixSort::SortPairsDescending(stmp, tb2, fq, skeys, iota, lq, n2, ns, roff, roff + 1, 0, 64, st);
+    { k_row_nnz<<<(ns + 255) / 256, 256, 0, st>>>(skeys, ns, nq); note_launch(); }
+    tb2 = tb;
+    cub::DeviceSegmentedRadixSort::SortPairsDescending(stmp, tb2, dens->pmax, skeys, iota, lp, n2, ns, roff, roff + 1, 0, 64, st);
+    { k_row_nnz<<<(ns + 255) / 256, 256, 0, st>>>(skeys, ns, np); note_launch(); }
+    HXF_CUDA(cudaGetLastError());
+    for (void* p : {(void*)stmp, (void*)skeys, (void*)iota, (void*)roff}) cudaFreeAsync(p, st);
+
+    DirectArgs da;
+    da.n_pairs = pairs->n_pairs;
+    da.pi = pairs->pi;
+    da.pj = pairs->pj;
+    da.meta = pairs->meta;
+    da.fq = fq;
+    da.pidm = pidm;
+    da.pm = dens->pmax;
+    da.lq = lq;
+    da.nq = nq;
+    da.lp = lp;
+    da.np = np;
+    da.ns = ns;
+    da.mod = mod;
+    da.rem = rem;
+    da.tau = o->tau_2e;
+    da.fqmax = schwarz ? std::sqrt(pairs->maxq) : pairs->maxq;
+    // ---- count pass + offsets
+    const int64_t npr = pairs->n_pairs;
+    int64_t* cnt = lalloc<int64_t>(npr + 1, st);
+    int64_t* off = lalloc<int64_t>(npr + 1, st);
+    HXF_CUDA(cudaMemsetAsync(cnt + npr, 0, sizeof(int64_t), st));
+    da.count = cnt;
+    da.off = nullptr;
+    da.rec = nullptr;
+    da.keys = nullptr;
+    const unsigned grid_all = (unsigned)((npr * 32 + 255) / 256);
+    if (npr) { k_direct<false><<<grid_all, 256, 0, st>>>(da, 0, npr); note_launch(); }
+    size_t stb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, stb, cnt, off, npr + 1, st);
+    void* scan_tmp = lalloc<char>(stb, st);
+    cub::DeviceScan::ExclusiveSum(scan_tmp, stb, cnt, off, npr + 1, st);
+    std::vector<int64_t> hoff(npr + 1);
+    HXF_CUDA(cudaMemcpyAsync(hoff.data(), off, (npr + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+    cudaFreeAsync(scan_tmp, st);
+    cudaFreeAsync(cnt, st);
+    g_timings[0] = tprep.stop();
+    const int64_t total = hoff[npr];
+
+    // ---- fixed-point K (the hierarchical build's scale: bitwise-comparable K)
+    const double kb = 2.0 * s->nfn * std::max(dens->frob, 1e-300) *
+                      std::max(std::sqrt(pairs->maxq * pairs->maxq), 1e-300);
+    int S = 97 - (int)std::ceil(std::log2(kb));
+    S = std::max(-900, std::min(S, 400));
+    unsigned long long* Kfx = nullptr;
+    long long* scount = lalloc<long long>(C_NCOUNTERS, st);
+    HXF_CUDA(cudaMemsetAsync(scount, 0, C_NCOUNTERS * sizeof(long long), st));
+    unsigned long long* ddigest = nullptr;
+    const bool want_digest = o->digest != nullptr && o->evaluate;
+    if (want_digest) {
+        ddigest = lalloc<unsigned long long>(3, st);
+        HXF_CUDA(cudaMemsetAsync(ddigest, 0, 3 * sizeof(unsigned long long), st));
+    }
+    if (o->evaluate && total) {
+        Kfx = lalloc<unsigned long long>(2 * nfn2, st);
+        HXF_CUDA(cudaMemsetAsync(Kfx, 0, 2 * nfn2 * sizeof(unsigned long long), st));
+        size_t freeb = 0, totb = 0;
+        cudaMemGetInfo(&freeb, &totb);
+        const int64_t cap = std::min<int64_t>(1ll << 29, std::max<int64_t>(1 << 16, (int64_t)(freeb / 160)));
+        SurvivorBufs sb;
+        sb.rec = lalloc<uint64_t>(cap, st);
+        sb.rec2 = lalloc<uint64_t>(cap, st);
+        sb.keys = lalloc<uint16_t>(cap, st);
+        sb.keys2 = lalloc<uint16_t>(cap, st);
+        sb.sort_tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, sb.sort_tb, sb.keys, sb.keys2, sb.rec, sb.rec2, cap, 0, 12, st);
+        sb.sort_tmp = lalloc<char>(sb.sort_tb, st);
+        sb.dbounds = lalloc<int64_t>(4097, st);
+        EriArgs e;
+        e.bpi = e.kpi = pairs->pi;
+        e.bpj = e.kpj = pairs->pj;
+        e.bppoff = e.kppoff = pairs->ppoff;
+        e.bpp = e.kpp = pairs->pp;
+        e.binfo = e.kinfo = pairs->info;
+        e.ctr = s->basis.ctr;
+        e.fn = s->basis.fn;
+        e.P = dens->P;
+        e.nfn = s->nfn;
+        e.S = S;
+        e.K = Kfx;
+        e.counters = scount;
+        da.off = off;
+        da.rec = sb.rec;
+        da.keys = sb.keys;
+        int64_t p0 = 0;
+        while (p0 < npr) {
+            // largest p1 with hoff[p1] - hoff[p0] <= cap
+            int64_t p1 = std::upper_bound(hoff.begin() + p0 + 1, hoff.end(), hoff[p0] + cap) - hoff.begin() - 1;
+            if (p1 <= p0) throw HxfError{HXF_ELOGIC, "survivor buffer too small for one bra pair"};
+            const int64_t nrec = hoff[p1] - hoff[p0];
+            if (nrec) {
+                Timer tsc(st);
+                { k_direct<true><<<(unsigned)(((p1 - p0) * 32 + 255) / 256), 256, 0, st>>>(da, p0, p1); note_launch(); }
+                g_timings[1] += tsc.stop();
+                Timer teri(st);
+                eri_sorted_stage(e, sb, nrec, false, st);
+                if (want_digest)
+                    { k_digest<<<(unsigned)std::min<int64_t>((nrec + 255) / 256, 4096), 256, 0, st>>>(
+                          sb.rec2, nrec, pairs->pi, pairs->pj, pairs->pi, pairs->pj, (uint64_t)ns, mod, rem,
+                          ddigest); note_launch(); }
+                HXF_CUDA(cudaStreamSynchronize(st));
+                g_timings[2] += teri.stop();
+            }
+            p0 = p1;
+        }
+        for (void* p : {(void*)sb.rec, (void*)sb.rec2, (void*)sb.keys, (void*)sb.keys2, sb.sort_tmp, (void*)sb.dbounds})
+            cudaFreeAsync(p, st);
+    }
+    // ---- epilogue
+    Timer tep(st);
+    if (K_out) {
+        double* Kd = o->K_on_device ? K_out : lalloc<double>(nfn2, st);
+        if (Kfx) { k_fx_to_double<<<1024, 256, 0, st>>>(Kfx, nfn2, S, Kd); note_launch(); }
+        else HXF_CUDA(cudaMemsetAsync(Kd, 0, nfn2 * sizeof(double), st));
+        if (!o->K_on_device) {
+            HXF_CUDA(cudaMemcpyAsync(K_out, Kd, nfn2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            cudaFreeAsync(Kd, st);
+        }
+    }
+    long long hc[C_NCOUNTERS];
+    HXF_CUDA(cudaMemcpyAsync(hc, scount, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    unsigned long long hd[3] = {0, 0, 0};
+    if (want_digest) HXF_CUDA(cudaMemcpyAsync(hd, ddigest, sizeof(hd), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+    if (o->digest)
+        for (int k = 0; k < 3; ++k) o->digest[k] = hd[k];
+    for (void* p : {(void*)Kfx, (void*)scount, (void*)ddigest, (void*)fq, (void*)pidm, (void*)lq, (void*)lp,
+                    (void*)nq, (void*)np, (void*)off})
+        if (p) cudaFreeAsync(p, st);
+    HXF_CUDA(cudaStreamSynchronize(st));
+    HXF_CUDA(cudaGetLastError());
+    g_timings[3] = tep.stop();
+    g_timings[4] = ttot.stop();
+    hxf_counters& c = *out;
+    memset(&c, 0, sizeof(c));
+    c.eri_shell_quartets = total;
+    c.prim_quartets = hc[C_PRIMQ];
+    for (int k = 0; k < 16; ++k) {
+        c.class_quartets[k] = hc[C_CLSQ0 + k];
+        c.class_prim_quartets[k] = hc[C_CLSPQ0 + k];
+    }
     return HXF_OK;
 }
 

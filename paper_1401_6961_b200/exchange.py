@@ -348,3 +348,51 @@ def build_exchange_symmetric(pairs: ShellPairNode, P: MatrixQuadtree, tau_2e: fl
     if quartet_log is not None and log is not None:
         quartet_log.extend(log)
     return K, out
+
+
+def dense_exchange_screened(pairs: ShellPairNode, P: MatrixQuadtree, tau_2e: float = 0.0,
+                            mode: str = "schwarz", K_out=None, digest=None, sample=(1, 0)):
+    """Direct-SCF twin on the GPU (oracle.py:69-108).
+
+    Every ordered shell quartet (i,j,k,l) of live pairs with
+    (f(Q_ij) |P|_jk) f(Q_kl) > tau_2e is evaluated -- no hierarchy -- by the
+    same ERI stage into the same fixed-point K, so the result equals
+    build_exchange_naive's K bit for bit when both evaluate the same set.
+    sample = (m, r) evaluates only quartets whose first shell i has
+    i % m == r (whole K rows of those shells' functions).  digest: optional
+    numpy uint64[3] filled as in run_exchange.  Returns (K, TraversalCounters)
+    with eri_shell_quartets and prim_quartets set; the reference's skipped
+    bound sum is not formed (it cancels catastrophically at full size).
+    """
+    if not (tau_2e >= 0.0):
+        raise InvalidArgumentError("tau_2e must be non-negative")
+    if mode not in ("schwarz", "literal"):
+        raise InvalidArgumentError(f"unknown screening mode {mode!r}")
+    _check_same_partition(pairs, pairs, P)
+    _require_root(pairs, "pairs")
+    L = _native.lib()
+    n = pairs.row.n_functions
+    opts = _native.ExchangeOpts()
+    opts.tau_2e = float(tau_2e)
+    opts.mode = 0 if mode == "schwarz" else 1
+    opts.evaluate = 1
+    opts.digest_mod, opts.digest_rem = int(sample[0]), int(sample[1])
+    if digest is not None:
+        if not (isinstance(digest, np.ndarray) and digest.dtype == np.uint64 and digest.shape == (3,)):
+            raise InvalidArgumentError("digest must be a contiguous numpy uint64[3]")
+        opts.digest = digest.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+    if K_out is None:
+        K = np.empty((n, n))
+        opts.K_on_device = 0
+        kptr = K.ctypes.data_as(ctypes.c_void_p)
+    else:
+        K = K_out
+        opts.K_on_device = 1
+        kptr = ctypes.c_void_p(K_out.data_ptr())
+    c = _native.Counters()
+    _native.check(L.hxf_exchange_direct(pairs._t.handle, P._t.handle, ctypes.byref(opts), kptr,
+                                        ctypes.byref(c), _native.current_stream()))
+    out = TraversalCounters()
+    out.eri_shell_quartets = int(c.eri_shell_quartets)
+    out.prim_quartets = int(c.prim_quartets)
+    return K, out
