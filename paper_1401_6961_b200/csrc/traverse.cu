@@ -19,6 +19,8 @@
 #include "hxf_internal.cuh"
 #include "traverse.cuh"
 
+#define TRAV_STRIPES 1024
+
 namespace {
 
 enum { O_NONE = 0, O_ABSENT, O_SCREEN, O_LEAF, O_EXPAND };
@@ -257,7 +259,11 @@ __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
         a.out_leaf[a.blk_off_leaf[blockIdx.x] + (excl & 0xffff)] = pack_task(lid[0], lid[1], lid[2], lid[3], v.live);
     }
     if (is_exp) a.out_expand[a.blk_off_expand[blockIdx.x] + (excl >> 16)] = pack_task(cm, cn, cl, cs, v.live);
-    // counters: warp-aggregated integer atomics (order independent)
+    // counters: warp-aggregated integer atomics (order independent) into one
+    // of TRAV_STRIPES copies, so the ~10^8 warps of a deep level do not all
+    // serialise on the same few addresses; k_fold_stripes sums the copies
+    long long* counters = a.counters + (blockIdx.x % TRAV_STRIPES) * C_NCOUNTERS;
+    unsigned long long* ledger = a.ledger + (blockIdx.x % TRAV_STRIPES) * LEDGER_LIMBS;
     const unsigned full = 0xffffffffu;
     const int valid_child = v.outcome != O_NONE;
     int vals[8] = {valid_child, v.outcome == O_SCREEN, v.outcome == O_ABSENT, is_leaf, is_exp,
@@ -267,11 +273,11 @@ __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const int s = __reduce_add_sync(full, vals[k]);
-        if ((threadIdx.x & 31) == 0 && s) atomic_add_ll(&a.counters[slots[k]], (long long)s);
+        if ((threadIdx.x & 31) == 0 && s) atomic_add_ll(&counters[slots[k]], (long long)s);
     }
     {
         const int s = __reduce_add_sync(full, valid_child);
-        if ((threadIdx.x & 31) == 0 && s) atomic_add_ll(&a.counters[C_SPAWNED], (long long)s);
+        if ((threadIdx.x & 31) == 0 && s) atomic_add_ll(&counters[C_SPAWNED], (long long)s);
     }
     if (SYM) {
         const bool counted = is_leaf || is_exp;
@@ -280,8 +286,8 @@ __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
             const int s1 = __reduce_add_sync(full, (int)(counted && v.label == k));
             const int s2 = __reduce_add_sync(full, (int)(is_leaf && v.label == k));
             if ((threadIdx.x & 31) == 0) {
-                if (s1) atomic_add_ll(&a.counters[C_CASE0 + k], (long long)s1);
-                if (s2) atomic_add_ll(&a.counters[C_CASELEAF0 + k], (long long)s2);
+                if (s1) atomic_add_ll(&counters[C_CASE0 + k], (long long)s1);
+                if (s2) atomic_add_ll(&counters[C_CASELEAF0 + k], (long long)s2);
             }
         }
     }
@@ -290,7 +296,31 @@ __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
     if (threadIdx.x == 0 && lsum != 0.0) {
         unsigned long long limb[LEDGER_LIMBS];
         fx_from_double<LEDGER_LIMBS>(lsum, LEDGER_SCALE, limb);
-        fx_atomic_add<LEDGER_LIMBS>(a.ledger, limb);
+        fx_atomic_add<LEDGER_LIMBS>(ledger, limb);
+    }
+}
+
+// sum the striped counter / ledger copies into the real ones (one block)
+__global__ void k_fold_stripes(const long long* sc, const unsigned long long* sl, long long* counters,
+                               unsigned long long* ledger) {
+    for (int k = threadIdx.x; k < C_NCOUNTERS; k += blockDim.x) {
+        long long s = 0;
+        for (int r = 0; r < TRAV_STRIPES; ++r) s += sc[r * C_NCOUNTERS + k];
+        counters[k] += s;
+    }
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < TRAV_STRIPES; ++r) {
+            unsigned long long carry = 0;
+            for (int k = 0; k < LEDGER_LIMBS; ++k) {
+                const unsigned long long a0 = ledger[k], b = sl[r * LEDGER_LIMBS + k];
+                const unsigned long long t = a0 + b;
+                const unsigned long long c1 = t < a0;
+                const unsigned long long t2 = t + carry;
+                const unsigned long long c2 = t2 < t;
+                ledger[k] = t2;
+                carry = c1 + c2;
+            }
+        }
     }
 }
 
@@ -367,6 +397,19 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         counters = scratch_c;
         ledger = scratch_l;
     }
+    // striped copies of the counters / ledger for the expand kernels
+    long long* sc = talloc<long long>((size_t)TRAV_STRIPES * C_NCOUNTERS, st);
+    unsigned long long* sl = talloc<unsigned long long>((size_t)TRAV_STRIPES * LEDGER_LIMBS, st);
+    auto zero_stripes = [&]() {
+        HXF_CUDA(cudaMemsetAsync(sc, 0, sizeof(long long) * TRAV_STRIPES * C_NCOUNTERS, st));
+        HXF_CUDA(cudaMemsetAsync(sl, 0, sizeof(unsigned long long) * TRAV_STRIPES * LEDGER_LIMBS, st));
+    };
+    auto fold_stripes = [&](long long* c, unsigned long long* l) {
+        k_fold_stripes<<<1, 128, 0, st>>>(sc, sl, c, l);
+        note_launch();
+        zero_stripes();
+    };
+    zero_stripes();
     const int D = s->n_levels - 1;
     std::vector<uint64_t*> leaf_parts;
     std::vector<int64_t> leaf_counts;
@@ -406,6 +449,7 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
                 leaf_parts.clear();
                 leaf_counts.clear();
             }
+            fold_stripes(counters, ledger);  // above the cut: scratch (discarded) on shards != 0
             counters = in.counters;
             ledger = in.ledger;
             if (n_cur == 0) break;
@@ -431,8 +475,8 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         a.child = ch;
         a.tv = tv;
         a.blk_counts = blk;
-        a.counters = counters;
-        a.ledger = ledger;
+        a.counters = sc;
+        a.ledger = sl;
         a.out_expand = nullptr;
         a.out_leaf = nullptr;
         a.blk_off_expand = oe;
@@ -470,6 +514,9 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         n_cur = tot[1];
         res.frontier_sizes.push_back(n_cur);
     }
+    fold_stripes(counters, ledger);
+    cudaFreeAsync(sc, st);
+    cudaFreeAsync(sl, st);
     if (in.frontier_only) {
         res.frontier = cur;
         res.n_frontier = n_cur;
