@@ -88,7 +88,7 @@ __device__ __forceinline__ double pblock_max(const ScreenArgs& a, int s, int t) 
 // record slots; a slab that cannot take the next ballot is padded with
 // sentinel records (key 0xFFFF sorts after every real 12-bit key and is
 // excluded by the key bounds), so no emitting iteration waits for an atomic.
-#define SLAB 256
+#define SLAB 1024
 #define SENTINEL_REC (~0ull)
 #define SENTINEL_KEY ((uint16_t)0xFFFF)
 
