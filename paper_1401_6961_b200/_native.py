@@ -13,7 +13,8 @@ import os
 from .basis import InvalidArgumentError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhxf.so")
+# HXF_LIB: alternative build of the same library (profiling variants; tools only)
+LIB_PATH = os.environ.get("HXF_LIB") or os.path.join(HERE, "libhxf.so")
 
 HXF_OK, HXF_EINVAL, HXF_ELOGIC, HXF_ECUDA, HXF_ENOMEM = 0, 1, 2, 3, 4
 NCASES = 9

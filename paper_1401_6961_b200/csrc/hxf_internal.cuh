@@ -97,6 +97,7 @@ struct hxf_pairs {
     int4* info;        // per pair id: {fn offset i, fn offset j, first prim pair, n prim pairs}
     int64_t n_prim_pairs;
     double maxq;
+    double amax;       // max over shells s of sum_{pairs (s,t) or (t,s)} n_f(t) sqrt(Q) (K scale bound)
     int has_p;
 };
 
@@ -262,27 +263,20 @@ __host__ __device__ inline double fx_to_double(const unsigned long long* limb, i
 
 #define LEDGER_LIMBS 4
 #define LEDGER_SCALE 160
-#define K_LIMBS 2
-
-// K accumulator (per element, 16 B): v = round(x 2^S) (|sums| < 2^98) is split
-// into non-overlapping parts hi = v >> 36 (signed) and lo = v & (2^36 - 1);
-// each is summed with a fire-and-forget 64-bit reduction (no returned value,
-// no dependent L2 round trip).  Integer sums are order independent, so K is
-// bitwise reproducible; exact while an element receives < 2^28 additions.
-#define K_LO_BITS 36
-
+// K accumulator (per element, 8 B): v = rint(x 2^S) summed with one
+// fire-and-forget 64-bit reduction per contribution.  S is chosen per build
+// from a rigorous bound B on the sum of |contributions| any element can
+// receive (k_scale_bits: B <= 4 A_max^2 max|P|, A(s) = sum over the pairs
+// (s,t) of n_f(t) sqrt(Q_st)), so every partial sum stays below 2^62 and
+// cannot overflow.  Integer sums are order independent, so K is bitwise
+// reproducible; each contribution is rounded once, to 2^-(S+1).
 __device__ __forceinline__ void k_fixed_add(unsigned long long* acc, double x, int S) {
-    unsigned long long v[2];
-    fx_from_double<2>(x, S, v);
-    const unsigned long long hi = (v[1] << (64 - K_LO_BITS)) | (v[0] >> K_LO_BITS);
-    const unsigned long long lo = v[0] & ((1ull << K_LO_BITS) - 1);
-    if (hi) atomicAdd(acc, hi);
-    if (lo) atomicAdd(acc + 1, lo);
+    const long long v = __double2ll_rn(ldexp(x, S));  // ldexp by a power of two: exact
+    if (v) atomicAdd(acc, (unsigned long long)v);
 }
 
 __host__ __device__ inline double k_fixed_value(const unsigned long long* acc, int S) {
-    const long long hi = (long long)acc[0];
-    return ldexp((double)hi, K_LO_BITS - S) + ldexp((double)acc[1], -S);
+    return ldexp((double)(long long)acc[0], -S);
 }
 
 // ---------------------------------------------------------------- warp utils

@@ -603,11 +603,17 @@ __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double
     if (v == 1.2345) e.K[0] = 1;
     return;
 #endif
-    k_fixed_add(e.K + 2 * ((int64_t)row * e.nfn + col), v, e.S);
+    k_fixed_add(e.K + ((int64_t)row * e.nfn + col), v, e.S);
 }
 
 template <int LA, int LB, int LC, int LD>
-__global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? 3 : 2) k_eri(EriArgs e) {
+#ifndef HXF_ERI_MINB0
+#define HXF_ERI_MINB0 3
+#endif
+#ifndef HXF_ERI_MINB1
+#define HXF_ERI_MINB1 2
+#endif
+__global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 : HXF_ERI_MINB1) k_eri(EriArgs e) {
     typedef Eri<LA, LB, LC, LD> E;
     constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL;
     constexpr int CLS = (LA << 3) | (LB << 2) | (LC << 1) | LD;
@@ -638,7 +644,11 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? 3 : 2) k_eri(E
 #ifdef HXF_EXP_NOPRIM  // timing experiment: skip the primitive loops (results wrong)
             for (int q = 0; q < NI * NJ * NK * NL; ++q) out[q] = e.bpp[ib.z].c * e.kpp[ik.z].c;
 #else
+#ifdef HXF_EXP_KQBCAST  // timing experiment: every lane reads lane 0's ket primitives (results wrong)
+            E::eval(e.bpp + ib.z, nb, e.kpp + __shfl_sync(__activemask(), ik.z, __ffs(__activemask()) - 1), nk, A, B, C, D, s_tab, out);
+#else
             E::eval(e.bpp + ib.z, nb, e.kpp + ik.z, nk, A, B, C, D, s_tab, out);
+#endif
 #endif
             const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
             const int64_t n = e.nfn;
@@ -903,7 +913,7 @@ __global__ void k_digest(const uint64_t* rec, int64_t n, const int* bpi, const i
 __global__ void k_fx_to_double(const unsigned long long* Kfx, int64_t n2, int S, double* K) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2;
          t += (int64_t)gridDim.x * blockDim.x)
-        K[t] = k_fixed_value(Kfx + 2 * t, S);
+        K[t] = k_fixed_value(Kfx + t, S);
 }
 
 __global__ void k_asym(const double* K, int n, unsigned long long* out) {
@@ -1068,6 +1078,19 @@ void host_ledger_add(unsigned long long* acc, const unsigned long long* v) {
 
 }  // namespace
 
+// Fixed-point scale of the K accumulator.  Any accumulator element (x, y)
+// receives terms -1/2 P_uv (x u|v y) with |(x u|v y)| <= sqrt(Q_{s(x)s(u)})
+// sqrt(Q_{s(v)s(y)}), each (x,u,v,y) at most 8 times over the symmetric
+// images and slots, so sum |contributions| <= 1/2 * 8 * A_bra A_ket max|P|
+// (A = hxf_pairs::amax).  S puts that bound below 2^61: partial sums never
+// overflow the signed 64-bit accumulator.
+int k_scale_bits(const hxf_pairs* bra, const hxf_pairs* ket, const hxf_density* dens) {
+    const double B = 4.0 * std::max(bra->amax, 1e-300) * std::max(ket->amax, 1e-300) *
+                     std::max(dens->maxabs, 1e-300) * (1.0 + 1e-9);
+    int S = 61 - (int)std::ceil(std::log2(B));
+    return std::max(-900, std::min(S, 900));
+}
+
 int hxf_last_timings_impl(double* ms, int n) {
     for (int k = 0; k < n && k < 8; ++k) ms[k] = g_timings[k];
     return HXF_OK;
@@ -1177,11 +1200,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         note_launch();
     };
 
-    // fixed-point scale for K: |K| <= 1/2 sum|P| max|(ij|kl)| <= 1/2 n ||P||_F maxQ
-    const double kb = 2.0 * s->nfn * std::max(dens->frob, 1e-300) *
-                      std::max(std::sqrt(bra->maxq * ket->maxq), 1e-300);
-    int S = 97 - (int)std::ceil(std::log2(kb));  // |sums of v| < 2^98 (k_fixed_add)
-    S = std::max(-900, std::min(S, 400));
+    const int S = k_scale_bits(bra, ket, dens);
 
     unsigned long long* Kfx = nullptr;
     int64_t logged = 0;
@@ -1233,8 +1252,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             g_timings[1] = tsc.stop();
         }
     } else {
-        Kfx = lalloc<unsigned long long>(2 * n2, st);
-        HXF_CUDA(cudaMemsetAsync(Kfx, 0, 2 * n2 * sizeof(unsigned long long), st));
+        Kfx = lalloc<unsigned long long>(n2, st);
+        HXF_CUDA(cudaMemsetAsync(Kfx, 0, n2 * sizeof(unsigned long long), st));
         // HXF_PIPE=1 double-buffers the survivor chunks: the screen of chunk
         // i+1 (stream st) runs while chunk i is sorted and evaluated (stream
         // se).  Measured neutral (c5 -1%, c4 +5%): the persistent ERI kernels
@@ -1352,7 +1371,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                     HXF_CUDA(cudaStreamWaitEvent(se, ev_scr[cur], 0));
                 }
                 HXF_CUDA(cudaEventRecord(ea, se));
-                eri_sorted_stage_async(e, sb[cur], nrec, se);
+                if (use_bp) eri_sorted_stage(e, sb[cur], nrec, true, se);
+                else eri_sorted_stage_async(e, sb[cur], nrec, se);
                 HXF_CUDA(cudaEventRecord(eb, se));
                 eri_ev.push_back({ea, eb});
                 if (want_log)
@@ -1716,10 +1736,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     const int64_t total = hoff[npr];
 
     // ---- fixed-point K (the hierarchical build's scale: bitwise-comparable K)
-    const double kb = 2.0 * s->nfn * std::max(dens->frob, 1e-300) *
-                      std::max(std::sqrt(pairs->maxq * pairs->maxq), 1e-300);
-    int S = 97 - (int)std::ceil(std::log2(kb));
-    S = std::max(-900, std::min(S, 400));
+    const int S = k_scale_bits(pairs, pairs, dens);
     unsigned long long* Kfx = nullptr;
     long long* scount = lalloc<long long>(C_NCOUNTERS, st);
     HXF_CUDA(cudaMemsetAsync(scount, 0, C_NCOUNTERS * sizeof(long long), st));
@@ -1730,8 +1747,8 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         HXF_CUDA(cudaMemsetAsync(ddigest, 0, 3 * sizeof(unsigned long long), st));
     }
     if (o->evaluate && total) {
-        Kfx = lalloc<unsigned long long>(2 * nfn2, st);
-        HXF_CUDA(cudaMemsetAsync(Kfx, 0, 2 * nfn2 * sizeof(unsigned long long), st));
+        Kfx = lalloc<unsigned long long>(nfn2, st);
+        HXF_CUDA(cudaMemsetAsync(Kfx, 0, nfn2 * sizeof(unsigned long long), st));
         size_t freeb = 0, totb = 0;
         cudaMemGetInfo(&freeb, &totb);
         const int64_t cap = std::min<int64_t>(1ll << 29, std::max<int64_t>(1 << 16, (int64_t)(freeb / 160)));

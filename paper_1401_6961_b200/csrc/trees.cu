@@ -330,6 +330,16 @@ __global__ void k_density_level(int level, int n, int nnext, const int* span_bas
     if (level == 0 && t == 0 && norm[me] < 0.0) norm[me] = 0.0;
 }
 
+// per shell: sum of n_f(partner) sqrt(Q) over the pairs that contain it (K scale bound)
+__global__ void k_pair_asum(DevBasis b, int64_t n, const int* pi, const int* pj, const double* sq, double* asum) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int i = pi[q], j = pj[q];
+    const double v = sq[q];
+    atomicAdd(asum + i, b.nf[j] * v);
+    atomicAdd(asum + j, b.nf[i] * v);
+}
+
 __global__ void k_maxabs(const double* v, int64_t n, unsigned long long* out) {
     double m = 0.0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
@@ -473,6 +483,17 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     tmp.push_back(dmax);
     HXF_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
     if (pr->n_pairs) { k_maxabs<<<256, 256, 0, st>>>(pr->q, pr->n_pairs, dmax); note_launch(); }
+    // K scale bound A(s) = sum over pairs touching shell s of n_f(partner) sqrt(Q)
+    double* asum = dalloc<double>(s->ns, st);
+    unsigned long long* damax = dalloc<unsigned long long>(1, st);
+    tmp.push_back(asum);
+    tmp.push_back(damax);
+    HXF_CUDA(cudaMemsetAsync(asum, 0, s->ns * sizeof(double), st));
+    HXF_CUDA(cudaMemsetAsync(damax, 0, sizeof(unsigned long long), st));
+    if (pr->n_pairs) { k_pair_asum<<<nblk(pr->n_pairs), 256, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->sq, asum); note_launch(); }
+    { k_maxabs<<<64, 256, 0, st>>>(asum, s->ns, damax); note_launch(); }
+    unsigned long long ham = 0;
+    HXF_CUDA(cudaMemcpyAsync(&ham, damax, sizeof(ham), cudaMemcpyDeviceToHost, st));
     unsigned long long hm = 0;
     HXF_CUDA(cudaMemcpyAsync(&hm, dmax, sizeof(hm), cudaMemcpyDeviceToHost, st));
     for (void* p : tmp) cudaFreeAsync(p, st);
@@ -481,6 +502,9 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     double mq;
     memcpy(&mq, &hm, sizeof(mq));
     pr->maxq = mq;
+    double am;
+    memcpy(&am, &ham, sizeof(am));
+    pr->amax = am * (1.0 + 1e-12);  // float atomics: the sum is an upper bound up to rounding
     int hasp = 0;
     for (int v : s->h_l) hasp |= v;
     pr->has_p = hasp;

@@ -213,7 +213,9 @@ class _DensityTree:
         self.handle = h
         weakref.finalize(self, _native.lib().hxf_density_destroy, h)
         self._norms = {}
-        self._views = {}
+        # weak cache: views reference their tree, so a strong cache would make a
+        # cycle and defer freeing the device arrays to the cyclic GC
+        self._views = weakref.WeakValueDictionary()
 
     def norms(self, level):
         v = self._norms.get(level)
@@ -371,7 +373,9 @@ class _PairTree:
         weakref.finalize(self, _native.lib().hxf_pairs_destroy, h)
         self._lvl = {}
         self._q = None
-        self._views = {}
+        # weak cache: views reference their tree, so a strong cache would make a
+        # cycle and defer freeing the device arrays to the cyclic GC
+        self._views = weakref.WeakValueDictionary()
 
     def level(self, L):
         v = self._lvl.get(L)
