@@ -98,8 +98,21 @@ struct hxf_pairs {
     int64_t n_prim_pairs;
     double maxq;
     double amax;       // max over shells s of sum_{pairs (s,t) or (t,s)} n_f(t) sqrt(Q) (K scale bound)
+    int* ncid;         // per leaf pair node (nleaf^2): compact live-node id, -1 if pruned
+    double* nvec;      // per live node: NVEC doubles, row/col max Q and row/col sums of sqrt(Q)
+    double* nvec_tri;  // per leaf span (diagonal node, canonical x <= y pairs): the same vectors
     int has_p;
 };
+
+// node vectors of a leaf pair node (mu, nu), shells x of mu and y of nu:
+//   [NV_FR + x] = max_y Q(x,y)   [NV_FC + y] = max_x Q(x,y)
+//   [NV_SR + x] = sum_y sqrtQ    [NV_SC + y] = sum_x sqrtQ
+#define NV_MAXS 10
+#define NV_FR 0
+#define NV_FC NV_MAXS
+#define NV_SR (2 * NV_MAXS)
+#define NV_SC (3 * NV_MAXS)
+#define NVEC (4 * NV_MAXS)
 
 struct hxf_density {
     hxf_system* sys;
@@ -302,7 +315,7 @@ enum {
     C_VISITED = 0, C_CULL_SCREEN, C_CULL_ABSENT, C_LEAF, C_ERIQ, C_CULL_LEAF, C_EXPANDED,
     C_SPAWNED, C_LINK_SCREEN, C_LINK_ABSENT, C_CASE0, C_CASELEAF0 = C_CASE0 + HXF_NCASES,
     C_TIE_TASK = C_CASELEAF0 + HXF_NCASES, C_TIE_LEAF, C_PRIMQ, C_OVERFLOW, C_CLSQ0,
-    C_CLSPQ0 = C_CLSQ0 + 16, C_DBG0 = C_CLSPQ0 + 16, C_NCOUNTERS = C_DBG0 + 4
+    C_CLSPQ0 = C_CLSQ0 + 16, C_DBG0 = C_CLSPQ0 + 16, C_NCOUNTERS = C_DBG0 + 8
 };
 
 // kernels launched by the library (evidence that the device path ran)

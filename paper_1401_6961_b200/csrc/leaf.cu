@@ -65,6 +65,12 @@ struct ScreenArgs {
     unsigned long long* fill;
     long long* counters;
     unsigned long long* ledger;
+    const int* ncidb;         // bra / ket pair trees: compact live-node ids and node vectors
+    const double* nvecb;
+    const double* nvecb_tri;
+    const int* ncidk;
+    const double* nveck;
+    const double* nveck_tri;
 };
 
 struct WarpSmem {
@@ -293,12 +299,16 @@ struct Smem2 {
     double fa[MP], sa[MP], fb[MP], sb[MP];
     double pm[NG][MP];
     double w[SYM ? 2 : 1][SYM ? MP : 1];    // g2/g3 row ledgers: sum_{b in L_k} pm_g[r, l(b)] sb[b]
-    double fbmax[MS], sbsum[MS];
+    double nvb[4 * MS], nvk[4 * MS];   // node vectors of the bra / ket leaf nodes (F entries as f),
+                                       // component o of shell r at (o / NV_MAXS) * MS + r
     double z[SYM ? 2 : 1][SYM ? MP : 1];    // g2/g3: max_{b in L_k} pm_g[r, l(b)] f_b
     unsigned char ax[MP], ay[MP], acl[MP], bx[MP], by[MP], bcl[MP];
     unsigned short apl[MP], bpl[MP];
     unsigned char bstart[MS], nl[MS];
     unsigned short queue[64];
+    double rmax[NG][MS];   // per slot and bra row shell: max over ket rows k of the triple factor
+    double rled[NG][MS];   // per slot and bra row shell: sum over ket rows k of the triple ledger factor
+    unsigned char alist[MP];  // bra pairs that pass the bra-level test
 };
 
 template <bool SYM, int MS>
@@ -325,7 +335,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
     const double tau = a.tau;
     const double tau_skip = tau * (1.0 - 1e-12);
 #ifdef HXF_PROF_SCREEN
-    long long cyc[4] = {0, 0, 0, 0};  // staging, tables, phase 1, phase 2
+    long long cyc[7] = {0, 0, 0, 0, 0, 0, 0};  // staging, tables, phase 1, phase 2, cell-culled tasks, tasks, zero-survivor tasks
 #define PROF_MARK(v) const long long v = clock64()
 #else
 #define PROF_MARK(v)
@@ -345,6 +355,66 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         const int ma = bdiag ? nmu * (nmu + 1) / 2 : nmu * nnu;
         const int mb = kdiag ? nlam * (nlam + 1) / 2 : nlam * nsig;
         const float inv_nnu = 1.0f / nnu, inv_nsig = 1.0f / nsig, inv_nlam = 1.0f / nlam;
+        // ---- stage density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
+        const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
+        const int cs[4] = {slam, slam, ssig, ssig}, cn[4] = {nlam, nlam, nsig, nsig};
+#pragma unroll
+        for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
+            if (!((live >> g) & 1)) continue;
+            const float inv = 1.0f / cn[g];
+#pragma unroll 1
+            for (int i = lane; i < rn[g] * cn[g]; i += 32) {
+                const int x = fdiv(i, cn[g], inv), y = i - x * cn[g];
+                sm.pm[g][i] = a.pmax[(int64_t)(rs[g] + x) * a.ns + cs[g] + y];
+            }
+        }
+        // ---- node vectors of the bra and ket leaf nodes (row / column max f, sums of s)
+        {
+            const double* vb = bdiag ? a.nvecb_tri + (int64_t)mu * NVEC
+                                     : a.nvecb + (int64_t)a.ncidb[(int64_t)mu * a.nleaf + nu] * NVEC;
+            const double* vk = kdiag ? a.nveck_tri + (int64_t)lam * NVEC
+                                     : a.nveck + (int64_t)a.ncidk[(int64_t)lam * a.nleaf + sig] * NVEC;
+#pragma unroll 1
+            for (int i = lane; i < 8 * MS; i += 32) {
+                const int h = i < 4 * MS ? i : i - 4 * MS;
+                const int o = h / MS, r = h - o * MS;
+                double v = __ldg((i < 4 * MS ? vb : vk) + o * NV_MAXS + r);
+                if (schwarz && o < 2) v = sqrt(v);   // max sqrt(Q) = sqrt(max Q) (monotone, correctly rounded)
+                (i < 4 * MS ? sm.nvb : sm.nvk)[h] = v;
+            }
+        }
+        __syncwarp();
+        // ---- cell test: for slot g, bra row shell r and ket column shell c, every
+        // quartet bound fl(fl(f_a p) f_b) <= F_A(r) p(r,c) F_B(c) (1 + 4 eps).  A task
+        // with no passing cell in any live slot is culled whole (no quartet can be a
+        // tie); its ledger is sum_{r,c} S_A(r) p(r,c) S_B(c) per slot.
+        {
+            bool anyp = false;
+            double lcell = 0.0;
+#pragma unroll
+            for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
+                if (!((live >> g) & 1)) continue;
+                const int fo = (g == 0 || g == 2) ? MS : 0, so = fo + 2 * MS;   // F_C / F_R, S_C / S_R
+                const int fk = g < 2 ? 0 : MS, sk = fk + 2 * MS;
+                const float inv = 1.0f / cn[g];
+#pragma unroll 1
+                for (int i = lane; i < rn[g] * cn[g]; i += 32) {
+                    const int r = fdiv(i, cn[g], inv), c = i - r * cn[g];
+                    const double pm = sm.pm[g][i];
+                    if (!(sm.nvb[fo + r] * pm * sm.nvk[fk + c] * (1.0 + 1e-14) <= tau_skip)) anyp = true;
+                    lcell += sm.nvb[so + r] * pm * sm.nvk[sk + c];
+                }
+            }
+            if (!__any_sync(0xffffffffu, anyp)) {
+                if (lane == 0) n_cull += (long long)ma * mb * __popc(live & (SYM ? 0xf : 1));
+                ledger += lcell;
+#ifdef HXF_PROF_SCREEN
+                ++cyc[4];
+#endif
+                __syncwarp();
+                continue;
+            }
+        }
         // ---- stage pair factors
 #pragma unroll 1
         for (int i = lane; i < ma; i += 32) {
@@ -374,40 +444,19 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
             sm.bpl[i] = x * nsig + y;
             sm.bcl[i] = a.metak[pid];
         }
-        // density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
-        const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
-        const int cs[4] = {slam, slam, ssig, ssig}, cn[4] = {nlam, nlam, nsig, nsig};
-#pragma unroll
-        for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
-            if (!((live >> g) & 1)) continue;
-            const float inv = 1.0f / cn[g];
-#pragma unroll 1
-            for (int i = lane; i < rn[g] * cn[g]; i += 32) {
-                const int x = fdiv(i, cn[g], inv), y = i - x * cn[g];
-                sm.pm[g][i] = a.pmax[(int64_t)(rs[g] + x) * a.ns + cs[g] + y];
-            }
+        // ket rows: L_k = ket pairs with row shell k (contiguous in the pair order);
+        // max f and sum s over L_k are the ket node's row vectors
+        if (lane < nlam) {
+            const int k = lane;
+            sm.bstart[k] = kdiag ? k * nlam - k * (k - 1) / 2 : k * nsig;
+            sm.nl[k] = kdiag ? nlam - k : nsig;
         }
         __syncwarp();
         PROF_MARK(c_staged);
-        // ket rows: L_k = ket pairs with row shell k (contiguous in the pair order)
-        if (lane < nlam) {
-            const int k = lane;
-            const int st = kdiag ? k * nlam - k * (k - 1) / 2 : k * nsig;
-            const int n = kdiag ? nlam - k : nsig;
-            sm.bstart[k] = st;
-            sm.nl[k] = n;
-        }
-        __syncwarp();
-        if (lane < nlam) {
-            const int k = lane, st = sm.bstart[k], n = sm.nl[k];
-            double fm = 0.0, ss = 0.0;
-            for (int b = st; b < st + n; ++b) {
-                fm = fmax(fm, sm.fb[b]);
-                ss += sm.sb[b];
-            }
-            sm.fbmax[k] = fm;
-            sm.sbsum[k] = ss;
-        }
+#ifdef HXF_PROF_SCREEN
+        const long long n_eri_before = n_eri;
+        ++cyc[5];
+#endif
         if (SYM) {
             // g2/g3: row maxima over l, and row ledgers per (r, k)
 #pragma unroll
@@ -432,13 +481,66 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
             }
         }
         __syncwarp();
+        // bra-level tables: for slot g and bra row shell r (y for g0/g2, x for g1/g3)
+        //   rmax = max_k triple factor (pm_g[r,k] fbmax_k, or z),  rled = sum_k triple ledger factor
+        for (int i = lane; i < Smem2<SYM, MS>::NG * MS; i += 32) {
+            const int g = i / MS, r = i - g * MS;
+            if (!((live >> g) & 1) || r >= rn[g]) continue;
+            double m = 0.0, l = 0.0;
+#pragma unroll 1
+            for (int k = 0; k < nlam; ++k) {
+                if (g < 2) {
+                    const double pm = sm.pm[g][r * nlam + k];
+                    m = fmax(m, pm * sm.nvk[k]);
+                    l += pm * sm.nvk[2 * MS + k];
+                } else {
+                    m = fmax(m, sm.z[g - 2][r * nlam + k]);
+                    l += sm.w[g - 2][r * nlam + k];
+                }
+            }
+            sm.rmax[g][r] = m;
+            sm.rled[g][r] = l;
+        }
+        __syncwarp();
         PROF_MARK(c_tables);
 #ifdef HXF_PROF_SCREEN
         long long c_flush = 0;
 #endif
-        // ---- phase 1: triples (a, k); phase 2: queued triples x l, exact tests
+        // ---- phase 0: bra pairs.  Every triple bound of bra pair a is
+        // fl(fl(f_a p) f) or fl(f_a z (1 + 1e-15)) <= f_a rmax (1 + 4 eps), so a
+        // pair with f_a rmax (1 + 1e-14) <= tau (1 - 1e-12) in every live slot is
+        // culled whole (all its triples would be culled; no quartet is a tie).
+        int npass = 0;
+#pragma unroll 1
+        for (int a0 = 0; a0 < ma; a0 += 32) {
+            const int ia = a0 + lane;
+            bool pass = false;
+            if (ia < ma) {
+                const double fa = sm.fa[ia], sa = sm.sa[ia];
+                const int x = sm.ax[ia], y = sm.ay[ia];
+                double lsum = 0.0;
+                int nlv = 0;
+#pragma unroll
+                for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
+                    if (!((live >> g) & 1)) continue;
+                    const int r = (g == 0 || g == 2) ? y : x;
+                    if (!(fa * sm.rmax[g][r] * (1.0 + 1e-14) <= tau_skip)) pass = true;
+                    lsum += sa * sm.rled[g][r];
+                    ++nlv;
+                }
+                if (!pass) {
+                    n_cull += (long long)nlv * mb;
+                    ledger += lsum;
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, pass);
+            if (pass) sm.alist[npass + __popc(bal & ((1u << lane) - 1u))] = (unsigned char)ia;
+            npass += __popc(bal);
+        }
+        __syncwarp();
+        // ---- phase 1: triples (a, k) of passing bra pairs; phase 2: queued triples x l, exact tests
         int qn = 0;
-        const int ntrip = ma * nlam;
+        const int ntrip = npass * nlam;
         const int Wl = kdiag ? nlam : nsig;       // lanes per queued triple
         const int per = 32 / Wl;                  // triples per phase-2 pass
         const int my_e = lane / Wl, my_l = lane - my_e * Wl;
@@ -499,9 +601,10 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
             bool pass = false;
             int ia = 0, k = 0;
             if (more && tt < ntrip) {
-                ia = fdiv(tt, nlam, inv_nlam);
-                k = tt - ia * nlam;
-                const double fa = sm.fa[ia], sa = sm.sa[ia], fm = sm.fbmax[k];
+                const int ai = fdiv(tt, nlam, inv_nlam);
+                k = tt - ai * nlam;
+                ia = sm.alist[ai];
+                const double fa = sm.fa[ia], sa = sm.sa[ia], fm = sm.nvk[k];
                 const int x = sm.ax[ia], y = sm.ay[ia];
                 double lsum = 0.0;
                 int ncul = 0;
@@ -512,7 +615,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                     if (g < 2) {
                         const double pm = sm.pm[g][(g == 0 ? y : x) * nlam + k];
                         ub = __dmul_rn(__dmul_rn(fa, pm), fm);
-                        led = __dmul_rn(sa, pm) * sm.sbsum[k];
+                        led = __dmul_rn(sa, pm) * sm.nvk[2 * MS + k];
                     } else {
                         // fl(fl(f_a p) f_b) <= f_a max(p f_b) (1 + 4 eps): the skip
                         // threshold tau (1 - 1e-12) leaves far more slack than that
@@ -551,6 +654,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
             cyc[1] += c_tables - c_staged;
             cyc[2] += c_end - c_tables - c_flush;
             cyc[3] += c_flush;
+            if (__reduce_add_sync(0xffffffffu, (unsigned)(n_eri - n_eri_before)) == 0) ++cyc[6];
 #endif
         }
     }
@@ -562,6 +666,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
     if (lane == 0) {
 #ifdef HXF_PROF_SCREEN
         for (int k = 0; k < 4; ++k) atomic_add_ll(&a.counters[C_DBG0 + k], cyc[k]);
+        for (int k = 4; k < 7; ++k) atomic_add_ll(&a.counters[C_DBG0 + k], cyc[k]);
 #endif
         if (n_eri) atomic_add_ll(&a.counters[C_ERIQ], n_eri);
         if (n_cull) atomic_add_ll(&a.counters[C_CULL_LEAF], n_cull);
@@ -1158,6 +1263,12 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.metab = bra->meta;
     sa.metak = ket->meta;
     sa.pmax = dens->pmax;
+    sa.ncidb = bra->ncid;
+    sa.nvecb = bra->nvec;
+    sa.nvecb_tri = bra->nvec_tri;
+    sa.ncidk = ket->ncid;
+    sa.nveck = ket->nvec;
+    sa.nveck_tri = ket->nvec_tri;
     sa.ns = s->ns;
     sa.fn = s->basis.fn;
     sa.nf = s->basis.nf;
@@ -1518,6 +1629,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     fprintf(stderr, "screen cycles (warp-summed): staging %.3e tables %.3e phase1 %.3e phase2 %.3e\n",
             (double)acc_c[C_DBG0], (double)acc_c[C_DBG0 + 1], (double)acc_c[C_DBG0 + 2],
             (double)acc_c[C_DBG0 + 3]);
+    fprintf(stderr, "screen tasks %lld: cell-test culled %lld, zero survivors %lld\n", acc_c[C_DBG0 + 5],
+            acc_c[C_DBG0 + 4], acc_c[C_DBG0 + 6]);
 #endif
     return HXF_OK;
 }

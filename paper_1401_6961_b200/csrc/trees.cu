@@ -330,6 +330,44 @@ __global__ void k_density_level(int level, int n, int nnext, const int* span_bas
     if (level == 0 && t == 0 && norm[me] < 0.0) norm[me] = 0.0;
 }
 
+// per live leaf pair node: row / column maxima of Q and row / column sums of
+// sqrt(Q) over its shell pairs (the whole block), and for diagonal nodes also
+// over the canonical triangle x <= y (the fourfold enumeration); fixed
+// summation order (deterministic)
+__global__ void k_node_vectors(const int* lslo, const int* lshi, int nl, const int64_t* leaf_base,
+                               const int* ncid, const double* q, const double* sq, double* nvec,
+                               double* nvec_tri) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nl * nl) return;
+    const int64_t bb = leaf_base[t];
+    if (bb < 0) return;
+    const int mu = (int)(t / nl), nu = (int)(t % nl);
+    const int nmu = lshi[mu] - lslo[mu], nnu = lshi[nu] - lslo[nu];
+    for (int tri = 0; tri < (mu == nu ? 2 : 1); ++tri) {
+        double* v = tri ? nvec_tri + (int64_t)mu * NVEC : nvec + (int64_t)ncid[t] * NVEC;
+        for (int k = 0; k < NVEC; ++k) v[k] = 0.0;
+        for (int x = 0; x < nmu; ++x)
+            for (int y = tri ? x : 0; y < nnu; ++y) {
+                const int64_t pid = bb + x * nnu + y;
+                const double qq = q[pid], s = sq[pid];
+                v[NV_FR + x] = fmax(v[NV_FR + x], qq);
+                v[NV_FC + y] = fmax(v[NV_FC + y], qq);
+                v[NV_SR + x] += s;
+                v[NV_SC + y] += s;
+            }
+    }
+}
+
+__global__ void k_live_flags(const int64_t* leaf_base, int64_t n, int* flag) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < n) flag[t] = leaf_base[t] >= 0 ? 1 : 0;
+}
+
+__global__ void k_live_ids(const int64_t* leaf_base, int64_t n, int* ncid) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < n && leaf_base[t] < 0) ncid[t] = -1;
+}
+
 // per shell: sum of n_f(partner) sqrt(Q) over the pairs that contain it (K scale bound)
 __global__ void k_pair_asum(DevBasis b, int64_t n, const int* pi, const int* pj, const double* sq, double* asum) {
     const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -457,6 +495,27 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     pr->meta = dalloc<uint8_t>(pr->n_pairs, st);
     { k_pair_meta<<<nblk(pr->n_pairs), 256, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->q,
                                                      pr->sq, pr->meta); note_launch(); }
+    {   // compact ids of the live leaf nodes and their screening vectors
+        int* flag = dalloc<int>(nl2 + 1, st);
+        tmp.push_back(flag);
+        HXF_CUDA(cudaMemsetAsync(flag + nl2, 0, sizeof(int), st));
+        { k_live_flags<<<nblk(nl2), 256, 0, st>>>(pr->leaf_base, nl2, flag); note_launch(); }
+        pr->ncid = dalloc<int>(nl2 + 1, st);
+        size_t tb2 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag, pr->ncid, nl2 + 1, st);
+        void* tbuf2 = dalloc<char>(tb2, st);
+        tmp.push_back(tbuf2);
+        cub::DeviceScan::ExclusiveSum(tbuf2, tb2, flag, pr->ncid, nl2 + 1, st);
+        int nlive = 0;
+        HXF_CUDA(cudaMemcpyAsync(&nlive, pr->ncid + nl2, sizeof(int), cudaMemcpyDeviceToHost, st));
+        HXF_CUDA(cudaStreamSynchronize(st));
+        { k_live_ids<<<nblk(nl2), 256, 0, st>>>(pr->leaf_base, nl2, pr->ncid); note_launch(); }
+        pr->nvec = dalloc<double>((int64_t)std::max(nlive, 1) * NVEC, st);
+        pr->nvec_tri = dalloc<double>((int64_t)nl * NVEC, st);
+        HXF_CUDA(cudaMemsetAsync(pr->nvec_tri, 0, (int64_t)nl * NVEC * sizeof(double), st));
+        { k_node_vectors<<<nblk(nl2, 128), 128, 0, st>>>(lt.lslo, lt.lshi, nl, pr->leaf_base, pr->ncid, pr->q,
+                                                       pr->sq, pr->nvec, pr->nvec_tri); note_launch(); }
+    }
     double* lnorm = dalloc<double>(nl2, st);
     double* lrow = dalloc<double>(nl2, st);
     double* lcol = dalloc<double>(nl2, st);
