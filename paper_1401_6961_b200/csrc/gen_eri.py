@@ -276,77 +276,6 @@ def gen_class(la, lb, lc, ld):
     return "\n".join(out)
 
 
-def gen_bp(la, lb, lc, ld):
-    """Bra-primitive-parallel pieces for light classes (L <= 1).
-
-    EriBP<...>::prim(bp, kp, ..., acc) adds one primitive quartet's [e0|f0]
-    values into acc[NACC]; EriBP<...>::hrr(acc, ...) turns the group-reduced
-    accumulators into the contracted block out[], as Eri<...>::core does.
-    """
-    es = carts_upto(la, la + lb)
-    fs = carts_upto(lc, lc + ld)
-    accs = [(e, f) for e in es for f in fs]
-    ni, nj, nk, nl = (len(carts(x)) for x in (la, lb, lc, ld))
-    out = []
-    w = out.append
-    w(f"template <> struct EriBP<{la},{lb},{lc},{ld}> {{")
-    w(f"  static constexpr int NACC = {len(accs)};")
-    w("  __device__ __forceinline__ static void prim(const PrimPair& bp, const PrimPair& kp,")
-    w("      const double3 A, const double3 C, const double* __restrict__ tab, double* __restrict__ acc) {")
-    for t, (e, f) in enumerate(accs):
-        w(f"    double& acc_{name(e)}_{name(f)} = acc[{t}];")
-    if la + lb > 0:
-        w("    const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
-        w("    const double o2p = 0.5 * bp.ip;")
-    prim_body(w, la, lb, lc, ld, accs, 4)
-    w("  }")
-    w("  __device__ __forceinline__ static void hrr(const double* __restrict__ acc, const double3 A,")
-    w("      const double3 B, const double3 C, const double3 D, double* __restrict__ out) {")
-    for t, (e, f) in enumerate(accs):
-        w(f"    const double acc_{name(e)}_{name(f)} = acc[{t}];")
-    memo, hl, cnt = {}, [], [0]
-
-    def hrr(a, b, c, d):
-        key = (a, b, c, d)
-        if key in memo:
-            return memo[key]
-        if b != ZERO:
-            i = next(t for t in range(3) if b[t] > 0)
-            b1 = sub(b, i)
-            x, y = hrr(add(a, i), b1, c, d), hrr(a, b1, c, d)
-            v = f"h{cnt[0]}"
-            cnt[0] += 1
-            hl.append(f"const double {v} = {x} + AB{AX[i]} * {y};")
-        elif d != ZERO:
-            i = next(t for t in range(3) if d[t] > 0)
-            d1 = sub(d, i)
-            x, y = hrr(a, b, add(c, i), d1), hrr(a, b, c, d1)
-            v = f"h{cnt[0]}"
-            cnt[0] += 1
-            hl.append(f"const double {v} = {x} + CD{AX[i]} * {y};")
-        else:
-            v = f"acc_{name(a)}_{name(c)}"
-        memo[key] = v
-        return v
-
-    outs = []
-    for (x, a), (y, b), (z, c), (t, d) in itertools.product(
-            enumerate(carts(la)), enumerate(carts(lb)), enumerate(carts(lc)), enumerate(carts(ld))):
-        outs.append((((x * nj + y) * nk + z) * nl + t, hrr(a, b, c, d)))
-    w("    (void)A; (void)B; (void)C; (void)D;")
-    if lb:
-        w("    const double ABx = A.x - B.x, ABy = A.y - B.y, ABz = A.z - B.z;")
-    if ld:
-        w("    const double CDx = C.x - D.x, CDy = C.y - D.y, CDz = C.z - D.z;")
-    for line in hl:
-        w("    " + line)
-    for idx, v in outs:
-        w(f"    out[{idx}] = {v};")
-    w("  }")
-    w("};")
-    return "\n".join(out)
-
-
 def _ops(expr):
     return expr.count("*") + expr.count("+") + expr.count(" - ")
 
@@ -396,13 +325,9 @@ def main():
     print("// generated by gen_eri.py -- do not edit")
     print("#pragma once")
     print("template <int LA, int LB, int LC, int LD> struct Eri;")
-    print("template <int LA, int LB, int LC, int LD> struct EriBP;")
     for cls in itertools.product((0, 1), repeat=4):
         print(gen_class(*cls))
         print()
-        if sum(cls) <= 1:
-            print(gen_bp(*cls))
-            print()
 
 
 if __name__ == "__main__":

@@ -749,11 +749,7 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
 #ifdef HXF_EXP_NOPRIM  // timing experiment: skip the primitive loops (results wrong)
             for (int q = 0; q < NI * NJ * NK * NL; ++q) out[q] = e.bpp[ib.z].c * e.kpp[ik.z].c;
 #else
-#ifdef HXF_EXP_KQBCAST  // timing experiment: every lane reads lane 0's ket primitives (results wrong)
-            E::eval(e.bpp + ib.z, nb, e.kpp + __shfl_sync(__activemask(), ik.z, __ffs(__activemask()) - 1), nk, A, B, C, D, s_tab, out);
-#else
             E::eval(e.bpp + ib.z, nb, e.kpp + ik.z, nk, A, B, C, D, s_tab, out);
-#endif
 #endif
             const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
             const int64_t n = e.nfn;
@@ -805,138 +801,6 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
         atomic_add_ll(&e.counters[C_CLSPQ0 + CLS], nprim);
         atomic_add_ll(&e.counters[C_CLSQ0 + CLS], nq);
     }
-}
-
-// ---------------------------------------------------------------------------
-// Light classes (L <= 1): bra-primitive parallel.  Launched per sub-segment of
-// uniform bra primitive count G = nb (survivors are sorted by it): a group of
-// G lanes owns one shell quartet, lane g owns bra primitive g and loops over
-// the ket primitives (same address across the group -> broadcast loads).  The
-// group sum is a fixed shuffle tree over G lanes (depends only on G, so the
-// result is independent of where the quartet sits in the warp), then the
-// group leader applies the horizontal transfer and contracts into K.  Few
-// registers per lane -> high occupancy.
-
-template <int LA, int LB, int LC, int LD>
-__global__ void __launch_bounds__(256) k_eri_bp(EriArgs e, int G) {
-    typedef Eri<LA, LB, LC, LD> E;
-    typedef EriBP<LA, LB, LC, LD> BP;
-    constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL, NACC = BP::NACC;
-    extern __shared__ __align__(16) double s_tab[];
-    boys_table_to_smem(s_tab, E::L);
-    const int lane = threadIdx.x & 31;
-    const int RW = 32 / G;                 // groups per warp
-    const int grp = lane / G, g = lane - grp * G;
-    const int64_t nwt = (e.n + RW - 1) / RW;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    long long nprim = 0, nq = 0;
-    for (int64_t wt = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); wt < nwt;
-         wt += nwarps) {
-        const int64_t r = wt * RW + grp;
-        bool act = grp < RW && r < e.n;
-        int mask = 0;
-        int4 ib = make_int4(0, 0, 0, 0), ik = make_int4(0, 0, 0, 0);
-        int64_t pb = 0, pk = 0;
-        double acc[NACC];
-#pragma unroll
-        for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
-        double3 A{0, 0, 0}, C{0, 0, 0};
-        if (act) {
-            const uint64_t rec = e.rec[r];
-            mask = (int)((rec >> 56) & 0xf);
-            act = mask != 0;
-            pb = (int64_t)(rec & 0xfffffff);
-            pk = (int64_t)((rec >> 28) & 0xfffffff);
-        }
-        if (act) {
-            ib = __ldg(e.binfo + pb);
-            ik = __ldg(e.kinfo + pk);
-            if (LA | LB) A = e.ctr[e.bpi[pb]];
-            if (LC | LD) C = e.ctr[e.kpi[pk]];
-            const PrimPair bp = load_pp(e.bpp + ib.z + g);
-            const PrimPair* kq = e.kpp + ik.z;
-            for (int t = 0; t < ik.w; ++t) BP::prim(bp, load_pp(kq + t), A, C, s_tab, acc);
-        }
-#pragma unroll
-        for (int k = 0; k < NACC; ++k) {
-#pragma unroll
-            for (int off = 8; off > 0; off >>= 1) {
-                const double o = __shfl_down_sync(0xffffffffu, acc[k], off);
-                if (g + off < G) acc[k] += o;
-            }
-        }
-        if (act && g == 0) {
-            nq += 1;
-            nprim += (long long)ib.w * ik.w;
-            double3 B{0, 0, 0}, D{0, 0, 0};
-            if (LB) B = e.ctr[e.bpj[pb]];
-            if (LD) D = e.ctr[e.kpj[pk]];
-            double out[NI * NJ * NK * NL];
-            BP::hrr(acc, A, B, C, D, out);
-            const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
-            const int64_t n = e.nfn;
-            const double* P = e.P;
-#define OUT(x, y, z, w) out[(((x) * NJ + (y)) * NK + (z)) * NL + (w)]
-            if (mask & 1)
-                for (int x = 0; x < NI; ++x)
-                    for (int w = 0; w < NL; ++w) {
-                        double s = 0.0;
-                        for (int y = 0; y < NJ; ++y)
-                            for (int z = 0; z < NK; ++z) s += __ldg(P + (fj + y) * n + fk + z) * OUT(x, y, z, w);
-                        k_add(e, fi + x, fl + w, -0.5 * s);
-                    }
-            if (mask & 2)
-                for (int y = 0; y < NJ; ++y)
-                    for (int w = 0; w < NL; ++w) {
-                        double s = 0.0;
-                        for (int x = 0; x < NI; ++x)
-                            for (int z = 0; z < NK; ++z) s += __ldg(P + (fi + x) * n + fk + z) * OUT(x, y, z, w);
-                        k_add(e, fj + y, fl + w, -0.5 * s);
-                    }
-            if (mask & 4)
-                for (int x = 0; x < NI; ++x)
-                    for (int z = 0; z < NK; ++z) {
-                        double s = 0.0;
-                        for (int y = 0; y < NJ; ++y)
-                            for (int w = 0; w < NL; ++w) s += __ldg(P + (fj + y) * n + fl + w) * OUT(x, y, z, w);
-                        k_add(e, fi + x, fk + z, -0.5 * s);
-                    }
-            if (mask & 8)
-                for (int y = 0; y < NJ; ++y)
-                    for (int z = 0; z < NK; ++z) {
-                        double s = 0.0;
-                        for (int x = 0; x < NI; ++x)
-                            for (int w = 0; w < NL; ++w) s += __ldg(P + (fi + x) * n + fl + w) * OUT(x, y, z, w);
-                        k_add(e, fj + y, fk + z, -0.5 * s);
-                    }
-#undef OUT
-        }
-    }
-    constexpr int CLS = (LA << 3) | (LB << 2) | (LC << 1) | LD;
-    nq = warp_sum_ll(nq);
-    nprim = warp_sum_ll(nprim);
-    if (lane == 0 && nprim) {
-        atomic_add_ll(&e.counters[C_PRIMQ], nprim);
-        atomic_add_ll(&e.counters[C_CLSPQ0 + CLS], nprim);
-        atomic_add_ll(&e.counters[C_CLSQ0 + CLS], nq);
-    }
-}
-
-template <int A, int B, int C, int D>
-void launch_eri_bp(const EriArgs& e, int G, cudaStream_t st) {
-    static int per_sm = -1, sms = 0;
-    if (per_sm < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_eri_bp<A, B, C, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BOYS_TAB_BYTES);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri_bp<A, B, C, D>, 256, BOYS_TAB_BYTES);
-        per_sm = std::max(per_sm, 1);
-    }
-    const int64_t warps = (e.n + (32 / G) - 1) / (32 / G);
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)sms * per_sm));
-    k_eri_bp<A, B, C, D><<<g, 256, BOYS_TAB_BYTES, st>>>(e, G);
-    note_launch();
 }
 
 // lower bounds of every 12-bit key value in the sorted key array
@@ -1098,11 +962,6 @@ struct SurvivorBufs {
     int64_t* dbounds;
 };
 
-struct Timer;
-// sort one chunk of survivors by (class, nb, nk) and run the per-class ERI
-// kernels over rec2 (the sorted copy)
-void eri_sorted_stage(EriArgs e, const SurvivorBufs& b, int64_t nrec, bool use_bp, cudaStream_t st);
-
 struct Timer {
     cudaEvent_t a, b;
     cudaStream_t st;
@@ -1122,42 +981,10 @@ struct Timer {
     }
 };
 
-void eri_sorted_stage(EriArgs e, const SurvivorBufs& b, int64_t nrec, bool use_bp, cudaStream_t st) {
-    size_t tb = b.sort_tb;
-    cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, 12, st);
-    { k_key_bounds<<<17, 256, 0, st>>>(b.keys2, nrec, b.dbounds); note_launch(); }
-    std::vector<int64_t> kbnd(4097);
-    HXF_CUDA(cudaMemcpyAsync(kbnd.data(), b.dbounds, 4097 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    HXF_CUDA(cudaStreamSynchronize(st));
-    Timer tk(st);
-    for (int c = 0; c < 16; ++c) {
-        if (use_bp && __builtin_popcount(c) <= 1) {
-            // light class: one launch per bra primitive count (group size)
-            for (int nb = 1; nb <= 16; ++nb) {
-                const int64_t b0 = kbnd[(c << 8) | ((nb - 1) << 4)], b1 = kbnd[(c << 8) + (nb << 4)];
-                if (b1 <= b0) continue;
-                e.rec = b.rec2 + b0;
-                e.n = b1 - b0;
-                switch (c) {
-                    case 0: launch_eri_bp<0, 0, 0, 0>(e, nb, st); break;
-                    case 1: launch_eri_bp<0, 0, 0, 1>(e, nb, st); break;
-                    case 2: launch_eri_bp<0, 0, 1, 0>(e, nb, st); break;
-                    case 4: launch_eri_bp<0, 1, 0, 0>(e, nb, st); break;
-                    case 8: launch_eri_bp<1, 0, 0, 0>(e, nb, st); break;
-                }
-            }
-            continue;
-        }
-        e.rec = b.rec2 + kbnd[c << 8];
-        e.n = kbnd[(c + 1) << 8] - kbnd[c << 8];
-        launch_eri_class(c, e, st);
-    }
-    g_timings[5] += tk.stop();
-    HXF_CUDA(cudaGetLastError());
-}
-
-// the same stage without a host synchronisation: every class kernel reads its
-// record range from the device-side key bounds (empty classes exit at once)
+// sort one chunk of survivors by (class, nb, nk) and run the per-class ERI
+// kernels over the sorted copy, without a host synchronisation: every class
+// kernel reads its record range from the device-side key bounds (empty classes
+// exit at once)
 void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cudaStream_t st) {
     size_t tb = b.sort_tb;
     cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, 12, st);
@@ -1284,10 +1111,6 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     // HXF_SCREEN=flat selects the per-quartet screen (A/B reference)
     const char* sv = getenv("HXF_SCREEN");
     const bool flat = sv && !strcmp(sv, "flat");
-    // HXF_ERI=bp enables the bra-primitive-parallel light-class kernels (measured
-    // slower than thread-per-quartet on c3/c4; kept as an A/B variant)
-    const char* ev = getenv("HXF_ERI");
-    const bool use_bp = ev && !strcmp(ev, "bp");
     const bool ms8 = s->max_leaf_shells <= 8;
     const int sw = flat ? SCREEN_WARPS
                         : (ms8 ? (sym ? screen2_warps<true, 8>() : screen2_warps<false, 8>())
@@ -1371,7 +1194,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         // fill every SM's registers, so the two stages cannot co-reside and
         // only the tails overlap.  Default: one buffer set, in order.
         const char* pv = getenv("HXF_PIPE");
-        const bool pipe = (pv && pv[0] == '1') && !use_bp;
+        const bool pipe = pv && pv[0] == '1';
         const int NB = pipe ? 2 : 1;
         size_t freeb = 0, totb = 0;
         cudaMemGetInfo(&freeb, &totb);
@@ -1482,8 +1305,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                     HXF_CUDA(cudaStreamWaitEvent(se, ev_scr[cur], 0));
                 }
                 HXF_CUDA(cudaEventRecord(ea, se));
-                if (use_bp) eri_sorted_stage(e, sb[cur], nrec, true, se);
-                else eri_sorted_stage_async(e, sb[cur], nrec, se);
+                eri_sorted_stage_async(e, sb[cur], nrec, se);
                 HXF_CUDA(cudaEventRecord(eb, se));
                 eri_ev.push_back({ea, eb});
                 if (want_log)
@@ -1902,7 +1724,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
                 { k_direct<true><<<(unsigned)(((p1 - p0) * 32 + 255) / 256), 256, 0, st>>>(da, p0, p1); note_launch(); }
                 g_timings[1] += tsc.stop();
                 Timer teri(st);
-                eri_sorted_stage(e, sb, nrec, false, st);
+                eri_sorted_stage_async(e, sb, nrec, st);
                 if (want_digest)
                     { k_digest<<<(unsigned)std::min<int64_t>((nrec + 255) / 256, 4096), 256, 0, st>>>(
                           sb.rec2, nrec, pairs->pi, pairs->pj, pairs->pi, pairs->pj, (uint64_t)ns, mod, rem,
