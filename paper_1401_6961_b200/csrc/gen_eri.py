@@ -118,7 +118,7 @@ def prim_body(w, la, lb, lc, ld, accs, ind, fold=False):
         w(p + "const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
         w(p + "const double T = bp.p * kp.p * (r * r) * R2;")
         w(p + "double F[1];")
-        w(p + "boys_bf<0>(T, F, tab);")
+        w(p + "boys_eval<0>(T, F, tab);")
         w(p + "accb = fma(kp.c * r, F[0], accb);")
         return
     w(p + "const double ps = bp.p + kp.p;")
@@ -129,7 +129,7 @@ def prim_body(w, la, lb, lc, ld, accs, ind, fold=False):
     w(p + "const double T = bp.p * kp.p * r2 * R2;")
     w(p + "const double pref = bp.c * kp.c * r;")
     w(p + f"double F[{L + 1}];")
-    w(p + f"boys_bf<{L}>(T, F, tab);")
+    w(p + f"boys_eval<{L}>(T, F, tab);")
     for m in range(L + 1):
         w(p + f"const double bm{m} = pref * F[{m}];")
     if L > 0:
@@ -324,6 +324,8 @@ def main():
         return
     print("// generated by gen_eri.py -- do not edit")
     print("#pragma once")
+    print("// boys_eval: boys_bf (Schwarz factors, trees.cu) or boys_bf_scaled (ERI kernels, leaf.cu),")
+    print("// chosen by the including translation unit")
     print("template <int LA, int LB, int LC, int LD> struct Eri;")
     for cls in itertools.product((0, 1), repeat=4):
         print(gen_class(*cls))

@@ -26,6 +26,7 @@
 
 #include "boys.cuh"
 #include "hxf_internal.cuh"
+#define boys_eval boys_bf_scaled  // ERI kernels: the short-chain Boys variant
 #include "eri_classes.cuh"
 #include "traverse.cuh"
 

@@ -16,6 +16,7 @@
 
 #include "boys.cuh"
 #include "hxf_internal.cuh"
+#define boys_eval boys_bf  // Schwarz factors: the reference Boys evaluation
 #include "eri_classes.cuh"
 
 #define SQRT_TWO_PI_POW_2_5 5.914967172795613 /* sqrt(2 pi^{5/2}) */
