@@ -98,11 +98,21 @@ struct hxf_pairs {
     int64_t n_prim_pairs;
     double maxq;
     double amax;       // max over shells s of sum_{pairs (s,t) or (t,s)} n_f(t) sqrt(Q) (K scale bound)
+    PrimPair* epp;     // ERI primitive table: each pair's primitives sorted by Schwarz factor, descending
+    double* eS;        // per entry of epp: primitive Schwarz factor sqrt(max_comp (ab|ab))
+    double smax_prim;  // max eS
     int* ncid;         // per leaf pair node (nleaf^2): compact live-node id, -1 if pruned
     double* nvec;      // per live node: NVEC doubles, row/col max Q and row/col sums of sqrt(Q)
     double* nvec_tri;  // per leaf span (diagonal node, canonical x <= y pairs): the same vectors
     int has_p;
 };
+
+// Primitive-quartet neglect in the ERI stage: a primitive pair ab is dropped
+// from a build when S_ab * max S_cd * max|P| <= HXF_PRIM_EPS, so every
+// dropped primitive quartet's contribution to any K element is <= HXF_PRIM_EPS
+// (|(ab|cd)| <= S_ab S_cd, Cauchy-Schwarz on the Coulomb metric).  The
+// Schwarz factors Q of the culling tests always use every primitive.
+#define HXF_PRIM_EPS 1e-16
 
 // node vectors of a leaf pair node (mu, nu), shells x of mu and y of nu:
 //   [NV_FR + x] = max_y Q(x,y)   [NV_FC + y] = max_x Q(x,y)

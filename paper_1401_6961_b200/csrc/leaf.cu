@@ -1011,6 +1011,46 @@ void host_ledger_add(unsigned long long* acc, const unsigned long long* v) {
 
 }  // namespace
 
+// Per-build ERI pair tables: the pair records and sort-key bytes with each
+// pair's primitive count cut to the primitives with S > thr (epp holds them
+// first, sorted by S); at least one primitive is kept.
+__global__ void k_prune_pairs(int64_t n, const int4* __restrict__ info, const uint8_t* __restrict__ meta,
+                              const double* __restrict__ eS, double thr, int4* einfo, uint8_t* emeta) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int4 v = info[t];
+    int keep = 0;
+    while (keep < v.w && eS[v.z + keep] > thr) ++keep;
+    keep = max(keep, 1);
+    einfo[t] = make_int4(v.x, v.y, v.z, keep);
+    emeta[t] = (uint8_t)((meta[t] & 3) | ((keep - 1) << 2));
+}
+
+struct EriTables {
+    int4* info = nullptr;
+    uint8_t* meta = nullptr;
+};
+
+// thr = HXF_PRIM_EPS / (max S of the other side * max|P|)
+EriTables prune_tables(const hxf_pairs* pr, double other_smax, double pmax, cudaStream_t st) {
+    EriTables t;
+    t.info = lalloc<int4>(pr->n_pairs, st);
+    t.meta = lalloc<uint8_t>(pr->n_pairs, st);
+    const double thr = HXF_PRIM_EPS / (std::max(other_smax, 1e-300) * std::max(pmax, 1e-300));
+    if (pr->n_pairs) {
+        k_prune_pairs<<<(unsigned)((pr->n_pairs + 255) / 256), 256, 0, st>>>(pr->n_pairs, pr->info, pr->meta, pr->eS,
+                                                                           thr, t.info, t.meta);
+        note_launch();
+    }
+    return t;
+}
+
+void free_tables(EriTables& t, cudaStream_t st) {
+    if (t.info) cudaFreeAsync(t.info, st);
+    if (t.meta) cudaFreeAsync(t.meta, st);
+    t = EriTables();
+}
+
 // Fixed-point scale of the K accumulator.  Any accumulator element (x, y)
 // receives terms -1/2 P_uv (x u|v y) with |(x u|v y)| <= sqrt(Q_{s(x)s(u)})
 // sqrt(Q_{s(v)s(y)}), each (x,u,v,y) at most 8 times over the symmetric
@@ -1088,8 +1128,12 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.poff = s->basis.poff;
     sa.sqb = bra->sq;
     sa.sqk = ket->sq;
-    sa.metab = bra->meta;
-    sa.metak = ket->meta;
+    // ERI pair tables of this build (negligible primitive tails dropped)
+    EriTables etb = prune_tables(bra, ket->smax_prim, dens->maxabs, st);
+    EriTables etk = bra == ket ? EriTables() : prune_tables(ket, bra->smax_prim, dens->maxabs, st);
+    const EriTables& etk_use = bra == ket ? etb : etk;
+    sa.metab = etb.meta;
+    sa.metak = etk_use.meta;
     sa.pmax = dens->pmax;
     sa.ncidb = bra->ncid;
     sa.nvecb = bra->nvec;
@@ -1228,13 +1272,13 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         e.bpi = bra->pi;
         e.bpj = bra->pj;
         e.bppoff = bra->ppoff;
-        e.bpp = bra->pp;
+        e.bpp = bra->epp;
         e.kpi = ket->pi;
         e.kpj = ket->pj;
         e.kppoff = ket->ppoff;
-        e.kpp = ket->pp;
-        e.binfo = bra->info;
-        e.kinfo = ket->info;
+        e.kpp = ket->epp;
+        e.binfo = etb.info;
+        e.kinfo = etk_use.info;
         e.ctr = s->basis.ctr;
         e.fn = s->basis.fn;
         e.P = dens->P;
@@ -1419,6 +1463,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     for (void* p : {(void*)Kfx, (void*)scount, (void*)sledger, (void*)dfill, (void*)dcount,
                     (void*)dledger, (void*)d_lslo, (void*)d_lshi, (void*)tr.leaf})
         if (p) cudaFreeAsync(p, st);
+    free_tables(etb, st);
+    free_tables(etk, st);
     HXF_CUDA(cudaStreamSynchronize(st));
     HXF_CUDA(cudaGetLastError());
     g_timings[3] = tep.stop();
@@ -1635,7 +1681,8 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     da.n_pairs = pairs->n_pairs;
     da.pi = pairs->pi;
     da.pj = pairs->pj;
-    da.meta = pairs->meta;
+    EriTables et = prune_tables(pairs, pairs->smax_prim, dens->maxabs, st);
+    da.meta = et.meta;
     da.fq = fq;
     da.pidm = pidm;
     da.pm = dens->pmax;
@@ -1702,8 +1749,8 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         e.bpi = e.kpi = pairs->pi;
         e.bpj = e.kpj = pairs->pj;
         e.bppoff = e.kppoff = pairs->ppoff;
-        e.bpp = e.kpp = pairs->pp;
-        e.binfo = e.kinfo = pairs->info;
+        e.bpp = e.kpp = pairs->epp;
+        e.binfo = e.kinfo = et.info;
         e.ctr = s->basis.ctr;
         e.fn = s->basis.fn;
         e.P = dens->P;
@@ -1759,6 +1806,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     for (void* p : {(void*)Kfx, (void*)scount, (void*)ddigest, (void*)fq, (void*)pidm, (void*)lq, (void*)lp,
                     (void*)nq, (void*)np, (void*)off})
         if (p) cudaFreeAsync(p, st);
+    free_tables(et, st);
     HXF_CUDA(cudaStreamSynchronize(st));
     HXF_CUDA(cudaGetLastError());
     g_timings[3] = tep.stop();

@@ -172,6 +172,43 @@ __global__ void k_diag_q(DevBasis B, int64_t n_pairs, const int* pi, const int* 
     }
 }
 
+// primitive Schwarz factors S = sqrt(max_comp (ab|ab)) of every primitive pair,
+// and the ERI copy of each pair's primitives sorted by S, descending (ties by
+// index), so a build can drop a negligible tail by shortening the count
+__global__ void k_prim_schwarz_sort(DevBasis B, int64_t n_pairs, const int* pi, const int* pj,
+                                    const int64_t* ppoff, const PrimPair* pp, PrimPair* epp, double* eS) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_pairs) return;
+    const int i = pi[t], j = pj[t];
+    const int64_t b0 = ppoff[t], b1 = ppoff[t + 1];
+    const double3 A = B.ctr[i], C = B.ctr[j];
+    const int li = B.l[i], lj = B.l[j];
+    double sv[16];
+    int idx[16];
+    const int n = (int)(b1 - b0);
+    for (int u = 0; u < n; ++u) {
+        const PrimPair* q = pp + b0 + u;
+        double v;
+        if (li == 0 && lj == 0) v = diag_q<0, 0>(q, 0, 1, A, C);
+        else if (li == 0) v = diag_q<0, 1>(q, 0, 1, A, C);
+        else if (lj == 0) v = diag_q<1, 0>(q, 0, 1, A, C);
+        else v = diag_q<1, 1>(q, 0, 1, A, C);
+        const double sval = sqrt(v);
+        int k = u;  // insertion sort, descending, stable
+        while (k > 0 && sv[k - 1] < sval) {
+            sv[k] = sv[k - 1];
+            idx[k] = idx[k - 1];
+            --k;
+        }
+        sv[k] = sval;
+        idx[k] = u;
+    }
+    for (int u = 0; u < n; ++u) {
+        epp[b0 + u] = pp[b0 + idx[u]];
+        eS[b0 + u] = sv[u];
+    }
+}
+
 // per pair: sqrt(Q) once (screening uses it for every quartet) and the class /
 // primitive-count byte of the survivor sort key
 __global__ void k_pair_meta(DevBasis B, int64_t n_pairs, const int* pi, const int* pj,
@@ -492,6 +529,16 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     { k_diag_q<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
                                                      pr->pp, lt.leaf_of_shell, lt.lslo, lt.lshi, nl,
                                                      pr->leaf_base, pr->q); note_launch(); }
+    pr->epp = dalloc<PrimPair>(pr->n_prim_pairs, st);
+    pr->eS = dalloc<double>(pr->n_prim_pairs, st);
+    { k_prim_schwarz_sort<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
+                                                                 pr->pp, pr->epp, pr->eS); note_launch(); }
+    unsigned long long* dsmax = dalloc<unsigned long long>(1, st);
+    tmp.push_back(dsmax);
+    HXF_CUDA(cudaMemsetAsync(dsmax, 0, sizeof(unsigned long long), st));
+    if (pr->n_prim_pairs) { k_maxabs<<<256, 256, 0, st>>>(pr->eS, pr->n_prim_pairs, dsmax); note_launch(); }
+    unsigned long long hsm = 0;
+    HXF_CUDA(cudaMemcpyAsync(&hsm, dsmax, sizeof(hsm), cudaMemcpyDeviceToHost, st));
     pr->sq = dalloc<double>(pr->n_pairs, st);
     pr->meta = dalloc<uint8_t>(pr->n_pairs, st);
     { k_pair_meta<<<nblk(pr->n_pairs), 256, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->q,
@@ -565,6 +612,7 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     double am;
     memcpy(&am, &ham, sizeof(am));
     pr->amax = am * (1.0 + 1e-12);  // float atomics: the sum is an upper bound up to rounding
+    memcpy(&pr->smax_prim, &hsm, sizeof(double));
     int hasp = 0;
     for (int v : s->h_l) hasp |= v;
     pr->has_p = hasp;
