@@ -28,6 +28,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ERI_FLOPS = os.path.join(ROOT, "paper_1401_6961_b200", "csrc", "eri_flops.json")
+# executed FP64 flops per primitive quartet per class, measured once with ncu
+# (tools/fp64_rate.py); the SURVEY 8(d) graded rate for the p classes
+ERI_FLOPS_EXEC = os.path.join(ROOT, "profiles", "r01_eri_fp64_executed.json")
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "surviving ERI quartets/s (FP64 exchange K-build)"
 
@@ -181,6 +184,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def eri_flops_executed(c):
+    try:
+        tab = json.load(open(ERI_FLOPS_EXEC))["per_prim"]
+    except (OSError, ValueError, KeyError):
+        return None
+    if any(c.class_prim_quartets[k] and tab[k] is None for k in range(16)):
+        return None
+    return sum(c.class_prim_quartets[k] * (tab[k] or 0.0) for k in range(16))
+
+
 def eri_flops(c):
     tab = json.load(open(ERI_FLOPS))
     return sum(c.class_prim_quartets[k] * tab["per_prim"][k] + c.class_quartets[k] * tab["per_quartet"][k]
@@ -303,8 +316,10 @@ def native_arm(args):
                                        K_out=K_dev, shard=shard, symmetrize=not (world > 1))
     tm = exchange.last_timings()
     flops = eri_flops(craw)
+    flops_exec = eri_flops_executed(craw)
     eri_ms = statistics.median([s[5] for s in stage]) if stage else tm[5]
     achieved = flops / (eri_ms * 1e-3) / 1e12 if eri_ms > 0 else 0.0
+    achieved_exec = flops_exec / (eri_ms * 1e-3) / 1e12 if (eri_ms > 0 and flops_exec) else None
 
     # e2e: host P -> device, density tree, build, K -> host, through the public API
     e2e_times = []
@@ -353,7 +368,15 @@ def native_arm(args):
                          "kernel": "k_eri<la,lb,lc,ld> (ERI + contraction), all classes",
                          "flops_per_step_rank0": flops,
                          "peak_source": "hxf_fp64_peak DFMA microbenchmark on this GPU "
-                                        "(MEASURED_PEAKS.json has no FP64 entry)"},
+                                        "(MEASURED_PEAKS.json has no FP64 entry)",
+                         "flops_basis": "algorithmic: 30 per (ss|ss) primitive quartet (SURVEY 8(d)), "
+                                        "generated OS/HGP operation counts for the p classes, "
+                                        "executed (non-neglected) primitive quartets"},
+            "roofline_executed": {"bound": "fp64", "achieved": achieved_exec, "peak": peak.value,
+                                  "unit": "TFLOP/s",
+                                  "frac": (achieved_exec / peak.value) if (achieved_exec and peak.value) else None,
+                                  "flops_basis": "executed FP64 (dadd + dmul + 2 dfma) per primitive quartet "
+                                                 "per class from ncu, profiles/r01_eri_fp64_executed.json"},
             "e2e": {"value": e2e_value, "unit": "quartets/s",
                     "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8,
                     "ms_per_step": float(et.item()) / max(args.e2e_steps, 1)},
