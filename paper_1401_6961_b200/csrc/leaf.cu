@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 
@@ -309,7 +310,8 @@ struct Smem2 {
     unsigned short queue[64];
     double rmax[NG][MS];   // per slot and bra row shell: max over ket rows k of the triple factor
     double rled[NG][MS];   // per slot and bra row shell: sum over ket rows k of the triple ledger factor
-    unsigned char alist[MP];  // bra pairs that pass the bra-level test
+    // bra pairs that pass the bra-level test: ia | (passing slots << 8) (SYM), ia (naive: slot 0 only)
+    typename std::conditional<SYM, unsigned short, unsigned char>::type alist[MP];
 };
 
 template <bool SYM, int MS>
@@ -335,6 +337,8 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
     const bool schwarz = a.mode == HXF_MODE_SCHWARZ;
     const double tau = a.tau;
     const double tau_skip = tau * (1.0 - 1e-12);
+    // tie window |bound - tau| <= 1e-12 tau (empty for tau = 0)
+    const double tie_lo = tau > 0.0 ? tau - 1e-12 * tau : 1.0, tie_hi = tau > 0.0 ? tau + 1e-12 * tau : -1.0;
 #ifdef HXF_PROF_SCREEN
     long long cyc[7] = {0, 0, 0, 0, 0, 0, 0};  // staging, tables, phase 1, phase 2, cell-culled tasks, tasks, zero-survivor tasks
 #define PROF_MARK(v) const long long v = clock64()
@@ -507,35 +511,34 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
 #ifdef HXF_PROF_SCREEN
         long long c_flush = 0;
 #endif
-        // ---- phase 0: bra pairs.  Every triple bound of bra pair a is
-        // fl(fl(f_a p) f) or fl(f_a z (1 + 1e-15)) <= f_a rmax (1 + 4 eps), so a
-        // pair with f_a rmax (1 + 1e-14) <= tau (1 - 1e-12) in every live slot is
-        // culled whole (all its triples would be culled; no quartet is a tie).
+        // ---- phase 0: bra pairs.  Every triple bound of bra pair a in slot g is
+        // fl(fl(f_a p) f) or fl(f_a z (1 + 1e-15)) <= f_a rmax_g (1 + 4 eps), so a
+        // slot with f_a rmax_g (1 + 1e-14) <= tau (1 - 1e-12) is culled for the
+        // whole bra pair (every quartet bound below tau, none a tie): its count
+        // and row ledger are added here and later phases test only the passing
+        // slots.  A pair with no passing slot is culled whole.
         int npass = 0;
 #pragma unroll 1
         for (int a0 = 0; a0 < ma; a0 += 32) {
             const int ia = a0 + lane;
-            bool pass = false;
+            int amask = 0;
             if (ia < ma) {
                 const double fa = sm.fa[ia], sa = sm.sa[ia];
                 const int x = sm.ax[ia], y = sm.ay[ia];
-                double lsum = 0.0;
-                int nlv = 0;
 #pragma unroll
                 for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
                     if (!((live >> g) & 1)) continue;
                     const int r = (g == 0 || g == 2) ? y : x;
-                    if (!(fa * sm.rmax[g][r] * (1.0 + 1e-14) <= tau_skip)) pass = true;
-                    lsum += sa * sm.rled[g][r];
-                    ++nlv;
-                }
-                if (!pass) {
-                    n_cull += (long long)nlv * mb;
-                    ledger += lsum;
+                    if (!(fa * sm.rmax[g][r] * (1.0 + 1e-14) <= tau_skip)) {
+                        amask |= 1 << g;
+                    } else {
+                        n_cull += mb;
+                        ledger += sa * sm.rled[g][r];
+                    }
                 }
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, pass);
-            if (pass) sm.alist[npass + __popc(bal & ((1u << lane) - 1u))] = (unsigned char)ia;
+            const unsigned bal = __ballot_sync(0xffffffffu, amask != 0);
+            if (amask) sm.alist[npass + __popc(bal & ((1u << lane) - 1u))] = SYM ? (ia | (amask << 8)) : ia;
             npass += __popc(bal);
         }
         __syncwarp();
@@ -553,7 +556,8 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                 int mask = 0, ia = 0, ib = 0;
                 if (my_e < per && e < count) {
                     const int ent = sm.queue[e];
-                    ia = ent >> 4;
+                    ia = ent >> 8;
+                    const int tmask = (ent >> 4) & 15;   // slots still open for this row
                     const int k = ent & 15;
                     if (my_l < sm.nl[k]) {
                         ib = sm.bstart[k] + my_l;
@@ -562,10 +566,10 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                         const int rowv[4] = {y, x, y, x}, colv[4] = {z, z, w, w};
 #pragma unroll
                         for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
-                            if (!((live >> g) & 1)) continue;
+                            if (!((tmask >> g) & 1)) continue;
                             const double pm = sm.pm[g][rowv[g] * cn[g] + colv[g]];
                             const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
-                            n_tie += tau > 0.0 && fabs(bound - tau) <= 1e-12 * tau;
+                            n_tie += bound >= tie_lo && bound <= tie_hi;
                             if (bound > tau) {
                                 keep_any = true;
                                 mask |= 1 << g;
@@ -599,19 +603,19 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         for (int t0 = 0;; t0 += 32) {
             const bool more = t0 < ntrip;
             const int tt = t0 + lane;
-            bool pass = false;
             int ia = 0, k = 0;
+            int tmask = 0;
             if (more && tt < ntrip) {
                 const int ai = fdiv(tt, nlam, inv_nlam);
                 k = tt - ai * nlam;
-                ia = sm.alist[ai];
+                const int ent = sm.alist[ai];
+                ia = ent & 0xff;
+                const int amask = SYM ? ent >> 8 : 1;
                 const double fa = sm.fa[ia], sa = sm.sa[ia], fm = sm.nvk[k];
                 const int x = sm.ax[ia], y = sm.ay[ia];
-                double lsum = 0.0;
-                int ncul = 0;
 #pragma unroll
                 for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
-                    if (!((live >> g) & 1)) continue;
+                    if (!((amask >> g) & 1)) continue;
                     double ub, led;
                     if (g < 2) {
                         const double pm = sm.pm[g][(g == 0 ? y : x) * nlam + k];
@@ -624,17 +628,17 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                         ub = fa * sm.z[g - 2][r * nlam + k] * (1.0 + 1e-15);
                         led = sa * sm.w[g - 2][r * nlam + k];
                     }
-                    if (!(ub <= tau_skip)) pass = true;
-                    lsum += led;
-                    ncul += sm.nl[k];
-                }
-                if (!pass) {
-                    n_cull += ncul;
-                    ledger += lsum;
+                    if (!(ub <= tau_skip)) {
+                        tmask |= 1 << g;
+                    } else {  // this slot culled for the whole row (no ties)
+                        n_cull += sm.nl[k];
+                        ledger += led;
+                    }
                 }
             }
+            const bool pass = tmask != 0;
             const unsigned bal = __ballot_sync(0xffffffffu, pass);
-            if (pass) sm.queue[qn + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)((ia << 4) | k);
+            if (pass) sm.queue[qn + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)((ia << 8) | (tmask << 4) | k);
             qn += __popc(bal);
             __syncwarp();
             if (qn >= 32 || (!more && qn > 0)) {
