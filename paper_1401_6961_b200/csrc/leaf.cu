@@ -11,7 +11,7 @@
 //            quartet, contracted into K with the density: naive slot
 //            K[i,l] += -1/2 P[j,k] (ij|kl) (exchange_naive.py:191-192); the
 //            4-fold scatter of exchange_symmetry.py:345-361 with its
-//            diagonal weights.  K accumulates in 128-bit fixed point with
+//            diagonal weights.  K accumulates in 64-bit fixed point with
 //            integer atomics, so the result is bitwise reproducible.
 //   epilogue fixed point -> FP64; fourfold: asymmetry check and (K+K^T)/2
 //            (symmetrize_final, exchange_symmetry.py:197-209).
