@@ -97,6 +97,13 @@ typedef struct hxf_exchange_opts {
     uint64_t* digest;
     int digest_mod;    /* <= 1: every quartet */
     int digest_rem;
+    /* K_fixed != 0 (requires K_on_device): K_out receives the signed 64-bit
+       fixed-point accumulator (int64 n x n, value = v * 2^-S) instead of FP64 K,
+       and *K_scale = S.  S depends only on (bra, ket, P), so shards of one build
+       share it and their partials sum exactly (integer all-reduce);
+       hxf_fixed_to_double converts.  symmetrize is ignored. */
+    int K_fixed;
+    int* K_scale;
 } hxf_exchange_opts;
 
 const char* hxf_last_error(void);
@@ -137,6 +144,8 @@ int hxf_density_download_pmax(const hxf_density* dens, double* pmax);
 
 int hxf_exchange(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, const hxf_exchange_opts* opts,
                  double* K_out, hxf_counters* counters, void* stream);
+/* K[t] = Kfx[t] * 2^-S for t < n2 (device arrays; may alias: in place). */
+int hxf_fixed_to_double(const int64_t* Kfx, int64_t n2, int S, double* K, void* stream);
 
 /* Direct-SCF twin (dense_exchange_screened, oracle.py:69-108; SURVEY.md 8(f)
  * f1): every ordered shell quartet of live pairs with

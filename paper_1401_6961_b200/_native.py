@@ -23,7 +23,8 @@ EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_de
             "hxf_system_info", "hxf_pairs_build", "hxf_pairs_destroy", "hxf_pairs_download",
             "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
             "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_exchange_direct", "hxf_frontier",
-            "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count")
+            "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count",
+            "hxf_fixed_to_double")
 
 
 class LogicError(RuntimeError):
@@ -66,7 +67,9 @@ class ExchangeOpts(ctypes.Structure):
                 ("log_count", ctypes.POINTER(ctypes.c_int64)),
                 ("digest", ctypes.POINTER(ctypes.c_uint64)),
                 ("digest_mod", ctypes.c_int),
-                ("digest_rem", ctypes.c_int)]
+                ("digest_rem", ctypes.c_int),
+                ("K_fixed", ctypes.c_int),
+                ("K_scale", ctypes.POINTER(ctypes.c_int))]
 
 
 _lib = None
@@ -107,6 +110,7 @@ def lib():
     L.hxf_symmetrize.argtypes = [vp, i32, dbl, vp]
     L.hxf_fp64_peak.argtypes = [P(dbl), vp]
     L.hxf_launch_count.argtypes = [P(i64)]
+    L.hxf_fixed_to_double.argtypes = [vp, i64, i32, vp, vp]
     _lib = L
     return L
 

@@ -17,6 +17,7 @@ static std::atomic<int64_t> g_launches{0};
 void note_launch(int n) { g_launches += n; }
 
 int hxf_last_timings_impl(double* ms, int n);
+int fixed_to_double_impl(const int64_t* Kfx, int64_t n2, int S, double* K, cudaStream_t st);
 
 #define HXF_TRY(...)                                         \
     try {                                                    \
@@ -338,6 +339,14 @@ int hxf_symmetrize(double* K_dev, int n, double tol, void* stream) {
     HXF_TRY({
         if (!K_dev || n < 0) throw HxfError{HXF_EINVAL, "bad arguments"};
         symmetrize_device(K_dev, n, tol, (cudaStream_t)stream);
+    })
+}
+
+int hxf_fixed_to_double(const int64_t* Kfx, int64_t n2, int S, double* K, void* stream) {
+    HXF_TRY({
+        if ((!Kfx || !K) && n2 > 0) throw HxfError{HXF_EINVAL, "NULL argument"};
+        if (n2 < 0) throw HxfError{HXF_EINVAL, "bad size"};
+        fixed_to_double_impl(Kfx, n2, S, K, (cudaStream_t)stream);
     })
 }
 

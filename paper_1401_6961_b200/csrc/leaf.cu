@@ -1068,6 +1068,15 @@ int k_scale_bits(const hxf_pairs* bra, const hxf_pairs* ket, const hxf_density* 
     return std::max(-900, std::min(S, 900));
 }
 
+int fixed_to_double_impl(const int64_t* Kfx, int64_t n2, int S, double* K, cudaStream_t st) {
+    if (n2 > 0) {
+        k_fx_to_double<<<1024, 256, 0, st>>>(reinterpret_cast<const unsigned long long*>(Kfx), n2, S, K);
+        note_launch();
+    }
+    HXF_CUDA(cudaGetLastError());
+    return HXF_OK;
+}
+
 int hxf_last_timings_impl(double* ms, int n) {
     for (int k = 0; k < n && k < 8; ++k) ms[k] = g_timings[k];
     return HXF_OK;
@@ -1415,7 +1424,12 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
 
     // ---- epilogue
     Timer tep(st);
-    if (K_out) {
+    if (K_out && o->K_fixed) {
+        if (!o->K_on_device) throw HxfError{HXF_EINVAL, "K_fixed requires K_on_device"};
+        if (Kfx) HXF_CUDA(cudaMemcpyAsync(K_out, Kfx, n2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+        else HXF_CUDA(cudaMemsetAsync(K_out, 0, n2 * sizeof(unsigned long long), st));
+        if (o->K_scale) *o->K_scale = S;
+    } else if (K_out) {
         double* Kd = o->K_on_device ? K_out : lalloc<double>(n2, st);
         if (Kfx) {
             { k_fx_to_double<<<1024, 256, 0, st>>>(Kfx, n2, S, Kd); note_launch(); }

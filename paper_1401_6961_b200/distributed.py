@@ -108,7 +108,9 @@ def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, sha
     """One rank's share of a sharded build + the all-reduce of K and counters.
 
     K_dev: torch CUDA tensor (n x n float64), overwritten with the full K on
-    every rank.  Returns (counters, shard plan).
+    every rank.  Each shard's K is its 64-bit fixed-point accumulator (same
+    scale on every rank); the int64 all-reduce is an exact integer sum, so the
+    reduced K is bitwise the single-device K.  Returns (counters, shard plan).
     """
     import torch
     import torch.distributed as dist
@@ -119,10 +121,14 @@ def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, sha
         shards = plan(bra, ket, P, tau_2e, mode, symmetry, world)
     level, ranges = shards
     b, e = ranges[rank]
-    _, c, _ = run_exchange(bra, ket, P, tau_2e, mode, symmetry, True, None, K_out=K_dev,
-                           shard=(level, b, e), symmetrize=False)
+    Kfx = K_dev.view(torch.int64)          # the FP64 buffer reused for the accumulator
+    (_, S), c, _ = run_exchange(bra, ket, P, tau_2e, mode, symmetry, True, None, K_out=Kfx,
+                                shard=(level, b, e), symmetrize=False, K_fixed=True)
     vec = torch.from_numpy(counters_vector(c)).to(K_dev.device)
-    allreduce_partials(K_dev, vec, group)
+    allreduce_partials(Kfx, vec, group)
+    _native.check(_native.lib().hxf_fixed_to_double(ctypes.c_void_p(Kfx.data_ptr()), Kfx.numel(), S,
+                                                    ctypes.c_void_p(K_dev.data_ptr()),
+                                                    _native.current_stream()))
     if symmetry:
         _native.check(_native.lib().hxf_symmetrize(ctypes.c_void_p(K_dev.data_ptr()), K_dev.shape[0],
                                                    1e-10, _native.current_stream()))

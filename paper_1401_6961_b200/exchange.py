@@ -225,11 +225,15 @@ def _require_root(node, what):
 
 
 def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log=None,
-                 K_out=None, shard=None, symmetrize=True, digest=None, digest_sample=(1, 0)):
+                 K_out=None, shard=None, symmetrize=True, digest=None, digest_sample=(1, 0),
+                 K_fixed=False):
     """Low-level call of hxf_exchange.
 
     K_out: None (return a new host array), or a CUDA tensor (n x n float64)
     written in place on the device.  shard: None or (level, begin, end).
+    K_fixed: K_out (a CUDA int64 n x n tensor) receives the 64-bit fixed-point
+    accumulator and the returned K is (K_out, S) with value = K_out * 2^-S
+    (exact integer sums across shards; include/hxf.h).
     digest: None, or a caller-owned numpy uint64[3] filled with the
     order-independent digest (count, sum h, sum h(h)) of the evaluated quartet
     tuples with i % digest_sample[0] == digest_sample[1] (include/hxf.h).
@@ -282,9 +286,17 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
             K = K_out
             opts.K_on_device = 1
             kptr = ctypes.c_void_p(K_out.data_ptr())
+        scale = ctypes.c_int(0)
+        if K_fixed:
+            if K_out is None or str(K_out.dtype) != "torch.int64":
+                raise InvalidArgumentError("K_fixed needs K_out as a CUDA int64 tensor")
+            opts.K_fixed = 1
+            opts.K_scale = ctypes.pointer(scale)
         c = _native.Counters()
         _native.check(L.hxf_exchange(bra._t.handle, ket._t.handle, P._t.handle, ctypes.byref(opts),
                                      kptr, ctypes.byref(c), _native.current_stream()))
+        if K_fixed:
+            K = (K_out, int(scale.value))
         if cap and log_count.value > cap:
             cap = int(log_count.value)
             continue

@@ -159,3 +159,26 @@ def test_sharded_shards_sum_to_full_build(sym):
         assert np.array_equal(vec[:-1], full[:-1]), (world, level, ranges)
         assert vec[-1] == pytest.approx(full[-1], rel=1e-12)
         assert np.abs(K - K_full).max() <= 1e-13
+        # the multi-GPU reduction path: integer sum of the shards' fixed-point
+        # accumulators (one scale for all shards) is bitwise the unsharded K
+        import torch
+        n = K_full.shape[0]
+        acc, scales = None, set()
+        for b, e in ranges:
+            buf = torch.empty((n, n), dtype=torch.int64, device="cuda")
+            (kf, S), _, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-9, "schwarz", sym,
+                                                  shard=(level, b, e), symmetrize=False,
+                                                  K_out=buf, K_fixed=True)
+            scales.add(S)
+            acc = kf.clone() if acc is None else acc + kf
+        assert len(scales) == 1
+        Kx = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        from paper_1401_6961_b200 import _native
+        import ctypes
+        _native.check(_native.lib().hxf_fixed_to_double(ctypes.c_void_p(acc.data_ptr()), acc.numel(),
+                                                        scales.pop(), ctypes.c_void_p(Kx.data_ptr()),
+                                                        _native.current_stream()))
+        Kx = Kx.cpu().numpy()
+        if sym:
+            Kx = hx.symmetrize_final(Kx)
+        assert np.array_equal(Kx, K_full), np.abs(Kx - K_full).max()
