@@ -182,3 +182,33 @@ def test_sharded_shards_sum_to_full_build(sym):
         if sym:
             Kx = hx.symmetrize_final(Kx)
         assert np.array_equal(Kx, K_full), np.abs(Kx - K_full).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sym", [False, True])
+def test_primitive_neglect_within_bound(sym, monkeypatch):
+    """Per-build primitive neglect (HXF_PRIM_EPS): dropping primitive
+    pairs with S_ab * max S_cd * max|P| <= eps changes K by at most eps per
+    dropped primitive quartet, leaves the culled set (counters) unchanged, and
+    eps = 0 keeps every primitive."""
+    from paper_1401_6961_b200 import exchange
+    cfg = configs.cube_cluster(12, 5, "tiny")
+    part = hx.build_partition(cfg.system, leaf_size=8)
+    pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
+    P_tree = hx.build_matrix_tree(cfg.P, part)
+    monkeypatch.setenv("HXF_PRIM_EPS", "0")
+    K0, c0, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-8, "schwarz", sym)
+    full = sum(int(x) for x in c0.class_prim_quartets)
+    monkeypatch.setenv("HXF_PRIM_EPS", "1e-9")   # coarse threshold: many primitives dropped
+    K1, c1, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-8, "schwarz", sym)
+    kept = sum(int(x) for x in c1.class_prim_quartets)
+    assert c1.eri_shell_quartets == c0.eri_shell_quartets
+    assert c1.quartets_culled_leaf == c0.quartets_culled_leaf
+    assert kept < full
+    # each dropped primitive quartet changes an element by <= eps per function
+    # component of the contracted density block (<= 9) in each of <= 4 slots
+    assert np.abs(K1 - K0).max() <= 36 * 1e-9 * (full - kept)
+    monkeypatch.delenv("HXF_PRIM_EPS")
+    K2, c2, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-8, "schwarz", sym)
+    assert sum(int(x) for x in c2.class_prim_quartets) <= full
+    assert np.abs(K2 - K0).max() <= 1e-12
