@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--units", type=int, default=None, help="override cluster size (c3-c5 recipe)")
-    ap.add_argument("--mode", default="fourfold", choices=["naive", "fourfold"])
+    ap.add_argument("--mode", default="fourfold", choices=["naive", "fourfold", "eightfold"],
+                    help="eightfold: the 4-fold build folded bra<->ket (same K, ~half the quartets; "
+                         "no reference counterpart, the CPU baseline runs the 4-fold port)")
     ap.add_argument("--tau", type=float, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-units", type=int, default=None)
@@ -102,7 +104,7 @@ def run_cpu(args, steps, warmup):
     cfg, desc = cpu_sample(args)
     st = ho.Setup(cfg.system, cfg.P, tau_ovlp=cfg.tau_ovlp, leaf_size=cfg.leaf_size)
     threads = os.cpu_count() or 1
-    f = st.symmetric if args.mode == "fourfold" else st.naive
+    f = st.naive if args.mode == "naive" else st.symmetric
     for _ in range(warmup):
         f(cfg.tau_2e, threads=threads)
     times, quartets = [], 0
@@ -226,7 +228,7 @@ def native_arm(args):
     else:
         P_gen = None
     gen_s = time.perf_counter() - t0
-    sym = args.mode == "fourfold"
+    sym = "eightfold" if args.mode == "eightfold" else args.mode == "fourfold"
     part = hx.build_partition(cfg.system, leaf_size=cfg.leaf_size)
     part.device(local)
     torch.cuda.synchronize()
@@ -264,7 +266,7 @@ def native_arm(args):
             return c
         _, c, _ = exchange.run_exchange(pairs, pairs, P_tree, cfg.tau_2e, "schwarz", sym, True,
                                         None, K_out=K_dev)
-        return distributed.counters_from_vector(distributed.counters_vector(c), sym)
+        return distributed.counters_from_vector(distributed.counters_vector(c), bool(sym))
 
     for _ in range(args.warmup):
         step(P_dev)

@@ -41,6 +41,8 @@ extern "C" {
 
 #define HXF_NAIVE 0     /* exchange_naive.py, ordered shell pairs      */
 #define HXF_FOURFOLD 1  /* exchange_symmetry.py, canonical pairs       */
+#define HXF_EIGHTFOLD 2 /* (new) fourfold folded bra<->ket: canonical pairs, bra pair <= ket pair;
+                           K = A + A^T (SURVEY.md 8(a) S8 optional mode)                        */
 
 #define HXF_NCASES 9 /* CASE_LABELS, exchange_symmetry.py:43 */
 
@@ -78,7 +80,7 @@ typedef struct hxf_counters {
 typedef struct hxf_exchange_opts {
     double tau_2e;
     int mode;          /* HXF_MODE_*   */
-    int symmetry;      /* HXF_NAIVE / HXF_FOURFOLD */
+    int symmetry;      /* HXF_NAIVE / HXF_FOURFOLD / HXF_EIGHTFOLD */
     int evaluate;      /* 0: counters only, K = 0 (exchange_naive.py:183) */
     int K_on_device;   /* K_out is a device pointer                  */
     int symmetrize;    /* fourfold: apply symmetrize_final (:197-209) */

@@ -9,7 +9,8 @@ from .basis import (Atom, BasisSystem, DensityModel, GaussianShell, InvalidArgum
                     SplitMix64, build_density, generate_cluster, hilbert_order)
 from ._native import LogicError
 from .exchange import (CASE_LABELS, SymmetryCase, SymmetryCounters, TraversalCounters,
-                       build_exchange_naive, build_exchange_symmetric, classify_quartet,
+                       build_exchange_eightfold, build_exchange_naive, build_exchange_symmetric,
+                       classify_quartet,
                        culled_task_bound, screening_test, symmetrize_final)
 from .quadtree import (MatrixQuadtree, Partition, ShellPairNode, Span, build_matrix_tree,
                        build_pair_tree, build_partition, shell_overlap_matrix, transpose_view)

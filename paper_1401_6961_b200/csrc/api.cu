@@ -328,7 +328,7 @@ int hxf_frontier(hxf_pairs* bra, hxf_pairs* ket, hxf_density* P, double tau_2e, 
     HXF_TRY({
         if (!bra || !ket || !P || !n_tasks) throw HxfError{HXF_EINVAL, "NULL argument"};
         set_device(bra->sys->device);
-        frontier_run(bra, ket, P, tau_2e, mode, symmetry == HXF_FOURFOLD, level, n_tasks, cost,
+        frontier_run(bra, ket, P, tau_2e, mode, symmetry == HXF_EIGHTFOLD ? 2 : (symmetry == HXF_FOURFOLD ? 1 : 0), level, n_tasks, cost,
                      cost_capacity, (cudaStream_t)stream);
     })
 }

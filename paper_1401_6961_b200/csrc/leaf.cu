@@ -73,6 +73,7 @@ struct ScreenArgs {
     const int* ncidk;
     const double* nveck;
     const double* nveck_tri;
+    int eight;                // eightfold: on a bra node == ket node task keep bra pair <= ket pair
 };
 
 struct WarpSmem {
@@ -359,6 +360,10 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         const bool bdiag = SYM && mu == nu, kdiag = SYM && lam == sig;
         const int ma = bdiag ? nmu * (nmu + 1) / 2 : nmu * nnu;
         const int mb = kdiag ? nlam * (nlam + 1) / 2 : nlam * nsig;
+        // eightfold: on a bra node == ket node task only quartets with bra pair <=
+        // ket pair exist (same enumeration on both sides); the bulk culls below
+        // count whole blocks, so such tasks take the per-quartet path throughout
+        const bool diag8 = SYM && a.eight && mu == lam && nu == sig;
         const float inv_nnu = 1.0f / nnu, inv_nsig = 1.0f / nsig, inv_nlam = 1.0f / nlam;
         // ---- stage density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
         const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                     lcell += sm.nvb[so + r] * pm * sm.nvk[sk + c];
                 }
             }
-            if (!__any_sync(0xffffffffu, anyp)) {
+            if (!__any_sync(0xffffffffu, anyp) && !diag8) {
                 if (lane == 0) n_cull += (long long)ma * mb * __popc(live & (SYM ? 0xf : 1));
                 ledger += lcell;
 #ifdef HXF_PROF_SCREEN
@@ -529,7 +534,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                 for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
                     if (!((live >> g) & 1)) continue;
                     const int r = (g == 0 || g == 2) ? y : x;
-                    if (!(fa * sm.rmax[g][r] * (1.0 + 1e-14) <= tau_skip)) {
+                    if (diag8 || !(fa * sm.rmax[g][r] * (1.0 + 1e-14) <= tau_skip)) {
                         amask |= 1 << g;
                     } else {
                         n_cull += mb;
@@ -559,7 +564,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                     ia = ent >> 8;
                     const int tmask = (ent >> 4) & 15;   // slots still open for this row
                     const int k = ent & 15;
-                    if (my_l < sm.nl[k]) {
+                    if (my_l < sm.nl[k] && !(diag8 && (int)sm.bstart[k] + my_l < ia)) {
                         ib = sm.bstart[k] + my_l;
                         const double fa = sm.fa[ia], fb = sm.fb[ib];
                         const int x = sm.ax[ia], y = sm.ay[ia], z = sm.bx[ib], w = sm.by[ib];
@@ -628,7 +633,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                         ub = fa * sm.z[g - 2][r * nlam + k] * (1.0 + 1e-15);
                         led = sa * sm.w[g - 2][r * nlam + k];
                     }
-                    if (!(ub <= tau_skip)) {
+                    if (diag8 || !(ub <= tau_skip)) {
                         tmask |= 1 << g;
                     } else {  // this slot culled for the whole row (no ties)
                         n_cull += sm.nl[k];
@@ -705,6 +710,7 @@ struct EriArgs {
     unsigned long long* K;
     long long* counters;
     const int64_t* dbounds;  // non-NULL: this class's record range is read on the device
+    int eight;               // eightfold: a quartet with bra pair == ket pair carries weight 1/2
 };
 
 __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double v) {
@@ -759,6 +765,9 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
             const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
             const int64_t n = e.nfn;
             const double* P = e.P;
+            // -1/2 exchange factor; eightfold: the self-mirror quartet (bra pair ==
+            // ket pair) enters A once and K = A + A^T, so it carries 1/2
+            const double half = (e.eight && pb == pk) ? -0.25 : -0.5;
 #define OUT(x, y, z, w) out[(((x) * NJ + (y)) * NK + (z)) * NL + (w)]
             if (mask & 1) {  // K[mu,sig] <- P[nu,lam]
                 for (int x = 0; x < NI; ++x)
@@ -766,7 +775,7 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
                         double s = 0.0;
                         for (int y = 0; y < NJ; ++y)
                             for (int z = 0; z < NK; ++z) s += __ldg(P + (fj + y) * n + fk + z) * OUT(x, y, z, w);
-                        k_add(e, fi + x, fl + w, -0.5 * s);
+                        k_add(e, fi + x, fl + w, half * s);
                     }
             }
             if (mask & 2) {  // K[nu,sig] <- P[mu,lam]
@@ -775,7 +784,7 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
                         double s = 0.0;
                         for (int x = 0; x < NI; ++x)
                             for (int z = 0; z < NK; ++z) s += __ldg(P + (fi + x) * n + fk + z) * OUT(x, y, z, w);
-                        k_add(e, fj + y, fl + w, -0.5 * s);
+                        k_add(e, fj + y, fl + w, half * s);
                     }
             }
             if (mask & 4) {  // K[mu,lam] <- P[nu,sig]
@@ -784,7 +793,7 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
                         double s = 0.0;
                         for (int y = 0; y < NJ; ++y)
                             for (int w = 0; w < NL; ++w) s += __ldg(P + (fj + y) * n + fl + w) * OUT(x, y, z, w);
-                        k_add(e, fi + x, fk + z, -0.5 * s);
+                        k_add(e, fi + x, fk + z, half * s);
                     }
             }
             if (mask & 8) {  // K[nu,lam] <- P[mu,sig]
@@ -793,7 +802,7 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
                         double s = 0.0;
                         for (int x = 0; x < NI; ++x)
                             for (int w = 0; w < NL; ++w) s += __ldg(P + (fi + x) * n + fl + w) * OUT(x, y, z, w);
-                        k_add(e, fj + y, fk + z, -0.5 * s);
+                        k_add(e, fj + y, fk + z, half * s);
                     }
             }
 #undef OUT
@@ -888,6 +897,23 @@ __global__ void k_fx_to_double(const unsigned long long* Kfx, int64_t n2, int S,
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2;
          t += (int64_t)gridDim.x * blockDim.x)
         K[t] = k_fixed_value(Kfx + t, S);
+}
+
+// eightfold epilogue: A + A^T on the fixed-point accumulator (integer, exact)
+__global__ void k_fold_fx(unsigned long long* K, int n) {
+    const int64_t n2 = (int64_t)n * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n2;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t / n), j = (int)(t % n);
+        if (i < j) {
+            const int64_t u = (int64_t)j * n + i;
+            const unsigned long long v = K[t] + K[u];
+            K[t] = v;
+            K[u] = v;
+        } else if (i == j) {
+            K[t] = K[t] * 2ull;
+        }
+    }
 }
 
 __global__ void k_asym(const double* K, int n, unsigned long long* out) {
@@ -1096,11 +1122,14 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     if (!(o->tau_2e >= 0.0)) throw HxfError{HXF_EINVAL, "tau_2e must be non-negative"};
     if (o->mode != HXF_MODE_SCHWARZ && o->mode != HXF_MODE_LITERAL)
         throw HxfError{HXF_EINVAL, "unknown screening mode"};
-    if (o->symmetry == HXF_FOURFOLD && bra != ket)
+    if (o->symmetry != HXF_NAIVE && o->symmetry != HXF_FOURFOLD && o->symmetry != HXF_EIGHTFOLD)
+        throw HxfError{HXF_EINVAL, "unknown symmetry driver"};
+    if (o->symmetry != HXF_NAIVE && bra != ket)
         throw HxfError{HXF_EINVAL, "the fourfold driver takes a single pair tree"};
     for (int k = 0; k < 8; ++k) g_timings[k] = 0.0;
     Timer ttot(st);
-    const int sym = o->symmetry == HXF_FOURFOLD;
+    const int sym = o->symmetry != HXF_NAIVE;
+    const int eight = o->symmetry == HXF_EIGHTFOLD;
     long long* dcount = lalloc<long long>(C_NCOUNTERS, st);
     unsigned long long* dledger = lalloc<unsigned long long>(LEDGER_LIMBS, st);
     HXF_CUDA(cudaMemsetAsync(dcount, 0, C_NCOUNTERS * sizeof(long long), st));
@@ -1108,7 +1137,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
 
     // ---- traversal
     Timer ttrav(st);
-    TravInput ti{s, bra, ket, dens, o->tau_2e, o->mode, sym, o->shard_level, o->shard_begin,
+    TravInput ti{s, bra, ket, dens, o->tau_2e, o->mode, eight ? 2 : sym, o->shard_level, o->shard_begin,
                  o->shard_end, 0, 0, dcount, dledger};
     TraversalResult tr = traverse(ti, st);
     g_timings[0] = ttrav.stop();
@@ -1165,6 +1194,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.nfn = s->nfn;
     sa.tau = o->tau_2e;
     sa.mode = o->mode;
+    sa.eight = eight;
 
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device);
@@ -1181,6 +1211,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * (sym ? 12 : 8)));
     auto launch_screen = [&](bool emit) {
         if (flat) {
+            if (eight) throw HxfError{HXF_EINVAL, "HXF_SCREEN=flat does not implement the eightfold driver"};
             if (sym) { if (emit) k_screen<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
             else { if (emit) k_screen<false, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<false, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
         } else {
@@ -1303,6 +1334,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         e.S = S;
         e.K = Kfx;
         e.counters = ecount;
+        e.eight = eight;
         cudaStream_t se = st;
         cudaEvent_t ev_in = nullptr, ev_scr[2] = {nullptr, nullptr}, ev_eri[2] = {nullptr, nullptr};
         if (pipe) {
@@ -1428,6 +1460,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
 
     // ---- epilogue
     Timer tep(st);
+    if (eight && Kfx) {  // K = A + A^T, exact in fixed point (each |entry| < 2^61)
+        k_fold_fx<<<1024, 256, 0, st>>>(Kfx, s->nfn);
+        note_launch();
+    }
     if (K_out && o->K_fixed) {
         if (!o->K_on_device) throw HxfError{HXF_EINVAL, "K_fixed requires K_on_device"};
         if (Kfx) HXF_CUDA(cudaMemcpyAsync(K_out, Kfx, n2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
@@ -1437,7 +1473,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         double* Kd = o->K_on_device ? K_out : lalloc<double>(n2, st);
         if (Kfx) {
             { k_fx_to_double<<<1024, 256, 0, st>>>(Kfx, n2, S, Kd); note_launch(); }
-            if (sym && o->symmetrize) {
+            if (sym && !eight && o->symmetrize) {
                 unsigned long long* dm = lalloc<unsigned long long>(1, st);
                 HXF_CUDA(cudaMemsetAsync(dm, 0, sizeof(unsigned long long), st));
                 { k_asym<<<1024, 256, 0, st>>>(Kd, s->nfn, dm); note_launch(); }
@@ -1780,6 +1816,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         e.S = S;
         e.K = Kfx;
         e.counters = scount;
+        e.eight = 0;
         da.off = off;
         da.rec = sb.rec;
         da.keys = sb.keys;

@@ -174,6 +174,7 @@ struct ExpandArgs {
     const int64_t* blk_off_leaf;
     long long* counters;
     unsigned long long* ledger;
+    int eight;         // eightfold: children of a bra == ket task keep (bra) <= (ket)
 };
 
 // children of a span (a leaf stands in for itself, quadtree.py:47-49)
@@ -242,6 +243,10 @@ __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
                 cn = kn[y];
                 cl = kl[z];
                 cs = ks[w];
+                // eightfold: a task with bra node == ket node spawns each mirror pair
+                // of children once (bra child <= ket child); tasks with bra < ket
+                // keep every child (their mirrors live under the excluded mirror task)
+                if (a.eight && mu == lam && nu == sig) valid = cm < cl || (cm == cl && cn <= cs);
             }
         }
         if (valid) v = SYM ? visit_sym(a.tv, a.child, cm, cn, cl, cs, alive)
@@ -481,6 +486,7 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         a.out_leaf = nullptr;
         a.blk_off_expand = oe;
         a.blk_off_leaf = ol;
+        a.eight = in.sym == 2;
         if (in.sym) { k_expand<true, false><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         else { k_expand<false, false><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         { k_unpack_counts<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(blk, nb, cl, ce); note_launch(); }

@@ -12,7 +12,7 @@ struct TravInput {
     hxf_density* dens;
     double tau;
     int mode;
-    int sym;
+    int sym;               // 0 naive, 1 fourfold, 2 eightfold (fourfold restricted to bra <= ket)
     int shard_level;       // < 0: whole tree
     int64_t shard_begin;
     int64_t shard_end;

@@ -41,14 +41,15 @@ def split_by_cost(costs, world: int):
 def frontier(bra, ket, P, tau_2e, mode, symmetry, level):
     """Expand-list size (and per-task cost estimates) at `level`."""
     n = ctypes.c_int64(0)
+    sym = 2 if symmetry == "eightfold" else (1 if symmetry else 0)
     _native.check(_native.lib().hxf_frontier(bra._t.handle, ket._t.handle, P._t.handle, float(tau_2e),
-                                             0 if mode == "schwarz" else 1, 1 if symmetry else 0,
+                                             0 if mode == "schwarz" else 1, sym,
                                              int(level), ctypes.byref(n), None, 0,
                                              _native.current_stream()))
     count = int(n.value)
     costs = np.empty(max(count, 1))
     _native.check(_native.lib().hxf_frontier(bra._t.handle, ket._t.handle, P._t.handle, float(tau_2e),
-                                             0 if mode == "schwarz" else 1, 1 if symmetry else 0,
+                                             0 if mode == "schwarz" else 1, sym,
                                              int(level), ctypes.byref(n), _native.ptr(costs), count,
                                              _native.current_stream()))
     return count, costs[:count]
@@ -129,7 +130,7 @@ def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, sha
     _native.check(_native.lib().hxf_fixed_to_double(ctypes.c_void_p(Kfx.data_ptr()), Kfx.numel(), S,
                                                     ctypes.c_void_p(K_dev.data_ptr()),
                                                     _native.current_stream()))
-    if symmetry:
+    if symmetry is True:  # fourfold; the eightfold K (A + A^T) is symmetric by construction
         _native.check(_native.lib().hxf_symmetrize(ctypes.c_void_p(K_dev.data_ptr()), K_dev.shape[0],
                                                    1e-10, _native.current_stream()))
     return counters_from_vector(vec.cpu().numpy(), symmetry), shards

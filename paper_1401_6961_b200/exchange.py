@@ -253,7 +253,8 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
     opts = _native.ExchangeOpts()
     opts.tau_2e = float(tau_2e)
     opts.mode = 0 if mode == "schwarz" else 1
-    opts.symmetry = 1 if symmetry else 0
+    # symmetry: False / True (fourfold) / "eightfold"
+    opts.symmetry = 2 if symmetry == "eightfold" else (1 if symmetry else 0)
     opts.evaluate = 1 if evaluate else 0
     opts.symmetrize = 1 if symmetrize else 0
     if shard is None:
@@ -350,6 +351,34 @@ def build_exchange_symmetric(pairs: ShellPairNode, P: MatrixQuadtree, tau_2e: fl
     """
     K, c, log = run_exchange(pairs, pairs, P, tau_2e, mode, True, evaluate, quartet_log,
                              symmetrize=evaluate)
+    out = SymmetryCounters()
+    _fill_common(out, c)
+    out.links_culled_screening = int(c.links_culled_screening)
+    out.links_culled_absent = int(c.links_culled_absent)
+    for g, lab in enumerate(CASE_LABELS):
+        out.case_tasks[lab] = int(c.case_tasks[g])
+        out.case_leaf_tasks[lab] = int(c.case_leaf_tasks[g])
+    if quartet_log is not None and log is not None:
+        quartet_log.extend(log)
+    return K, out
+
+
+def build_exchange_eightfold(pairs: ShellPairNode, P: MatrixQuadtree, tau_2e: float = 0.0,
+                             mode: str = "schwarz", quartet_log: list | None = None,
+                             evaluate: bool = True, threads: int = 1):
+    """(new) 8-fold mode: the 4-fold build folded bra <-> ket.
+
+    Evaluates only canonical quartets with bra pair <= ket pair (product-tree
+    tasks with bra node <= ket node; on a bra == ket leaf task, bra pair <= ket
+    pair) and forms K = A + A^T, A = sum_{bra < ket} C(q) + 1/2 sum_{bra = ket} C(q),
+    C(q) the 4-fold slot contributions of q: because P is symmetric, the
+    mirror quartet's contributions are C(q)^T and its culling decisions equal
+    q's.  The evaluated set is the 4-fold quartet_log folded to
+    {unordered (bra pair, ket pair)}.  Counters count this traversal (about half
+    the 4-fold tasks and quartets); K equals the 4-fold K within rounding.
+    Returns (K, SymmetryCounters).
+    """
+    K, c, log = run_exchange(pairs, pairs, P, tau_2e, mode, "eightfold", evaluate, quartet_log)
     out = SymmetryCounters()
     _fill_common(out, c)
     out.links_culled_screening = int(c.links_culled_screening)

@@ -212,3 +212,35 @@ def test_primitive_neglect_within_bound(sym, monkeypatch):
     K2, c2, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-8, "schwarz", sym)
     assert sum(int(x) for x in c2.class_prim_quartets) <= full
     assert np.abs(K2 - K0).max() <= 1e-12
+
+
+def _fold(log):
+    """4-fold quartet tuples folded bra <-> ket: {min((i,j,k,l), (k,l,i,j))}."""
+    return {min((i, j, k, l), (k, l, i, j)) for (i, j, k, l) in log}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["s_lattice", "p_cube"])
+def test_eightfold_matches_fourfold(case):
+    """Eightfold mode (optional): evaluated set = the 4-fold
+    quartet log folded to unordered (bra pair, ket pair); K equal to the 4-fold
+    K within rounding; about half the quartets."""
+    if case == "s_lattice":
+        cfg = configs.config1()
+        leaf = 4
+    else:
+        cfg = configs.cube_cluster(10, 7, "tiny")
+        leaf = 6
+    part = hx.build_partition(cfg.system, leaf_size=leaf)
+    pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
+    P_tree = hx.build_matrix_tree(cfg.P, part)
+    log4, log8 = [], []
+    K4, c4 = hx.build_exchange_symmetric(pairs, P_tree, tau_2e=1e-8, quartet_log=log4)
+    K8, c8 = hx.build_exchange_eightfold(pairs, P_tree, tau_2e=1e-8, quartet_log=log8)
+    assert c4.ties_leaf == 0 and c8.ties_leaf == 0 and c8.ties_task == 0
+    # each unordered (bra pair, ket pair) exactly once, and exactly the folded 4-fold set
+    assert len(log8) == len(_fold(log8)) == c8.eri_shell_quartets
+    assert _fold(log8) == _fold(log4)
+    assert np.array_equal(K8, K8.T)
+    assert np.abs(K8 - K4).max() <= 1e-12
+    assert c8.eri_shell_quartets < 0.6 * c4.eri_shell_quartets
