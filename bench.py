@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-units", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-eightfold", action="store_true",
+                    help="fourfold runs: skip the companion eightfold K-build timing")
     return ap.parse_args()
 
 
@@ -342,6 +344,35 @@ def native_arm(args):
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e2e_value = quartets * args.e2e_steps / (float(et.item()) * 1e-3) if args.e2e_steps else None
 
+    # companion eightfold build (same K, bra<->ket folded): K-build time, folded
+    # quartet count, and max |K8 - K4| against the fourfold K of the timed steps
+    eight = None
+    if args.mode == "fourfold" and world == 1 and not args.no_eightfold:
+        K4 = K_dev.clone()
+        K8 = torch.empty_like(K_dev)
+        e8 = []
+        c8 = None
+        for it in range(1 + args.steps):
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            Pt8 = hx.build_matrix_tree(P_dev, part)
+            _, c8, _ = exchange.run_exchange(pairs, pairs, Pt8, cfg.tau_2e, "schwarz", "eightfold", True,
+                                             None, K_out=K8)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            del Pt8
+            if it:  # the first is a warm-up
+                e8.append(a0.elapsed_time(a1))
+        ms8 = statistics.median(e8)
+        eight = {"k_build_ms": ms8, "surviving_quartets_per_step": int(c8.eri_shell_quartets),
+                 "prim_quartets_per_step": int(c8.prim_quartets),
+                 "fourfold_quartets_per_s": quartets / (ms8 * 1e-3),
+                 "max_abs_diff_vs_fourfold_K": float((K8 - K4).abs().max().item()),
+                 "note": "same K as the fourfold build (bra<->ket folded, K = A + A^T); "
+                         "fourfold_quartets_per_s = the fourfold surviving-quartet count / this K-build time"}
+        del K4, K8
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu(args, 1, 0)
@@ -383,6 +414,7 @@ def native_arm(args):
                     "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8,
                     "ms_per_step": float(et.item()) / max(args.e2e_steps, 1)},
             "cpu_baseline": cpu,
+            "eightfold": eight,
             "gpu_launches": int(lc1.value - lc0.value),
             "clocks": clk,
         }
