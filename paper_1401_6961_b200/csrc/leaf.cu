@@ -73,7 +73,6 @@ struct ScreenArgs {
     const int* ncidk;
     const double* nveck;
     const double* nveck_tri;
-    int eight;                // eightfold: on a bra node == ket node task keep bra pair <= ket pair
 };
 
 struct WarpSmem {
@@ -256,7 +255,7 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
                     const int ca = sm.acl[ia], cb = sm.bcl[ib];
                     const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
                     // sort key: class, bra / ket primitive-pair counts (uniform warps)
-                    slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60),
+                    slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56),
                               (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2)), lane);
                 }
             }
@@ -324,7 +323,8 @@ __device__ __forceinline__ int fdiv(int a, int n, float inv) {
     return __float2int_rz(((float)a + 0.5f) * inv);  // exact for a < 2^20, n <= 32
 }
 
-template <bool SYM, bool EMIT, int MS>
+// EIGHT (with SYM): the eightfold driver's bra pair <= ket pair rule on bra == ket tasks
+template <bool SYM, bool EMIT, int MS, bool EIGHT = false>
 __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(ScreenArgs a) {
     constexpr int NW = screen2_warps<SYM, MS>();
     __shared__ Smem2<SYM, MS> sm_all[NW];
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         // eightfold: on a bra node == ket node task only quartets with bra pair <=
         // ket pair exist (same enumeration on both sides); the bulk culls below
         // count whole blocks, so such tasks take the per-quartet path throughout
-        const bool diag8 = SYM && a.eight && mu == lam && nu == sig;
+        const bool diag8 = EIGHT && mu == lam && nu == sig;
         const float inv_nnu = 1.0f / nnu, inv_nsig = 1.0f / nsig, inv_nlam = 1.0f / nlam;
         // ---- stage density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
         const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
@@ -598,7 +598,9 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                         const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
                         const int ca = sm.acl[ia], cb = sm.bcl[ib];
                         const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
-                        slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56) | (cls << 60),
+                        // bit 60: eightfold self-mirror quartet (bra pair == ket pair), weight 1/2
+                        const uint64_t selfm = (EIGHT && pb == pk) ? 1ull : 0ull;
+                        slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56) | (selfm << 60),
                                   (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2)), lane);
                     }
                 }
@@ -710,7 +712,6 @@ struct EriArgs {
     unsigned long long* K;
     long long* counters;
     const int64_t* dbounds;  // non-NULL: this class's record range is read on the device
-    int eight;               // eightfold: a quartet with bra pair == ket pair carries weight 1/2
 };
 
 __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double v) {
@@ -766,8 +767,10 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
             const int64_t n = e.nfn;
             const double* P = e.P;
             // -1/2 exchange factor; eightfold: the self-mirror quartet (bra pair ==
-            // ket pair) enters A once and K = A + A^T, so it carries 1/2
-            const double half = (e.eight && pb == pk) ? -0.25 : -0.5;
+            // ket pair, record bit 60, only in classes with bra class == ket class)
+            // enters A once and K = A + A^T, so it carries 1/2
+            double half = -0.5;
+            if constexpr (LA == LC && LB == LD) half = ((r >> 60) & 1) ? -0.25 : -0.5;
 #define OUT(x, y, z, w) out[(((x) * NJ + (y)) * NK + (z)) * NL + (w)]
             if (mask & 1) {  // K[mu,sig] <- P[nu,lam]
                 for (int x = 0; x < NI; ++x)
@@ -1194,7 +1197,6 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.nfn = s->nfn;
     sa.tau = o->tau_2e;
     sa.mode = o->mode;
-    sa.eight = eight;
 
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device);
@@ -1217,10 +1219,12 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         } else {
             const dim3 g(screen_grid), b(sw * 32);
             if (ms8) {
-                if (sym) { if (emit) k_screen2<true, true, 8><<<g, b, 0, st>>>(sa); else k_screen2<true, false, 8><<<g, b, 0, st>>>(sa); }
+                if (eight) { if (emit) k_screen2<true, true, 8, true><<<g, b, 0, st>>>(sa); else k_screen2<true, false, 8, true><<<g, b, 0, st>>>(sa); }
+                else if (sym) { if (emit) k_screen2<true, true, 8><<<g, b, 0, st>>>(sa); else k_screen2<true, false, 8><<<g, b, 0, st>>>(sa); }
                 else { if (emit) k_screen2<false, true, 8><<<g, b, 0, st>>>(sa); else k_screen2<false, false, 8><<<g, b, 0, st>>>(sa); }
             } else {
-                if (sym) { if (emit) k_screen2<true, true, 10><<<g, b, 0, st>>>(sa); else k_screen2<true, false, 10><<<g, b, 0, st>>>(sa); }
+                if (eight) { if (emit) k_screen2<true, true, 10, true><<<g, b, 0, st>>>(sa); else k_screen2<true, false, 10, true><<<g, b, 0, st>>>(sa); }
+                else if (sym) { if (emit) k_screen2<true, true, 10><<<g, b, 0, st>>>(sa); else k_screen2<true, false, 10><<<g, b, 0, st>>>(sa); }
                 else { if (emit) k_screen2<false, true, 10><<<g, b, 0, st>>>(sa); else k_screen2<false, false, 10><<<g, b, 0, st>>>(sa); }
             }
         }
@@ -1334,7 +1338,6 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         e.S = S;
         e.K = Kfx;
         e.counters = ecount;
-        e.eight = eight;
         cudaStream_t se = st;
         cudaEvent_t ev_in = nullptr, ev_scr[2] = {nullptr, nullptr}, ev_eri[2] = {nullptr, nullptr};
         if (pipe) {
@@ -1680,7 +1683,7 @@ __global__ void __launch_bounds__(256) k_direct(DirectArgs a, int64_t p0, int64_
                     const int pk = a.pidm[(int64_t)k * ns + lrow[t]];
                     const int cb = a.meta[pk];
                     const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
-                    a.rec[pos] = (uint64_t)p | ((uint64_t)pk << 28) | (1ull << 56) | (cls << 60);
+                    a.rec[pos] = (uint64_t)p | ((uint64_t)pk << 28) | (1ull << 56);
                     a.keys[pos] = (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2));
                 }
             }
@@ -1816,7 +1819,6 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         e.S = S;
         e.K = Kfx;
         e.counters = scount;
-        e.eight = 0;
         da.off = off;
         da.rec = sb.rec;
         da.keys = sb.keys;

@@ -175,6 +175,7 @@ struct ExpandArgs {
     long long* counters;
     unsigned long long* ledger;
     int eight;         // eightfold: children of a bra == ket task keep (bra) <= (ket)
+    uint8_t* outc;     // per child thread: is_leaf | is_expand << 1 | live << 2 (count pass -> write pass)
 };
 
 // children of a span (a leaf stands in for itself, quadtree.py:47-49)
@@ -204,6 +205,58 @@ __device__ __forceinline__ bool canon_key(int key, int r, int c, int nr, int nc,
     return true;
 }
 
+// Two passes per level.  Count pass: visit every child (norm gathers, bounds,
+// counters, ledger), store a one-byte outcome per child and the block's leaf /
+// expand counts.  Write pass: re-read the outcome byte (no second visit), scan,
+// write the children's task words at their deterministic positions.
+template <bool SYM>
+__device__ __forceinline__ bool child_spans(const ExpandArgs& a, uint64_t task, int c, int* cm, int* cn,
+                                            int* cl, int* cs) {
+    const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
+              sig = (task >> 45) & 0x7fff;
+    int km[2], kn[2], kl[2], ks[2];
+    const int nm = kids(a, mu, km), nn = kids(a, nu, kn), nl = kids(a, lam, kl), ns = kids(a, sig, ks);
+    bool valid;
+    if (!SYM) {
+        const int ia = (c >> 3) & 1, ic = (c >> 2) & 1, id = (c >> 1) & 1, ibb = c & 1;
+        valid = ia < nm && ic < nn && id < nl && ibb < ns;
+        if (valid) {
+            *cm = km[ia];
+            *cn = kn[ic];
+            *cl = kl[id];
+            *cs = ks[ibb];
+        }
+    } else {
+        int x, y, z, w;
+        valid = canon_key(c >> 2, mu, nu, nm, nn, &x, &y) && canon_key(c & 3, lam, sig, nl, ns, &z, &w);
+        if (valid) {
+            *cm = km[x];
+            *cn = kn[y];
+            *cl = kl[z];
+            *cs = ks[w];
+            // eightfold: a task with bra node == ket node spawns each mirror pair
+            // of children once (bra child <= ket child); tasks with bra < ket
+            // keep every child (their mirrors live under the excluded mirror task)
+            if (a.eight && mu == lam && nu == sig) valid = *cm < *cl || (*cm == *cl && *cn <= *cs);
+        }
+    }
+    return valid;
+}
+
+// per-warp sum of 6-bit (or 8-bit) packed per-thread counts: one reduction per word
+template <int N>
+__device__ __forceinline__ void flush_packed(long long* counters, unsigned word, int bits, const int (&slots)[N]) {
+    const unsigned s = __reduce_add_sync(0xffffffffu, word);
+    if ((threadIdx.x & 31) == 0 && s) {
+        const unsigned m = (1u << bits) - 1u;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const unsigned v = (s >> (bits * k)) & m;
+            if (v) atomic_add_ll(&counters[slots[k]], (long long)v);
+        }
+    }
+}
+
 template <bool SYM, bool WRITE>
 __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
     typedef cub::BlockScan<int, 256> Scan;
@@ -215,86 +268,69 @@ __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
     const int64_t t = blockIdx.x * 256ll + threadIdx.x;
     const int64_t parent = t >> 4;
     const int c = (int)(t & 15);
-    Visit v{O_NONE, 0, 0, 0, 0, 0, 0.0};
-    int cm = 0, cn = 0, cl = 0, cs = 0;
-    if (parent < a.n_in) {
-        const uint64_t task = a.in[parent];
-        const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
-                  sig = (task >> 45) & 0x7fff;
-        const int alive = (int)(task >> 60);
-        int km[2], kn[2], kl[2], ks[2];
-        const int nm = kids(a, mu, km), nn = kids(a, nu, kn), nl = kids(a, lam, kl),
-                  ns = kids(a, sig, ks);
-        bool valid;
-        if (!SYM) {
-            const int ia = (c >> 3) & 1, ic = (c >> 2) & 1, id = (c >> 1) & 1, ibb = c & 1;
-            valid = ia < nm && ic < nn && id < nl && ibb < ns;
-            if (valid) {
-                cm = km[ia];
-                cn = kn[ic];
-                cl = kl[id];
-                cs = ks[ibb];
-            }
-        } else {
-            int x, y, z, w;
-            valid = canon_key(c >> 2, mu, nu, nm, nn, &x, &y) && canon_key(c & 3, lam, sig, nl, ns, &z, &w);
-            if (valid) {
-                cm = km[x];
-                cn = kn[y];
-                cl = kl[z];
-                cs = ks[w];
-                // eightfold: a task with bra node == ket node spawns each mirror pair
-                // of children once (bra child <= ket child); tasks with bra < ket
-                // keep every child (their mirrors live under the excluded mirror task)
-                if (a.eight && mu == lam && nu == sig) valid = cm < cl || (cm == cl && cn <= cs);
+    if (WRITE) {
+        const int oc = parent < a.n_in ? a.outc[t] : 0;
+        const int is_leaf = oc & 1, is_exp = (oc >> 1) & 1, live = oc >> 2;
+        int packed = is_leaf | (is_exp << 16), excl, total;
+        Scan(tmp.scan).ExclusiveSum(packed, excl, total);
+        if (is_leaf | is_exp) {
+            int cm = 0, cn = 0, cl = 0, cs = 0;
+            child_spans<SYM>(a, a.in[parent], c, &cm, &cn, &cl, &cs);
+            if (is_leaf) {
+                const int lid[4] = {a.child.leaf_id[cm], a.child.leaf_id[cn], a.child.leaf_id[cl], a.child.leaf_id[cs]};
+                a.out_leaf[a.blk_off_leaf[blockIdx.x] + (excl & 0xffff)] = pack_task(lid[0], lid[1], lid[2], lid[3], live);
+            } else {
+                a.out_expand[a.blk_off_expand[blockIdx.x] + (excl >> 16)] = pack_task(cm, cn, cl, cs, live);
             }
         }
-        if (valid) v = SYM ? visit_sym(a.tv, a.child, cm, cn, cl, cs, alive)
-                           : visit_naive(a.tv, a.child, cm, cn, cl, cs);
+        return;
+    }
+    Visit v{O_NONE, 0, 0, 0, 0, 0, 0.0};
+    if (parent < a.n_in) {
+        const uint64_t task = a.in[parent];
+        int cm = 0, cn = 0, cl = 0, cs = 0;
+        if (child_spans<SYM>(a, task, c, &cm, &cn, &cl, &cs))
+            v = SYM ? visit_sym(a.tv, a.child, cm, cn, cl, cs, (int)(task >> 60))
+                    : visit_naive(a.tv, a.child, cm, cn, cl, cs);
+        const int is_leaf = v.outcome == O_LEAF, is_exp = v.outcome == O_EXPAND;
+        a.outc[t] = (uint8_t)(is_leaf | (is_exp << 1) | ((is_leaf | is_exp) ? (v.live << 2) : 0));
     }
     const int is_leaf = v.outcome == O_LEAF, is_exp = v.outcome == O_EXPAND;
     int packed = is_leaf | (is_exp << 16), excl, total;
     Scan(tmp.scan).ExclusiveSum(packed, excl, total);
-    if (!WRITE) {
-        if (threadIdx.x == 0) a.blk_counts[blockIdx.x] = total;
-        return;
-    }
-    if (is_leaf) {
-        const int lid[4] = {a.child.leaf_id[cm], a.child.leaf_id[cn], a.child.leaf_id[cl], a.child.leaf_id[cs]};
-        a.out_leaf[a.blk_off_leaf[blockIdx.x] + (excl & 0xffff)] = pack_task(lid[0], lid[1], lid[2], lid[3], v.live);
-    }
-    if (is_exp) a.out_expand[a.blk_off_expand[blockIdx.x] + (excl >> 16)] = pack_task(cm, cn, cl, cs, v.live);
-    // counters: warp-aggregated integer atomics (order independent) into one
-    // of TRAV_STRIPES copies, so the ~10^8 warps of a deep level do not all
-    // serialise on the same few addresses; k_fold_stripes sums the copies
+    if (threadIdx.x == 0) a.blk_counts[blockIdx.x] = total;
+    // counters: per-warp sums of packed per-thread counts, warp-aggregated
+    // integer atomics (order independent) into one of TRAV_STRIPES copies, so
+    // the ~10^8 warps of a deep level do not all serialise on the same addresses;
+    // k_fold_stripes sums the copies
     long long* counters = a.counters + (blockIdx.x % TRAV_STRIPES) * C_NCOUNTERS;
     unsigned long long* ledger = a.ledger + (blockIdx.x % TRAV_STRIPES) * LEDGER_LIMBS;
-    const unsigned full = 0xffffffffu;
-    const int valid_child = v.outcome != O_NONE;
-    int vals[8] = {valid_child, v.outcome == O_SCREEN, v.outcome == O_ABSENT, is_leaf, is_exp,
-                   v.tie, v.links_screen, v.links_absent};
-    const int slots[8] = {C_VISITED, C_CULL_SCREEN, C_CULL_ABSENT, C_LEAF, C_EXPANDED, C_TIE_TASK,
-                          C_LINK_SCREEN, C_LINK_ABSENT};
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int s = __reduce_add_sync(full, vals[k]);
-        if ((threadIdx.x & 31) == 0 && s) atomic_add_ll(&counters[slots[k]], (long long)s);
-    }
+    const unsigned valid_child = v.outcome != O_NONE;
     {
-        const int s = __reduce_add_sync(full, valid_child);
-        if ((threadIdx.x & 31) == 0 && s) atomic_add_ll(&counters[C_SPAWNED], (long long)s);
+        const unsigned w0 = valid_child | (valid_child << 6) | ((unsigned)(v.outcome == O_SCREEN) << 12) |
+                            ((unsigned)(v.outcome == O_ABSENT) << 18) | ((unsigned)is_leaf << 24);
+        const int s0[5] = {C_VISITED, C_SPAWNED, C_CULL_SCREEN, C_CULL_ABSENT, C_LEAF};
+        flush_packed(counters, w0, 6, s0);
+        const unsigned w1 = (unsigned)is_exp | ((unsigned)v.tie << 8) | ((unsigned)v.links_screen << 16) |
+                            ((unsigned)v.links_absent << 24);
+        const int s1[4] = {C_EXPANDED, C_TIE_TASK, C_LINK_SCREEN, C_LINK_ABSENT};
+        flush_packed(counters, w1, 8, s1);
     }
     if (SYM) {
-        const bool counted = is_leaf || is_exp;
-#pragma unroll
-        for (int k = 0; k < HXF_NCASES; ++k) {
-            const int s1 = __reduce_add_sync(full, (int)(counted && v.label == k));
-            const int s2 = __reduce_add_sync(full, (int)(is_leaf && v.label == k));
-            if ((threadIdx.x & 31) == 0) {
-                if (s1) atomic_add_ll(&counters[C_CASE0 + k], (long long)s1);
-                if (s2) atomic_add_ll(&counters[C_CASELEAF0 + k], (long long)s2);
-            }
-        }
+        const unsigned counted = (unsigned)(is_leaf || is_exp);
+        const unsigned lab = (unsigned)v.label;
+        // one-hot label fields: labels 0-4 in one word, 5-8 in the next
+        const unsigned c_lo = lab < 5 ? counted << (6 * lab) : 0u, c_hi = lab >= 5 ? counted << (6 * (lab - 5)) : 0u;
+        const unsigned l_lo = lab < 5 ? (unsigned)is_leaf << (6 * lab) : 0u,
+                       l_hi = lab >= 5 ? (unsigned)is_leaf << (6 * (lab - 5)) : 0u;
+        const int sc0[5] = {C_CASE0, C_CASE0 + 1, C_CASE0 + 2, C_CASE0 + 3, C_CASE0 + 4};
+        const int sc1[4] = {C_CASE0 + 5, C_CASE0 + 6, C_CASE0 + 7, C_CASE0 + 8};
+        const int sl0[5] = {C_CASELEAF0, C_CASELEAF0 + 1, C_CASELEAF0 + 2, C_CASELEAF0 + 3, C_CASELEAF0 + 4};
+        const int sl1[4] = {C_CASELEAF0 + 5, C_CASELEAF0 + 6, C_CASELEAF0 + 7, C_CASELEAF0 + 8};
+        flush_packed(counters, c_lo, 6, sc0);
+        flush_packed(counters, c_hi, 6, sc1);
+        flush_packed(counters, l_lo, 6, sl0);
+        flush_packed(counters, l_hi, 6, sl1);
     }
     __syncthreads();
     const double lsum = Red(tmp.red).Sum(v.ledger);
@@ -472,7 +508,9 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         int64_t* ce = talloc<int64_t>(nb + 1, st);
         int64_t* ol = talloc<int64_t>(nb + 1, st);
         int64_t* oe = talloc<int64_t>(nb + 1, st);
+        uint8_t* outc = talloc<uint8_t>(nthreads, st);
         ExpandArgs a;
+        a.outc = outc;
         a.in = cur;
         a.n_in = n_cur;
         a.kid0 = s->lv.kid0 + s->h_off[L];
@@ -508,7 +546,7 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         if (in.sym) { k_expand<true, true><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         else { k_expand<false, true><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         HXF_CUDA(cudaGetLastError());
-        for (void* p : {(void*)blk, (void*)cl, (void*)ce, (void*)ol, (void*)oe, tbuf, (void*)cur})
+        for (void* p : {(void*)blk, (void*)cl, (void*)ce, (void*)ol, (void*)oe, tbuf, (void*)cur, (void*)outc})
             cudaFreeAsync(p, st);
         if (tot[0]) {
             leaf_parts.push_back(lf);

@@ -18,7 +18,8 @@ part = hx.build_partition(cfg.system, cfg.leaf_size)
 pairs = hx.build_pair_tree(cfg.system, part, cfg.tau_ovlp)
 for _ in range(reps):
     Pt = hx.build_matrix_tree(cfg.P, part)
-    K, c, _ = exchange.run_exchange(pairs, pairs, Pt, cfg.tau_2e, "schwarz", mode == "fourfold")
+    K, c, _ = exchange.run_exchange(pairs, pairs, Pt, cfg.tau_2e, "schwarz",
+                                    "eightfold" if mode == "eightfold" else mode == "fourfold")
     t = exchange.last_timings()
     print(name, mode, "quartets", c.eri_shell_quartets, "prim", c.prim_quartets,
           "stages_ms", [round(x, 2) for x in t], flush=True)
