@@ -133,7 +133,7 @@ def test_repeated_builds_bitwise_identical():
         assert c1.to_dict() == c2.to_dict()
 
 
-@pytest.mark.parametrize("sym", [False, True])
+@pytest.mark.parametrize("sym", [False, True, "eightfold"])
 def test_sharded_shards_sum_to_full_build(sym):
     """Multi-GPU semantics on one device: the shards of a frontier cut, run one
     after another, sum (K and counters) to the unsharded build."""
@@ -153,7 +153,7 @@ def test_sharded_shards_sum_to_full_build(sym):
                                              shard=(level, b, e), symmetrize=False)
             K += Ks
             vec = vec + distributed.counters_vector(c)
-        if sym:
+        if sym is True:
             K = hx.symmetrize_final(K)
         full = distributed.counters_vector(c_full)
         assert np.array_equal(vec[:-1], full[:-1]), (world, level, ranges)
@@ -179,7 +179,7 @@ def test_sharded_shards_sum_to_full_build(sym):
                                                         scales.pop(), ctypes.c_void_p(Kx.data_ptr()),
                                                         _native.current_stream()))
         Kx = Kx.cpu().numpy()
-        if sym:
+        if sym is True:
             Kx = hx.symmetrize_final(Kx)
         assert np.array_equal(Kx, K_full), np.abs(Kx - K_full).max()
 
