@@ -319,6 +319,13 @@ constexpr int screen2_warps() {  // static smem <= 48 KB per block
     return MS <= 8 ? (SYM ? 6 : 12) : (SYM ? 4 : 8);
 }
 
+// 1/n for the span sizes n <= 32 (fdiv's reciprocal), a constant-bank lookup
+// instead of an IEEE single division per use
+__constant__ float c_inv[33] = {0.f, 1.f / 1, 1.f / 2, 1.f / 3, 1.f / 4, 1.f / 5, 1.f / 6, 1.f / 7, 1.f / 8,
+                                1.f / 9, 1.f / 10, 1.f / 11, 1.f / 12, 1.f / 13, 1.f / 14, 1.f / 15, 1.f / 16,
+                                1.f / 17, 1.f / 18, 1.f / 19, 1.f / 20, 1.f / 21, 1.f / 22, 1.f / 23, 1.f / 24,
+                                1.f / 25, 1.f / 26, 1.f / 27, 1.f / 28, 1.f / 29, 1.f / 30, 1.f / 31, 1.f / 32};
+
 __device__ __forceinline__ int fdiv(int a, int n, float inv) {
     return __float2int_rz(((float)a + 0.5f) * inv);  // exact for a < 2^20, n <= 32
 }
@@ -364,14 +371,14 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         // ket pair exist (same enumeration on both sides); the bulk culls below
         // count whole blocks, so such tasks take the per-quartet path throughout
         const bool diag8 = EIGHT && mu == lam && nu == sig;
-        const float inv_nnu = 1.0f / nnu, inv_nsig = 1.0f / nsig, inv_nlam = 1.0f / nlam;
+        const float inv_nnu = c_inv[nnu], inv_nsig = c_inv[nsig], inv_nlam = c_inv[nlam];
         // ---- stage density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
         const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
         const int cs[4] = {slam, slam, ssig, ssig}, cn[4] = {nlam, nlam, nsig, nsig};
 #pragma unroll
         for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
             if (!((live >> g) & 1)) continue;
-            const float inv = 1.0f / cn[g];
+            const float inv = c_inv[cn[g]];
 #pragma unroll 1
             for (int i = lane; i < rn[g] * cn[g]; i += 32) {
                 const int x = fdiv(i, cn[g], inv), y = i - x * cn[g];
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                 if (!((live >> g) & 1)) continue;
                 const int fo = (g == 0 || g == 2) ? MS : 0, so = fo + 2 * MS;   // F_C / F_R, S_C / S_R
                 const int fk = g < 2 ? 0 : MS, sk = fk + 2 * MS;
-                const float inv = 1.0f / cn[g];
+                const float inv = c_inv[cn[g]];
 #pragma unroll 1
                 for (int i = lane; i < rn[g] * cn[g]; i += 32) {
                     const int r = fdiv(i, cn[g], inv), c = i - r * cn[g];
