@@ -202,7 +202,7 @@ void hxf_pairs_destroy(hxf_pairs* p) {
     cudaSetDevice(p->device);
     void* ptrs[] = {p->norm, p->rowsum, p->colsum, p->smax, p->leaf_base, p->pi,
                     p->pj,   p->ppoff,  p->q,      p->pp,       p->info, p->sq, p->meta,
-                    p->ncid, p->nvec,   p->nvec_tri, p->epp, p->eS};
+                    p->ncid, p->nvec,   p->nvec_tri, p->epp, p->eS, p->snorm, p->srow, p->scol};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     delete p;

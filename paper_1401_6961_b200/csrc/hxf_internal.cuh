@@ -85,6 +85,9 @@ struct hxf_pairs {
     double* rowsum;
     double* colsum;
     double* smax;      // block max |S|
+    double* snorm;     // per node: sqrt(diag_norm) (Schwarz task factor), -1 where pruned
+    double* srow;      // per node: sqrt(max(rowsum, 0)), sqrt(max(colsum, 0)) (ledger factors)
+    double* scol;
     int64_t* leaf_base;  // per leaf pair (nleaf^2): first pair id, -1 if pruned
     int64_t n_pairs;
     int* pi;           // per pair id: shells

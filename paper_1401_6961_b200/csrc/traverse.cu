@@ -33,11 +33,13 @@ struct LevelView {
     const int* flo;
 };
 
+// bf / kf: the task factors f(norm) (sqrt(norm) for Schwarz, norm for literal),
+// negative where pruned; b/k row, col: sqrt of the row / column sum maxima
 struct TreeView {
-    const double* bnorm;
+    const double* bf;
     const double* brow;
     const double* bcol;
-    const double* knorm;
+    const double* kf;
     const double* krow;
     const double* kcol;
     const double* pnorm;
@@ -55,15 +57,15 @@ struct Visit {
     double ledger;
 };
 
-__device__ __forceinline__ double fnorm(double v, int mode) { return mode == HXF_MODE_SCHWARZ ? sqrt(v) : v; }
 
 __device__ __forceinline__ bool is_tie(double bound, double tau) {
     return tau > 0.0 && fabs(bound - tau) <= 1e-12 * tau;
 }
 
-// culled_task_bound (exchange_naive.py:91-102)
-__device__ __forceinline__ double ledger_term(double pn, double bs, double ks) {
-    return __dmul_rn(__dmul_rn(__dmul_rn(0.5, pn), sqrt(fmax(bs, 0.0))), sqrt(fmax(ks, 0.0)));
+// culled_task_bound (exchange_naive.py:91-102); sbs / sks: the precomputed
+// sqrt(max(rowsum or colsum, 0)) of the bra / ket node
+__device__ __forceinline__ double ledger_term(double pn, double sbs, double sks) {
+    return __dmul_rn(__dmul_rn(__dmul_rn(0.5, pn), sbs), sks);
 }
 
 __device__ Visit visit_naive(const TreeView& tv, const LevelView& lv, int mu, int nu, int lam,
@@ -73,12 +75,12 @@ __device__ Visit visit_naive(const TreeView& tv, const LevelView& lv, int mu, in
     const int64_t ib = lv.node_off + mu * n + nu;
     const int64_t ip = lv.node_off + nu * n + lam;
     const int64_t ik = lv.node_off + lam * n + sig;
-    const double nb = tv.bnorm[ib], np = tv.pnorm[ip], nk = tv.knorm[ik];
-    if (nb < 0.0 || np < 0.0 || nk < 0.0) {
+    const double fb = tv.bf[ib], np = tv.pnorm[ip], fk = tv.kf[ik];
+    if (fb < 0.0 || np < 0.0 || fk < 0.0) {
         v.outcome = O_ABSENT;
         return v;
     }
-    const double bound = sorted_product3(fnorm(nb, tv.mode), np, fnorm(nk, tv.mode));
+    const double bound = sorted_product3(fb, np, fk);
     v.tie = is_tie(bound, tv.tau);
     if (bound <= tv.tau) {
         v.outcome = O_SCREEN;
@@ -113,12 +115,11 @@ __device__ Visit visit_sym(const TreeView& tv, const LevelView& lv, int mu, int 
     const int64_t n = lv.n;
     const int64_t ib = lv.node_off + mu * n + nu;
     const int64_t ik = lv.node_off + lam * n + sig;
-    const double nb = tv.bnorm[ib], nk = tv.knorm[ik];
-    if (nb < 0.0 || nk < 0.0) {
+    const double fb = tv.bf[ib], fk = tv.kf[ik];
+    if (fb < 0.0 || fk < 0.0) {
         v.outcome = O_ABSENT;
         return v;
     }
-    const double fb = fnorm(nb, tv.mode), fk = fnorm(nk, tv.mode);
     // slot refs: g0 P[nu,lam], g1 P[mu,lam], g2 P[nu,sig], g3 P[mu,sig]
     const int rr[4] = {nu, mu, nu, mu}, rc[4] = {lam, lam, sig, sig};
     bool screened = false, absent = false;
@@ -417,8 +418,9 @@ __global__ void k_unpack_counts(const int* packed, int64_t n, int64_t* leaf, int
 // tasks produced above the cut are discarded (they belong to rank 0).
 TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     hxf_system* s = in.sys;
-    TreeView tv{in.bra->norm, in.bra->rowsum, in.bra->colsum, in.ket->norm, in.ket->rowsum,
-                in.ket->colsum, in.dens->norm, in.tau, in.mode};
+    const bool schwarz = in.mode == HXF_MODE_SCHWARZ;
+    TreeView tv{schwarz ? in.bra->snorm : in.bra->norm, in.bra->srow, in.bra->scol,
+                schwarz ? in.ket->snorm : in.ket->norm, in.ket->srow, in.ket->scol, in.dens->norm, in.tau, in.mode};
     TraversalResult res;
     res.leaf = nullptr;
     res.n_leaf = 0;

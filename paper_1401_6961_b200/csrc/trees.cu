@@ -406,6 +406,16 @@ __global__ void k_live_ids(const int64_t* leaf_base, int64_t n, int* ncid) {
     if (t < n && leaf_base[t] < 0) ncid[t] = -1;
 }
 
+__global__ void k_node_sqrts(int64_t n, const double* norm, const double* row, const double* col, double* snorm,
+                             double* srow, double* scol) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const double v = norm[t];
+    snorm[t] = v < 0.0 ? -1.0 : sqrt(v);
+    srow[t] = sqrt(fmax(row[t], 0.0));
+    scol[t] = sqrt(fmax(col[t], 0.0));
+}
+
 // per shell: sum of n_f(partner) sqrt(Q) over the pairs that contain it (K scale bound)
 __global__ void k_pair_asum(DevBasis b, int64_t n, const int* pi, const int* pj, const double* sq, double* asum) {
     const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -586,6 +596,12 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
             L, n, nnext, d_off + L, s->lv.leaf_id, s->lv.kid0, s->lv.kid1, nl, lnorm, lrow, lcol,
             lsmax, pr->tau_ovlp, d_node_off, pr->norm, pr->rowsum, pr->colsum, pr->smax); note_launch(); }
     }
+    // the traversal's per-node square roots, once per pair tree (correctly rounded:
+    // bitwise what a per-visit sqrt would give)
+    pr->snorm = dalloc<double>(nn, st);
+    pr->srow = dalloc<double>(nn, st);
+    pr->scol = dalloc<double>(nn, st);
+    { k_node_sqrts<<<nblk(nn), 256, 0, st>>>(nn, pr->norm, pr->rowsum, pr->colsum, pr->snorm, pr->srow, pr->scol); note_launch(); }
     unsigned long long* dmax = dalloc<unsigned long long>(1, st);
     tmp.push_back(dmax);
     HXF_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
