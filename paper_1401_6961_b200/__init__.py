@@ -15,4 +15,6 @@ from .exchange import (CASE_LABELS, SymmetryCase, SymmetryCounters, TraversalCou
 from .quadtree import (MatrixQuadtree, Partition, ShellPairNode, Span, build_matrix_tree,
                        build_pair_tree, build_partition, shell_overlap_matrix, transpose_view)
 
+from .harness import RunConfig, load_report_schema, run_report, scaling_series
+
 __version__ = "0.1.0"
