@@ -354,7 +354,7 @@ def native_arm(args):
     shard = None
     if world > 1:
         lv, rng = shards
-        shard = (lv, rng[rank][0], rng[rank][1])
+        shard = (lv,) + tuple(rng[rank])
     _, craw, _ = exchange.run_exchange(pairs, pairs, P_tree, cfg.tau_2e, "schwarz", sym, True, None,
                                        K_out=K_dev, shard=shard, symmetrize=not (world > 1))
     tm = exchange.last_timings()

@@ -75,8 +75,8 @@ typedef struct hxf_counters {
 
 /* Exchange options.  The shard fields select a subset of the product-tree
  * tasks at level `shard_level` (tasks [shard_begin, shard_end) of that
- * level's frontier, in frontier order) for multi-GPU runs; shard_level < 0
- * runs the whole tree. */
+ * level's frontier, in frontier order, every shard_stride-th one when
+ * shard_stride > 1) for multi-GPU runs; shard_level < 0 runs the whole tree. */
 typedef struct hxf_exchange_opts {
     double tau_2e;
     int mode;          /* HXF_MODE_*   */
@@ -106,6 +106,9 @@ typedef struct hxf_exchange_opts {
        hxf_fixed_to_double converts.  symmetrize is ignored. */
     int K_fixed;
     int* K_scale;
+    /* <= 1: contiguous shard range; s > 1: tasks shard_begin, shard_begin + s,
+       ... below shard_end (cyclic assignment: rank r of N takes begin r, stride N) */
+    int64_t shard_stride;
 } hxf_exchange_opts;
 
 const char* hxf_last_error(void);

@@ -69,7 +69,8 @@ class ExchangeOpts(ctypes.Structure):
                 ("digest_mod", ctypes.c_int),
                 ("digest_rem", ctypes.c_int),
                 ("K_fixed", ctypes.c_int),
-                ("K_scale", ctypes.POINTER(ctypes.c_int))]
+                ("K_scale", ctypes.POINTER(ctypes.c_int)),
+                ("shard_stride", ctypes.c_int64)]
 
 
 _lib = None

@@ -414,7 +414,7 @@ __global__ void k_unpack_counts(const int* packed, int64_t n, int64_t* leaf, int
 // Run the traversal.  Returns the leaf-task list (device, caller frees with
 // cudaFreeAsync).  Counters / ledger are accumulated into the device arrays.
 // If shard_level >= 0 the expand frontier at that level is restricted to
-// [shard_begin, shard_end) and, unless shard_begin == 0, counters and leaf
+// [shard_begin, shard_end) (every shard_stride-th task) and, unless shard_begin == 0, counters and leaf
 // tasks produced above the cut are discarded (they belong to rank 0).
 TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     hxf_system* s = in.sys;
@@ -480,12 +480,15 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
             // restrict the frontier to this shard; from here on counters are real
             const int64_t b = std::min<int64_t>(in.shard_begin, n_cur);
             const int64_t e = std::min<int64_t>(std::max<int64_t>(in.shard_end, b), n_cur);
-            uint64_t* part = talloc<uint64_t>(e - b, st);
-            if (e > b)
-                HXF_CUDA(cudaMemcpyAsync(part, cur + b, (e - b) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+            const int64_t stride = std::max<int64_t>(in.shard_stride, 1);
+            const int64_t cnt = (e - b + stride - 1) / stride;
+            uint64_t* part = talloc<uint64_t>(std::max<int64_t>(cnt, 1), st);
+            if (cnt > 0)  // every stride-th task: a 2D copy of 8-byte rows
+                HXF_CUDA(cudaMemcpy2DAsync(part, sizeof(uint64_t), cur + b, stride * sizeof(uint64_t),
+                                           sizeof(uint64_t), cnt, cudaMemcpyDeviceToDevice, st));
             cudaFreeAsync(cur, st);
             cur = part;
-            n_cur = e - b;
+            n_cur = cnt;
             if (discard_top) {
                 // leaf tasks above the cut belong to shard 0
                 for (uint64_t* p : leaf_parts) cudaFreeAsync(p, st);

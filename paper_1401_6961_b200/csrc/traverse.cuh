@@ -16,6 +16,7 @@ struct TravInput {
     int shard_level;       // < 0: whole tree
     int64_t shard_begin;
     int64_t shard_end;
+    int64_t shard_stride;  // > 1: every stride-th task of [begin, end)
     int frontier_only;     // stop at frontier_level and return its expand list
     int frontier_level;
     long long* counters;   // device C_NCOUNTERS

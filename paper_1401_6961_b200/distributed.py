@@ -4,8 +4,8 @@ SURVEY.md 8(e): subtrees of the product (hextree) task space are independent
 except for accumulation into K (the reference's depth-1 thread farm,
 exchange_naive.py:220-235, and the paper's parallel argument).  Every rank
 expands the top levels identically to a cut level whose frontier holds
->= 64 tasks per rank, takes a contiguous, cost-balanced range of that
-frontier (deterministic), runs traversal + leaf screening + ERIs on it into a
+>= 64 tasks per rank, takes every world-th task of that frontier starting
+at its rank (deterministic; or a contiguous range), runs traversal + leaf screening + ERIs on it into a
 private K, and the partial K are summed with one all-reduce (NCCL over
 NVLink; gloo on CPU for the host-logic tests).  The fourfold epilogue
 (symmetrize_final) runs once on the reduced K.  Counters are summed the same
@@ -55,8 +55,23 @@ def frontier(bra, ket, P, tau_2e, mode, symmetry, level):
     return count, costs[:count]
 
 
-def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=64):
-    """Choose the cut level and this job's shard ranges (same on every rank)."""
+def split_cyclic(n: int, world: int):
+    """Rank r takes frontier tasks r, r + world, r + 2 world, ... as (begin, end, stride).
+
+    Frontier order follows the space-filling shell order, so neighbouring tasks
+    have similar cost; dealing them out cyclically balances ranks without a
+    per-task cost model (contiguous ranges of a 3D cluster's frontier differ by
+    the density of surviving work in their region)."""
+    return [(min(r, n), n, max(world, 1)) for r in range(max(world, 1))]
+
+
+def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=64, strategy="cyclic"):
+    """Choose the cut level and this job's shard selections (same on every rank).
+
+    Returns (level, [(begin, end, stride)] per rank); strategy "cyclic"
+    (split_cyclic) or "contiguous" (split_by_cost ranges, stride 1)."""
+    if strategy not in ("cyclic", "contiguous"):
+        raise ValueError(f"unknown shard strategy {strategy!r}")
     n_levels = len(bra._t.ds.levels)
     level, count, costs = 0, 1, np.ones(1)
     for L in range(n_levels - 1):
@@ -64,7 +79,9 @@ def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=64):
         level = L
         if count >= min_tasks_per_rank * world:
             break
-    return level, split_by_cost(costs, world)
+    if strategy == "cyclic":
+        return level, split_cyclic(count, world)
+    return level, [(b, e, 1) for b, e in split_by_cost(costs, world)]
 
 
 def counters_vector(c) -> np.ndarray:
@@ -121,10 +138,11 @@ def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, sha
     if shards is None:
         shards = plan(bra, ket, P, tau_2e, mode, symmetry, world)
     level, ranges = shards
-    b, e = ranges[rank]
+    b, e, stride = ranges[rank]
     Kfx = K_dev.view(torch.int64)          # the FP64 buffer reused for the accumulator
     (_, S), c, _ = run_exchange(bra, ket, P, tau_2e, mode, symmetry, True, None, K_out=Kfx,
-                                shard=(level, b, e), symmetrize=False, K_fixed=True)
+                                shard=(level, b, e, stride), symmetrize=False,
+                                K_fixed=True)
     vec = torch.from_numpy(counters_vector(c)).to(K_dev.device)
     allreduce_partials(Kfx, vec, group)
     _native.check(_native.lib().hxf_fixed_to_double(ctypes.c_void_p(Kfx.data_ptr()), Kfx.numel(), S,

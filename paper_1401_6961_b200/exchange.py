@@ -230,7 +230,8 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
     """Low-level call of hxf_exchange.
 
     K_out: None (return a new host array), or a CUDA tensor (n x n float64)
-    written in place on the device.  shard: None or (level, begin, end).
+    written in place on the device.  shard: None, (level, begin, end) or
+    (level, begin, end, stride) (every stride-th frontier task of [begin, end)).
     K_fixed: K_out (a CUDA int64 n x n tensor) receives the 64-bit fixed-point
     accumulator and the returned K is (K_out, S) with value = K_out * 2^-S
     (exact integer sums across shards; include/hxf.h).
@@ -260,7 +261,8 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
     if shard is None:
         opts.shard_level, opts.shard_begin, opts.shard_end = -1, 0, 0
     else:
-        opts.shard_level, opts.shard_begin, opts.shard_end = shard
+        opts.shard_level, opts.shard_begin, opts.shard_end = shard[:3]
+        opts.shard_stride = int(shard[3]) if len(shard) > 3 else 1
     if digest is not None:
         if not (isinstance(digest, np.ndarray) and digest.dtype == np.uint64 and digest.shape == (3,)
                 and digest.flags.c_contiguous):

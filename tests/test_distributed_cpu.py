@@ -1,7 +1,8 @@
 """Multi-rank host logic on CPU (gloo, world_size 2).
 
 The device path shards the product-tree frontier at a cut level into
-contiguous cost-balanced ranges (distributed.split_by_cost), each rank runs
+cyclic selections (distributed.split_cyclic: every world-th task from the
+rank's index) or contiguous ranges (distributed.split_by_cost), each rank runs
 its subtrees into a private K, work above the cut is counted by shard 0
 only, and K / counters are summed by one all-reduce
 (distributed.allreduce_partials).  Here the per-rank compute is the CPU
@@ -34,6 +35,15 @@ def test_split_by_cost_contiguous_balanced():
     r = distributed.split_by_cost(np.ones(100), 4)
     assert [e - b for b, e in r] == [25, 25, 25, 25]
     assert distributed.split_by_cost(np.ones(0), 3) == [(0, 0), (0, 0), (0, 0)]
+
+
+def test_split_cyclic_partitions_frontier():
+    for n in (0, 1, 5, 64, 1000):
+        for world in (1, 2, 3, 8):
+            sel = distributed.split_cyclic(n, world)
+            assert len(sel) == world
+            got = sorted(i for b, e, s in sel for i in range(b, e, s))
+            assert got == list(range(n))
 
 
 def test_counters_vector_roundtrip():
@@ -119,12 +129,15 @@ def _expand_children(run, b, p, k):
                     run.visit(bch, pch, k.child(d, bb))
 
 
-def _sharded_run(st, tau, level, world, rank):
+def _sharded_run(st, tau, level, world, rank, strategy):
     top = ho._Naive(st.shells, st.P, st.P.shape[0], tau, "schwarz", True, False)
     frontier = _frontier(st, tau, level, top)
-    ranges = distributed.split_by_cost(np.ones(len(frontier)), world)
+    if strategy == "cyclic":
+        b0, e0, s0 = distributed.split_cyclic(len(frontier), world)[rank]
+    else:
+        (b0, e0), s0 = distributed.split_by_cost(np.ones(len(frontier)), world)[rank], 1
     mine = ho._Naive(st.shells, st.P, st.P.shape[0], tau, "schwarz", True, False)
-    for b, p, k in frontier[ranges[rank][0]:ranges[rank][1]]:
+    for b, p, k in frontier[b0:e0:s0]:
         _expand_children(mine, b, p, k)
     if rank == 0:
         mine.K += top.K
@@ -138,12 +151,12 @@ def _vec(c):
                      c.tasks_expanded, c.children_spawned, c.culled_bound_ledger], dtype=np.float64)
 
 
-def _worker(rank, world, port, result_path):
+def _worker(rank, world, port, result_path, strategy):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cfg = configs.cube_cluster(4, 7, "tiny")
     st = ho.Setup(cfg.system, cfg.P, tau_ovlp=1e-11, leaf_size=4)
-    run = _sharded_run(st, 1e-8, 2, world, rank)
+    run = _sharded_run(st, 1e-8, 2, world, rank, strategy)
     K = torch.from_numpy(run.K.copy())
     vec = torch.from_numpy(_vec(run.c))
     distributed.allreduce_partials(K, vec)
@@ -159,10 +172,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_sharded_build_equals_single_process(tmp_path, world):
+@pytest.mark.parametrize("world,strategy", [(2, "cyclic"), (2, "contiguous")])
+def test_gloo_sharded_build_equals_single_process(tmp_path, world, strategy):
     path = str(tmp_path / "res.npz")
-    mp.spawn(_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), path, strategy), nprocs=world, join=True)
     res = np.load(path)
     cfg = configs.cube_cluster(4, 7, "tiny")
     st = ho.Setup(cfg.system, cfg.P, tau_ovlp=1e-11, leaf_size=4)

@@ -143,14 +143,14 @@ def test_sharded_shards_sum_to_full_build(sym):
     pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
     P_tree = hx.build_matrix_tree(cfg.P, part)
     K_full, c_full, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-9, "schwarz", sym)
-    for world in (2, 3):
+    for world, strategy in ((2, "cyclic"), (3, "cyclic"), (2, "contiguous"), (3, "contiguous")):
         level, ranges = distributed.plan(pairs, pairs, P_tree, 1e-9, "schwarz", sym, world,
-                                         min_tasks_per_rank=4)
+                                         min_tasks_per_rank=4, strategy=strategy)
         K = np.zeros_like(K_full)
         vec = 0
-        for b, e in ranges:
+        for b, e, s in ranges:
             Ks, c, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-9, "schwarz", sym,
-                                             shard=(level, b, e), symmetrize=False)
+                                             shard=(level, b, e, s), symmetrize=False)
             K += Ks
             vec = vec + distributed.counters_vector(c)
         if sym is True:
@@ -164,10 +164,10 @@ def test_sharded_shards_sum_to_full_build(sym):
         import torch
         n = K_full.shape[0]
         acc, scales = None, set()
-        for b, e in ranges:
+        for b, e, s in ranges:
             buf = torch.empty((n, n), dtype=torch.int64, device="cuda")
             (kf, S), _, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-9, "schwarz", sym,
-                                                  shard=(level, b, e), symmetrize=False,
+                                                  shard=(level, b, e, s), symmetrize=False,
                                                   K_out=buf, K_fixed=True)
             scales.add(S)
             acc = kf.clone() if acc is None else acc + kf
