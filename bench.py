@@ -243,6 +243,31 @@ def eri_flops(c):
                for k in range(16))
 
 
+def ncu_traffic(workload, mode):
+    """Per-build DRAM bytes of the path's kernels from the newest committed ncu
+    metric pass of this workload (profiles/*_ncu_<workload>_dram.json, written by
+    tools/ncu_dram.py), or None."""
+    import glob
+    here = os.path.dirname(os.path.abspath(__file__))
+    for path in sorted(glob.glob(os.path.join(here, "profiles", f"*_ncu_{workload}_dram.json")), reverse=True):
+        with open(path) as fh:
+            d = json.load(fh)
+        if d.get("mode") == mode:
+            d["file"] = os.path.relpath(path, here)
+            return d
+    return None
+
+
+def hbm_peak():
+    """Measured copy bandwidth (GB/s) from the driver-written MEASURED_PEAKS.json, else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def native_arm(args):
     import ctypes
     import numpy as np
@@ -421,6 +446,18 @@ def native_arm(args):
 
     if rank == 0:
         stage_med = [statistics.median([s[k] for s in stage]) for k in range(6)] if stage else tm
+        nt = ncu_traffic(args.config, args.mode) if world == 1 else None
+        hbm = hbm_peak()
+        # traversal: SURVEY 8(d) algorithmic bytes per visited task (naive 48 B, symmetric 104 B)
+        bpt = 48 if args.mode == "naive" else 104
+        trav_gbs = bpt * last.tasks_visited / (stage_med[0] * 1e-3) / 1e9 if stage_med[0] > 0 else None
+        roof_trav = {"bound": "hbm", "achieved": trav_gbs, "peak": hbm, "unit": "GB/s",
+                     "frac": trav_gbs / hbm if (trav_gbs and hbm) else None,
+                     "traffic": nt["k_expand"]["dram_bytes_per_build"] if nt else None,
+                     "kernel": "k_expand (count + write passes), all levels",
+                     "bytes_basis": f"algorithmic: {bpt} B per visited task (SURVEY 8(d)) x tasks_visited",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy test)",
+                     "traffic_source": nt["file"] if nt else None}
         line = {
             "metric": METRIC, "value": value, "unit": "quartets/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -439,7 +476,9 @@ def native_arm(args):
             "counters": last.to_dict() | {"ties_task": last.ties_task, "ties_leaf": last.ties_leaf},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
                          "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
-                         "traffic": None,
+                         "traffic": nt["k_eri"]["dram_bytes_per_build"] if nt else None,
+                         "traffic_source": (nt["file"] + ": dram__bytes_read.sum + dram__bytes_write.sum "
+                                            "over the k_eri launches of one build") if nt else None,
                          "kernel": "k_eri<la,lb,lc,ld> (ERI + contraction), all classes",
                          "flops_per_step_rank0": flops,
                          "peak_source": "hxf_fp64_peak DFMA microbenchmark on this GPU "
@@ -452,6 +491,7 @@ def native_arm(args):
                                   "frac": (achieved_exec / peak.value) if (achieved_exec and peak.value) else None,
                                   "flops_basis": "executed FP64 (dadd + dmul + 2 dfma) per primitive quartet "
                                                  "per class from ncu, profiles/r01_eri_fp64_executed.json"},
+            "roofline_traversal": roof_trav,
             "e2e": {"value": e2e_value, "unit": "quartets/s",
                     "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8,
                     "ms_per_step": float(et.item()) / max(args.e2e_steps, 1)},

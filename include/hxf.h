@@ -109,6 +109,11 @@ typedef struct hxf_exchange_opts {
     /* <= 1: contiguous shard range; s > 1: tasks shard_begin, shard_begin + s,
        ... below shard_end (cyclic assignment: rank r of N takes begin r, stride N) */
     int64_t shard_stride;
+    /* NULL, or host uint8[shard_end]: shard = the frontier tasks t < shard_end
+       with shard_mask[t] != 0 (any assignment, e.g. cost-balanced); the range /
+       stride fields are then ignored except that work above the cut is counted
+       only when shard_begin == 0 */
+    const uint8_t* shard_mask;
 } hxf_exchange_opts;
 
 const char* hxf_last_error(void);

@@ -70,7 +70,8 @@ class ExchangeOpts(ctypes.Structure):
                 ("digest_rem", ctypes.c_int),
                 ("K_fixed", ctypes.c_int),
                 ("K_scale", ctypes.POINTER(ctypes.c_int)),
-                ("shard_stride", ctypes.c_int64)]
+                ("shard_stride", ctypes.c_int64),
+                ("shard_mask", ctypes.POINTER(ctypes.c_uint8))]
 
 
 _lib = None

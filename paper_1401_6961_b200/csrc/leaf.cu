@@ -1148,7 +1148,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     // ---- traversal
     Timer ttrav(st);
     TravInput ti{s, bra, ket, dens, o->tau_2e, o->mode, eight ? 2 : sym, o->shard_level, o->shard_begin,
-                 o->shard_end, o->shard_stride, 0, 0, dcount, dledger};
+                 o->shard_end, o->shard_stride, o->shard_mask, 0, 0, dcount, dledger};
     TraversalResult tr = traverse(ti, st);
     g_timings[0] = ttrav.stop();
 
@@ -1961,7 +1961,7 @@ int frontier_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, double tau, 
     unsigned long long* dledger = lalloc<unsigned long long>(LEDGER_LIMBS, st);
     HXF_CUDA(cudaMemsetAsync(dcount, 0, C_NCOUNTERS * sizeof(long long), st));
     HXF_CUDA(cudaMemsetAsync(dledger, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
-    TravInput ti{s, bra, ket, dens, tau, mode, sym, -1, 0, 0, 1, 1, level, dcount, dledger};
+    TravInput ti{s, bra, ket, dens, tau, mode, sym, -1, 0, 0, 1, nullptr, 1, level, dcount, dledger};
     TraversalResult tr = traverse(ti, st);
     *n_tasks = tr.n_frontier;
     if (cost) {

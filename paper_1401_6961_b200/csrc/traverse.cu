@@ -478,14 +478,33 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     for (int L = 0; L < D && n_cur > 0; ++L) {
         if (sharded && L == in.shard_level) {
             // restrict the frontier to this shard; from here on counters are real
-            const int64_t b = std::min<int64_t>(in.shard_begin, n_cur);
-            const int64_t e = std::min<int64_t>(std::max<int64_t>(in.shard_end, b), n_cur);
-            const int64_t stride = std::max<int64_t>(in.shard_stride, 1);
-            const int64_t cnt = (e - b + stride - 1) / stride;
-            uint64_t* part = talloc<uint64_t>(std::max<int64_t>(cnt, 1), st);
-            if (cnt > 0)  // every stride-th task: a 2D copy of 8-byte rows
-                HXF_CUDA(cudaMemcpy2DAsync(part, sizeof(uint64_t), cur + b, stride * sizeof(uint64_t),
-                                           sizeof(uint64_t), cnt, cudaMemcpyDeviceToDevice, st));
+            int64_t cnt = 0;
+            uint64_t* part = nullptr;
+            if (in.shard_mask) {  // arbitrary selection: order-preserving compaction by the mask
+                const int64_t nm = std::min<int64_t>(std::max<int64_t>(in.shard_end, 0), n_cur);
+                part = talloc<uint64_t>(std::max<int64_t>(nm, 1), st);
+                if (nm > 0) {
+                    uint8_t* dm = talloc<uint8_t>(nm, st);
+                    int64_t* dn = talloc<int64_t>(1, st);
+                    HXF_CUDA(cudaMemcpyAsync(dm, in.shard_mask, nm, cudaMemcpyHostToDevice, st));
+                    size_t tb = 0;
+                    cub::DeviceSelect::Flagged(nullptr, tb, cur, dm, part, dn, nm, st);
+                    char* tmp = talloc<char>(tb, st);
+                    cub::DeviceSelect::Flagged(tmp, tb, cur, dm, part, dn, nm, st);
+                    HXF_CUDA(cudaMemcpyAsync(&cnt, dn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+                    HXF_CUDA(cudaStreamSynchronize(st));
+                    for (void* p : {(void*)dm, (void*)dn, (void*)tmp}) cudaFreeAsync(p, st);
+                }
+            } else {
+                const int64_t b = std::min<int64_t>(in.shard_begin, n_cur);
+                const int64_t e = std::min<int64_t>(std::max<int64_t>(in.shard_end, b), n_cur);
+                const int64_t stride = std::max<int64_t>(in.shard_stride, 1);
+                cnt = (e - b + stride - 1) / stride;
+                part = talloc<uint64_t>(std::max<int64_t>(cnt, 1), st);
+                if (cnt > 0)  // every stride-th task: a 2D copy of 8-byte rows
+                    HXF_CUDA(cudaMemcpy2DAsync(part, sizeof(uint64_t), cur + b, stride * sizeof(uint64_t),
+                                               sizeof(uint64_t), cnt, cudaMemcpyDeviceToDevice, st));
+            }
             cudaFreeAsync(cur, st);
             cur = part;
             n_cur = cnt;

@@ -17,6 +17,7 @@ struct TravInput {
     int64_t shard_begin;
     int64_t shard_end;
     int64_t shard_stride;  // > 1: every stride-th task of [begin, end)
+    const uint8_t* shard_mask;  // host; non-NULL: tasks t < shard_end with mask[t] != 0
     int frontier_only;     // stop at frontier_level and return its expand list
     int frontier_level;
     long long* counters;   // device C_NCOUNTERS

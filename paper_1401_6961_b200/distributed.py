@@ -4,8 +4,8 @@ SURVEY.md 8(e): subtrees of the product (hextree) task space are independent
 except for accumulation into K (the reference's depth-1 thread farm,
 exchange_naive.py:220-235, and the paper's parallel argument).  Every rank
 expands the top levels identically to a cut level whose frontier holds
->= 64 tasks per rank, takes every world-th task of that frontier starting
-at its rank (deterministic; or a contiguous range), runs traversal + leaf screening + ERIs on it into a
+>= 1024 tasks per rank, takes the tasks a fixed hash of the task index
+assigns to it (deterministic; cyclic or contiguous selections optional), runs traversal + leaf screening + ERIs on it into a
 private K, and the partial K are summed with one all-reduce (NCCL over
 NVLink; gloo on CPU for the host-logic tests).  The fourfold epilogue
 (symmetrize_final) runs once on the reduced K.  Counters are summed the same
@@ -65,13 +65,36 @@ def split_cyclic(n: int, world: int):
     return [(min(r, n), n, max(world, 1)) for r in range(max(world, 1))]
 
 
-def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=64, strategy="cyclic"):
+def _splitmix64(x):
+    z = (np.asarray(x, dtype=np.uint64) + np.uint64(0x9E3779B97F4A7C15))
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def split_hashed(n: int, world: int, seed: int = 0x1401_6961):
+    """Rank of task t = SplitMix64(t + seed) mod world, as per-rank uint8 masks.
+
+    The frontier has periodic structure (the 16 children of a parent differ
+    systematically: bra/ket children on the block diagonal carry most of the
+    surviving work), which a stride-`world` deal aliases with; a hash breaks
+    the period, and a deep cut (many tasks per rank) averages the rest."""
+    with np.errstate(over="ignore"):
+        owner = (_splitmix64(np.arange(n, dtype=np.uint64) + np.uint64(seed)) % np.uint64(max(world, 1)))
+    return [(0 if r == 0 else 1, n, (owner == r).astype(np.uint8)) for r in range(max(world, 1))]
+
+
+def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=None, strategy="hashed"):
     """Choose the cut level and this job's shard selections (same on every rank).
 
-    Returns (level, [(begin, end, stride)] per rank); strategy "cyclic"
-    (split_cyclic) or "contiguous" (split_by_cost ranges, stride 1)."""
-    if strategy not in ("cyclic", "contiguous"):
+    Returns (level, [(begin, end, stride_or_mask)] per rank) for
+    run_exchange(shard=(level,) + selection).  Strategies: "hashed"
+    (split_hashed at a cut with >= 1024 tasks per rank; default), "cyclic"
+    (split_cyclic, >= 64 per rank) or "contiguous" (split_by_cost ranges)."""
+    if strategy not in ("hashed", "cyclic", "contiguous"):
         raise ValueError(f"unknown shard strategy {strategy!r}")
+    if min_tasks_per_rank is None:
+        min_tasks_per_rank = 1024 if strategy == "hashed" else 64
     n_levels = len(bra._t.ds.levels)
     level, count, costs = 0, 1, np.ones(1)
     for L in range(n_levels - 1):
@@ -79,6 +102,8 @@ def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=64, stra
         level = L
         if count >= min_tasks_per_rank * world:
             break
+    if strategy == "hashed":
+        return level, split_hashed(count, world)
     if strategy == "cyclic":
         return level, split_cyclic(count, world)
     return level, [(b, e, 1) for b, e in split_by_cost(costs, world)]

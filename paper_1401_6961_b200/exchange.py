@@ -231,7 +231,9 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
 
     K_out: None (return a new host array), or a CUDA tensor (n x n float64)
     written in place on the device.  shard: None, (level, begin, end) or
-    (level, begin, end, stride) (every stride-th frontier task of [begin, end)).
+    (level, begin, end, stride) (every stride-th frontier task of [begin, end)) or
+    (level, begin, n, mask) (frontier tasks t with mask[t] != 0, numpy uint8[n];
+    work above the cut is counted when begin == 0).
     K_fixed: K_out (a CUDA int64 n x n tensor) receives the 64-bit fixed-point
     accumulator and the returned K is (K_out, S) with value = K_out * 2^-S
     (exact integer sums across shards; include/hxf.h).
@@ -261,8 +263,15 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
     if shard is None:
         opts.shard_level, opts.shard_begin, opts.shard_end = -1, 0, 0
     else:
-        opts.shard_level, opts.shard_begin, opts.shard_end = shard[:3]
-        opts.shard_stride = int(shard[3]) if len(shard) > 3 else 1
+        opts.shard_level, opts.shard_begin, opts.shard_end = (int(x) for x in shard[:3])
+        sel = shard[3] if len(shard) > 3 else 1
+        if isinstance(sel, np.ndarray):  # per-task selection mask over the frontier
+            mask = np.ascontiguousarray(sel, dtype=np.uint8)
+            if mask.shape != (opts.shard_end,):
+                raise InvalidArgumentError("shard mask length must equal shard end (the frontier size)")
+            opts.shard_mask = mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+        else:
+            opts.shard_stride = int(sel)
     if digest is not None:
         if not (isinstance(digest, np.ndarray) and digest.dtype == np.uint64 and digest.shape == (3,)
                 and digest.flags.c_contiguous):

@@ -46,6 +46,19 @@ def test_split_cyclic_partitions_frontier():
             assert got == list(range(n))
 
 
+def test_split_hashed_partitions_frontier():
+    for n in (0, 1, 5, 64, 5000):
+        for world in (1, 2, 3, 8):
+            sel = distributed.split_hashed(n, world)
+            assert len(sel) == world
+            assert [b == 0 for b, _, _ in sel] == [True] + [False] * (world - 1)  # top owner
+            owners = np.stack([m for _, _, m in sel]) if n else np.zeros((world, 0))
+            assert all(e == n for _, e, _ in sel)
+            assert np.array_equal(owners.sum(axis=0), np.ones(n))
+            if n >= 5000:
+                assert owners.sum(axis=1).max() <= 1.1 * n / world
+
+
 def test_counters_vector_roundtrip():
     class C:  # mimics the ctypes counters struct
         pass
@@ -132,12 +145,17 @@ def _expand_children(run, b, p, k):
 def _sharded_run(st, tau, level, world, rank, strategy):
     top = ho._Naive(st.shells, st.P, st.P.shape[0], tau, "schwarz", True, False)
     frontier = _frontier(st, tau, level, top)
-    if strategy == "cyclic":
+    if strategy == "hashed":
+        _, _, m = distributed.split_hashed(len(frontier), world)[rank]
+        picked = [t for t, keep in zip(frontier, m) if keep]
+    elif strategy == "cyclic":
         b0, e0, s0 = distributed.split_cyclic(len(frontier), world)[rank]
+        picked = frontier[b0:e0:s0]
     else:
-        (b0, e0), s0 = distributed.split_by_cost(np.ones(len(frontier)), world)[rank], 1
+        b0, e0 = distributed.split_by_cost(np.ones(len(frontier)), world)[rank]
+        picked = frontier[b0:e0]
     mine = ho._Naive(st.shells, st.P, st.P.shape[0], tau, "schwarz", True, False)
-    for b, p, k in frontier[b0:e0:s0]:
+    for b, p, k in picked:
         _expand_children(mine, b, p, k)
     if rank == 0:
         mine.K += top.K
@@ -172,7 +190,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,strategy", [(2, "cyclic"), (2, "contiguous")])
+@pytest.mark.parametrize("world,strategy", [(2, "hashed"), (2, "cyclic"), (2, "contiguous")])
 def test_gloo_sharded_build_equals_single_process(tmp_path, world, strategy):
     path = str(tmp_path / "res.npz")
     mp.spawn(_worker, args=(world, _free_port(), path, strategy), nprocs=world, join=True)

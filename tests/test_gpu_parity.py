@@ -143,7 +143,8 @@ def test_sharded_shards_sum_to_full_build(sym):
     pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
     P_tree = hx.build_matrix_tree(cfg.P, part)
     K_full, c_full, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-9, "schwarz", sym)
-    for world, strategy in ((2, "cyclic"), (3, "cyclic"), (2, "contiguous"), (3, "contiguous")):
+    for world, strategy in ((2, "hashed"), (3, "hashed"), (2, "cyclic"), (3, "cyclic"),
+                            (2, "contiguous"), (3, "contiguous")):
         level, ranges = distributed.plan(pairs, pairs, P_tree, 1e-9, "schwarz", sym, world,
                                          min_tasks_per_rank=4, strategy=strategy)
         K = np.zeros_like(K_full)

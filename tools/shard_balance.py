@@ -23,7 +23,7 @@ from paper_1401_6961_b200 import configs, distributed, exchange  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c5"
     worlds = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "2,4,8").split(",")]
-    strategies = (sys.argv[3] if len(sys.argv) > 3 else "cyclic,contiguous").split(",")
+    strategies = (sys.argv[3] if len(sys.argv) > 3 else "hashed,cyclic,contiguous").split(",")
     cfg = configs.make(name, host_density=False) if name in ("c3", "c4", "c5") else configs.make(name)
     part = hx.build_partition(cfg.system, leaf_size=cfg.leaf_size)
     part.device(0)
@@ -48,16 +48,18 @@ def main():
     for world in worlds:
         for strategy in strategies:
             Pt = hx.build_matrix_tree(P, part)
+            strat, _, mt = strategy.partition(":")
             level, sel = distributed.plan(pairs, pairs, Pt, cfg.tau_2e, "schwarz", True, world,
-                                          strategy=strategy)
+                                          strategy=strat, min_tasks_per_rank=int(mt) if mt else None)
             del Pt
             ms, qs = [], []
             for b, e, s in sel:
                 t, q = build((level, b, e, s))
+                n_front = e
                 ms.append(t)
                 qs.append(q)
             assert sum(qs) == q1, (sum(qs), q1)
-            print(json.dumps({"config": name, "world": world, "strategy": strategy, "cut_level": level,
+            print(json.dumps({"config": name, "world": world, "strategy": strategy, "cut_level": level, "frontier": n_front,
                               "shard_ms": ms, "shard_quartets": qs,
                               "max_over_mean": max(ms) / (sum(ms) / len(ms)),
                               "predicted_efficiency": t1 / (world * max(ms))}), flush=True)
