@@ -321,7 +321,11 @@ def native_arm(args):
     shards = None
     if world > 1:
         P_tree0 = hx.build_matrix_tree(P_dev, part)
-        shards = distributed.plan(pairs, pairs, P_tree0, cfg.tau_2e, "schwarz", sym, world)
+        # once per geometry + density (an SCF reuses it across iterations): hashed task
+        # groups, costs from counters-only builds (each rank measures 1/world of
+        # them), longest-first onto ranks
+        shards = distributed.plan(pairs, pairs, P_tree0, cfg.tau_2e, "schwarz", sym, world,
+                                  strategy="balanced", K_scratch=K_dev)
         del P_tree0
 
     def step(P_src):

@@ -79,22 +79,78 @@ def split_hashed(n: int, world: int, seed: int = 0x1401_6961):
     systematically: bra/ket children on the block diagonal carry most of the
     surviving work), which a stride-`world` deal aliases with; a hash breaks
     the period, and a deep cut (many tasks per rank) averages the rest."""
-    with np.errstate(over="ignore"):
-        owner = (_splitmix64(np.arange(n, dtype=np.uint64) + np.uint64(seed)) % np.uint64(max(world, 1)))
+    owner = _owner(n, world, seed)
     return [(0 if r == 0 else 1, n, (owner == r).astype(np.uint8)) for r in range(max(world, 1))]
 
 
-def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=None, strategy="hashed"):
+# Seconds per unit of counted work on one B200 (c5 fourfold stage times / counters:
+# ERI 5.0 s / 2.16e10 surviving quartets, leaf screen 2.66 s / 9.75e8 leaf tasks,
+# traversal 0.26 s / 5.64e9 visited tasks); only their ratios matter.
+COST_PER_QUARTET, COST_PER_LEAF_TASK, COST_PER_VISIT = 2.32e-10, 2.73e-9, 4.6e-11
+
+
+def group_costs(bra, ket, P, tau_2e, mode, symmetry, level, n, groups, K_scratch, group=None):
+    """Modelled cost of each hashed task group of the level-`level` frontier (n tasks).
+
+    One counters-only build (evaluate = 0: traversal + leaf screen, no ERIs) per
+    group; cost = the counted surviving quartets, leaf tasks and visits weighted by
+    their measured unit times.  Under torch.distributed every rank measures every
+    world-th group and the cost vector is all-reduced (same result on every rank).
+    K_scratch: a device float64 n_fn x n_fn tensor the counting builds may clear."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    owner = _owner(n, groups)
+    cost = np.zeros(groups)
+    for g in range(rank, groups, world):
+        mask = (owner == g).astype(np.uint8)
+        if not mask.any():
+            continue
+        _, c, _ = run_exchange(bra, ket, P, tau_2e, mode, symmetry, False, None, K_out=K_scratch,
+                               shard=(level, 1, n, mask), symmetrize=False)
+        cost[g] = (COST_PER_QUARTET * c.eri_shell_quartets + COST_PER_LEAF_TASK * c.leaf_contractions
+                   + COST_PER_VISIT * c.tasks_visited)
+    if world > 1:
+        t = torch.from_numpy(cost).to(K_scratch.device)
+        dist.all_reduce(t, group=group)
+        cost = t.cpu().numpy()
+    return cost
+
+
+def _owner(n, buckets, seed=0x1401_6961):
+    with np.errstate(over="ignore"):
+        return (_splitmix64(np.arange(n, dtype=np.uint64) + np.uint64(seed))
+                % np.uint64(max(buckets, 1))).astype(np.int64)
+
+
+def split_lpt(n, world, groups, costs):
+    """Assign hashed task groups to ranks by longest-processing-time-first (ties by
+    group index, so deterministic); returns per-rank (begin, n, mask) like split_hashed."""
+    load = np.zeros(max(world, 1))
+    rank_of = np.zeros(groups, dtype=np.int64)
+    for g in sorted(range(groups), key=lambda g: (-costs[g], g)):
+        r = int(np.argmin(load))
+        rank_of[g] = r
+        load[r] += costs[g]
+    owner = rank_of[_owner(n, groups)] if n else np.zeros(0, dtype=np.int64)
+    return [(0 if r == 0 else 1, n, (owner == r).astype(np.uint8)) for r in range(max(world, 1))]
+
+
+def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=None, strategy="hashed",
+         K_scratch=None, groups_per_rank=16, group=None):
     """Choose the cut level and this job's shard selections (same on every rank).
 
     Returns (level, [(begin, end, stride_or_mask)] per rank) for
     run_exchange(shard=(level,) + selection).  Strategies: "hashed"
-    (split_hashed at a cut with >= 1024 tasks per rank; default), "cyclic"
-    (split_cyclic, >= 64 per rank) or "contiguous" (split_by_cost ranges)."""
-    if strategy not in ("hashed", "cyclic", "contiguous"):
+    (split_hashed at a cut with >= 1024 tasks per rank; default), "balanced"
+    (hashed groups_per_rank * world task groups, costs measured by counters-only
+    builds, LPT-assigned; needs K_scratch), "cyclic" (split_cyclic, >= 64 per
+    rank) or "contiguous" (split_by_cost ranges)."""
+    if strategy not in ("hashed", "balanced", "cyclic", "contiguous"):
         raise ValueError(f"unknown shard strategy {strategy!r}")
     if min_tasks_per_rank is None:
-        min_tasks_per_rank = 1024 if strategy == "hashed" else 64
+        min_tasks_per_rank = 1024 if strategy in ("hashed", "balanced") else 64
     n_levels = len(bra._t.ds.levels)
     level, count, costs = 0, 1, np.ones(1)
     for L in range(n_levels - 1):
@@ -104,6 +160,14 @@ def plan(bra, ket, P, tau_2e, mode, symmetry, world, min_tasks_per_rank=None, st
             break
     if strategy == "hashed":
         return level, split_hashed(count, world)
+    if strategy == "balanced":
+        if world <= 1:
+            return level, split_hashed(count, world)
+        if K_scratch is None:
+            raise ValueError("the balanced plan needs K_scratch (device n_fn x n_fn float64)")
+        groups = groups_per_rank * world
+        costs = group_costs(bra, ket, P, tau_2e, mode, symmetry, level, count, groups, K_scratch, group)
+        return level, split_lpt(count, world, groups, costs)
     if strategy == "cyclic":
         return level, split_cyclic(count, world)
     return level, [(b, e, 1) for b, e in split_by_cost(costs, world)]

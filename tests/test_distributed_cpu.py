@@ -46,6 +46,27 @@ def test_split_cyclic_partitions_frontier():
             assert got == list(range(n))
 
 
+def test_split_lpt_balances_group_costs():
+    rng = np.random.default_rng(5)
+    for world, groups in ((2, 32), (4, 64), (8, 128)):
+        costs = rng.pareto(2.0, size=groups) + 0.1
+        n = 20000
+        sel = distributed.split_lpt(n, world, groups, costs)
+        owners = np.stack([m for _, _, m in sel])
+        assert np.array_equal(owners.sum(axis=0), np.ones(n))
+        assert [b == 0 for b, _, _ in sel] == [True] + [False] * (world - 1)
+        # every task of a group lands on one rank; rank loads within the LPT bound
+        grp = distributed._owner(n, groups)
+        load = np.zeros(world)
+        for g in range(groups):
+            ranks = {int(np.argmax(owners[:, t])) for t in np.nonzero(grp == g)[0]}
+            assert len(ranks) <= 1
+            if ranks:
+                load[ranks.pop()] += costs[g]
+        assert load.max() <= costs.sum() / world + costs.max() + 1e-12
+    assert distributed.split_lpt(0, 3, 8, np.ones(8))[0][2].shape == (0,)
+
+
 def test_split_hashed_partitions_frontier():
     for n in (0, 1, 5, 64, 5000):
         for world in (1, 2, 3, 8):

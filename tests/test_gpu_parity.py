@@ -143,10 +143,13 @@ def test_sharded_shards_sum_to_full_build(sym):
     pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
     P_tree = hx.build_matrix_tree(cfg.P, part)
     K_full, c_full, _ = exchange.run_exchange(pairs, pairs, P_tree, 1e-9, "schwarz", sym)
-    for world, strategy in ((2, "hashed"), (3, "hashed"), (2, "cyclic"), (3, "cyclic"),
-                            (2, "contiguous"), (3, "contiguous")):
+    import torch
+    scratch = torch.empty(K_full.shape, dtype=torch.float64, device="cuda")
+    for world, strategy in ((2, "balanced"), (3, "balanced"), (2, "hashed"), (3, "hashed"),
+                            (2, "cyclic"), (3, "cyclic"), (2, "contiguous"), (3, "contiguous")):
         level, ranges = distributed.plan(pairs, pairs, P_tree, 1e-9, "schwarz", sym, world,
-                                         min_tasks_per_rank=4, strategy=strategy)
+                                         min_tasks_per_rank=4, strategy=strategy, K_scratch=scratch,
+                                         groups_per_rank=4)
         K = np.zeros_like(K_full)
         vec = 0
         for b, e, s in ranges:

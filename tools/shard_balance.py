@@ -11,6 +11,7 @@ unsharded build's (checked).
 import json
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -23,7 +24,7 @@ from paper_1401_6961_b200 import configs, distributed, exchange  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c5"
     worlds = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "2,4,8").split(",")]
-    strategies = (sys.argv[3] if len(sys.argv) > 3 else "hashed,cyclic,contiguous").split(",")
+    strategies = (sys.argv[3] if len(sys.argv) > 3 else "balanced,hashed,cyclic,contiguous").split(",")
     cfg = configs.make(name, host_density=False) if name in ("c3", "c4", "c5") else configs.make(name)
     part = hx.build_partition(cfg.system, leaf_size=cfg.leaf_size)
     part.device(0)
@@ -48,9 +49,14 @@ def main():
     for world in worlds:
         for strategy in strategies:
             Pt = hx.build_matrix_tree(P, part)
-            strat, _, mt = strategy.partition(":")
+            strat, _, rest = strategy.partition(":")
+            mt, _, gp = rest.partition(":")
+            tp = time.perf_counter()
             level, sel = distributed.plan(pairs, pairs, Pt, cfg.tau_2e, "schwarz", True, world,
-                                          strategy=strat, min_tasks_per_rank=int(mt) if mt else None)
+                                          strategy=strat, min_tasks_per_rank=int(mt) if mt else None,
+                                          K_scratch=Kb.view(torch.float64),
+                                          groups_per_rank=int(gp) if gp else 16)
+            plan_s = time.perf_counter() - tp
             del Pt
             ms, qs = [], []
             for b, e, s in sel:
@@ -59,7 +65,7 @@ def main():
                 ms.append(t)
                 qs.append(q)
             assert sum(qs) == q1, (sum(qs), q1)
-            print(json.dumps({"config": name, "world": world, "strategy": strategy, "cut_level": level, "frontier": n_front,
+            print(json.dumps({"config": name, "world": world, "strategy": strategy, "cut_level": level, "frontier": n_front, "plan_s": plan_s,
                               "shard_ms": ms, "shard_quartets": qs,
                               "max_over_mean": max(ms) / (sum(ms) / len(ms)),
                               "predicted_efficiency": t1 / (world * max(ms))}), flush=True)
