@@ -164,6 +164,8 @@ class ClockSampler:
         self.stop_evt = threading.Event()
 
     def start(self):
+        if os.environ.get("HXF_BENCH_NO_CLOCKS"):  # diagnostic: no sampling thread
+            return
         try:
             import pynvml
             pynvml.nvmlInit()

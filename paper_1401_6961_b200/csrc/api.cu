@@ -4,7 +4,11 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
+#include <unordered_map>
 #include <vector>
 
 #include "hxf_internal.cuh"
@@ -61,7 +65,84 @@ void set_device(int dev) {
     }
 }
 
+struct ScratchCache {
+    std::mutex mu;
+    std::map<std::tuple<int, cudaStream_t, size_t>, std::vector<void*>> free_lists;
+    std::unordered_map<void*, std::pair<cudaStream_t, size_t>> live;  // ptr -> (unused, bucket)
+    std::unordered_map<void*, int> dev_of;
+};
+
+ScratchCache& scratch_cache() {
+    static ScratchCache* c = new ScratchCache();  // never destroyed (outlives CUDA teardown)
+    return *c;
+}
+
+// size buckets 2^k and 3 * 2^(k-1): at most a third of a block is slack
+size_t bucket_of(size_t b) {
+    if (b <= 256) return 256;
+    size_t p = 256;
+    while (p < b) p <<= 1;
+    return b <= p / 4 * 3 ? p / 4 * 3 : p;
+}
+
 }  // namespace
+
+void* hxf_cache_alloc(size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t bk = bucket_of(std::max<size_t>(bytes, 1));
+    ScratchCache& c = scratch_cache();
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        auto it = c.free_lists.find(std::make_tuple(dev, st, bk));
+        if (it != c.free_lists.end() && !it->second.empty()) {
+            void* p = it->second.back();
+            it->second.pop_back();
+            c.live[p] = {st, bk};
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bk, st);
+    if (e != cudaSuccess) {  // out of memory: hand every cached block of this device back, retry
+        (void)cudaGetLastError();
+        {
+            std::lock_guard<std::mutex> g(c.mu);
+            for (auto& kv : c.free_lists) {
+                if (std::get<0>(kv.first) != dev) continue;
+                for (void* q : kv.second) {
+                    cudaFreeAsync(q, std::get<1>(kv.first));
+                    c.dev_of.erase(q);
+                }
+                kv.second.clear();
+            }
+        }
+        cudaDeviceSynchronize();
+        e = cudaMallocAsync(&p, bk, st);
+        if (e != cudaSuccess)
+            throw HxfError{HXF_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e)};
+    }
+    std::lock_guard<std::mutex> g(c.mu);
+    c.live[p] = {st, bk};
+    c.dev_of[p] = dev;
+    return p;
+}
+
+void hxf_cache_free(void* p, cudaStream_t st) {
+    if (!p) return;
+    ScratchCache& c = scratch_cache();
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        auto it = c.live.find(p);
+        if (it != c.live.end()) {
+            const size_t bk = it->second.second;
+            c.live.erase(it);
+            c.free_lists[std::make_tuple(c.dev_of[p], st, bk)].push_back(p);
+            return;
+        }
+    }
+    cudaFreeAsync(p, st);
+}
 
 extern "C" {
 

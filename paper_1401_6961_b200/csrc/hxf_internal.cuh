@@ -127,6 +127,16 @@ struct hxf_pairs {
 #define NV_SC (3 * NV_MAXS)
 #define NVEC (4 * NV_MAXS)
 
+// Stream-ordered caching allocator for the builds' scratch (api.cu).  Freed blocks
+// go to a per-(device, stream, size-bucket) free list instead of back to the CUDA
+// pool: cudaMallocAsync stalled for up to ~0.7 s now and then between builds
+// (HXF_TRAV_TRACE), so steady-state builds allocate nothing.  A block freed on
+// stream s is only reused by later allocations on s (stream order = safety, as
+// with cudaFreeAsync).  hxf_cache_free of a pointer it did not allocate falls back
+// to cudaFreeAsync.
+void* hxf_cache_alloc(size_t bytes, cudaStream_t st);
+void hxf_cache_free(void* p, cudaStream_t st);
+
 struct hxf_density {
     hxf_system* sys;
     int device;

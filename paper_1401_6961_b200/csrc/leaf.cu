@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 
         if (e.n <= 0) return;
     }
     extern __shared__ __align__(16) double s_tab[];
-    boys_table_to_smem(s_tab, E::L);
+    boys_eri_table_to_smem<E::L>(s_tab);
     long long nprim = 0, nq = 0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < e.n;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -954,29 +954,27 @@ __global__ void k_symmetrize(double* K, int n) {
 
 template <typename T>
 T* lalloc(size_t n, cudaStream_t st) {
-    void* p = nullptr;
     if (n == 0) n = 1;
-    cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
-    if (e != cudaSuccess) throw HxfError{HXF_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e)};
-    return (T*)p;
+    return (T*)hxf_cache_alloc(n * sizeof(T), st);
 }
 
 // persistent grid: every block stages its Boys table once, then strides
 template <int A, int B, int C, int D>
 void launch_eri(const EriArgs& e, cudaStream_t st) {
+    constexpr int TB = boys_eri_tab_bytes(A + B + C + D);
     static int per_sm = -1, sms = 0;
     if (per_sm < 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_eri<A, B, C, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BOYS_TAB_BYTES);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri<A, B, C, D>, 128, BOYS_TAB_BYTES);
+        cudaFuncSetAttribute(k_eri<A, B, C, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri<A, B, C, D>, 128, TB);
         if (const char* cap = getenv("HXF_ERI_PERSM")) per_sm = std::min(per_sm, atoi(cap));
         per_sm = std::max(per_sm, 1);
     }
     const int64_t want = e.dbounds ? (int64_t)sms * per_sm : (e.n + 127) / 128;
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
-    k_eri<A, B, C, D><<<g, 128, BOYS_TAB_BYTES, st>>>(e);
+    k_eri<A, B, C, D><<<g, 128, TB, st>>>(e);
     note_launch();
 }
 
@@ -1090,8 +1088,8 @@ EriTables prune_tables(const hxf_pairs* pr, double other_smax, double pmax, cuda
 }
 
 void free_tables(EriTables& t, cudaStream_t st) {
-    if (t.info) cudaFreeAsync(t.info, st);
-    if (t.meta) cudaFreeAsync(t.meta, st);
+    if (t.info) hxf_cache_free(t.info, st);
+    if (t.meta) hxf_cache_free(t.meta, st);
     t = EriTables();
 }
 
@@ -1458,14 +1456,14 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         for (int b = 0; b < NB; ++b) {
             for (void* p : {(void*)sb[b].rec, (void*)sb[b].rec2, (void*)sb[b].keys, (void*)sb[b].keys2,
                             sb[b].sort_tmp, (void*)sb[b].dbounds})
-                cudaFreeAsync(p, st);
+                hxf_cache_free(p, st);
             if (b) {
-                cudaFreeAsync(bfill[b], st);
-                cudaFreeAsync(bcount[b], st);
-                cudaFreeAsync(bledger[b], st);
+                hxf_cache_free(bfill[b], st);
+                hxf_cache_free(bcount[b], st);
+                hxf_cache_free(bledger[b], st);
             }
         }
-        cudaFreeAsync(ecount, st);
+        hxf_cache_free(ecount, st);
     }
 
     // ---- epilogue
@@ -1490,7 +1488,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                 unsigned long long hm = 0;
                 HXF_CUDA(cudaMemcpyAsync(&hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, st));
                 HXF_CUDA(cudaStreamSynchronize(st));
-                cudaFreeAsync(dm, st);
+                hxf_cache_free(dm, st);
                 double asym;
                 memcpy(&asym, &hm, sizeof(asym));
                 if (asym > 1e-10) {
@@ -1505,7 +1503,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         }
         if (!o->K_on_device) {
             HXF_CUDA(cudaMemcpyAsync(K_out, Kd, n2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-            cudaFreeAsync(Kd, st);
+            hxf_cache_free(Kd, st);
         }
     }
     if (want_log) {
@@ -1515,8 +1513,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         logged = (int64_t)lf;
         const int64_t ncopy = std::min<int64_t>(logged, o->log_capacity);
         if (ncopy) HXF_CUDA(cudaMemcpyAsync(o->quartet_log, dlog, 4 * ncopy * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        cudaFreeAsync(dlog, st);
-        cudaFreeAsync(dlogfill, st);
+        hxf_cache_free(dlog, st);
+        hxf_cache_free(dlogfill, st);
     }
     if (o->log_count) *o->log_count = logged;
     if (o->digest) {
@@ -1524,13 +1522,13 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         if (want_digest) {
             HXF_CUDA(cudaMemcpyAsync(hd, ddigest, sizeof(hd), cudaMemcpyDeviceToHost, st));
             HXF_CUDA(cudaStreamSynchronize(st));
-            cudaFreeAsync(ddigest, st);
+            hxf_cache_free(ddigest, st);
         }
         for (int k = 0; k < 3; ++k) o->digest[k] = hd[k];
     }
     for (void* p : {(void*)Kfx, (void*)scount, (void*)sledger, (void*)dfill, (void*)dcount,
                     (void*)dledger, (void*)d_lslo, (void*)d_lshi, (void*)tr.leaf})
-        if (p) cudaFreeAsync(p, st);
+        if (p) hxf_cache_free(p, st);
     free_tables(etb, st);
     free_tables(etk, st);
     HXF_CUDA(cudaStreamSynchronize(st));
@@ -1743,7 +1741,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     cub::DeviceSegmentedRadixSort::SortPairsDescending(stmp, tb2, dens->pmax, skeys, iota, lp, n2, ns, roff, roff + 1, 0, 64, st);
     { k_row_nnz<<<(ns + 255) / 256, 256, 0, st>>>(skeys, ns, np); note_launch(); }
     HXF_CUDA(cudaGetLastError());
-    for (void* p : {(void*)stmp, (void*)skeys, (void*)iota, (void*)roff}) cudaFreeAsync(p, st);
+    for (void* p : {(void*)stmp, (void*)skeys, (void*)iota, (void*)roff}) hxf_cache_free(p, st);
 
     DirectArgs da;
     da.n_pairs = pairs->n_pairs;
@@ -1781,8 +1779,8 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     std::vector<int64_t> hoff(npr + 1);
     HXF_CUDA(cudaMemcpyAsync(hoff.data(), off, (npr + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaStreamSynchronize(st));
-    cudaFreeAsync(scan_tmp, st);
-    cudaFreeAsync(cnt, st);
+    hxf_cache_free(scan_tmp, st);
+    hxf_cache_free(cnt, st);
     g_timings[0] = tprep.stop();
     const int64_t total = hoff[npr];
 
@@ -1851,7 +1849,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
             p0 = p1;
         }
         for (void* p : {(void*)sb.rec, (void*)sb.rec2, (void*)sb.keys, (void*)sb.keys2, sb.sort_tmp, (void*)sb.dbounds})
-            cudaFreeAsync(p, st);
+            hxf_cache_free(p, st);
     }
     // ---- epilogue
     Timer tep(st);
@@ -1861,7 +1859,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         else HXF_CUDA(cudaMemsetAsync(Kd, 0, nfn2 * sizeof(double), st));
         if (!o->K_on_device) {
             HXF_CUDA(cudaMemcpyAsync(K_out, Kd, nfn2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-            cudaFreeAsync(Kd, st);
+            hxf_cache_free(Kd, st);
         }
     }
     long long hc[C_NCOUNTERS];
@@ -1873,7 +1871,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         for (int k = 0; k < 3; ++k) o->digest[k] = hd[k];
     for (void* p : {(void*)Kfx, (void*)scount, (void*)ddigest, (void*)fq, (void*)pidm, (void*)lq, (void*)lp,
                     (void*)nq, (void*)np, (void*)off})
-        if (p) cudaFreeAsync(p, st);
+        if (p) hxf_cache_free(p, st);
     free_tables(et, st);
     HXF_CUDA(cudaStreamSynchronize(st));
     HXF_CUDA(cudaGetLastError());
@@ -1917,7 +1915,7 @@ int symmetrize_device(double* K, int n, double tol, cudaStream_t st) {
     unsigned long long hm = 0;
     HXF_CUDA(cudaMemcpyAsync(&hm, dm, sizeof(hm), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaStreamSynchronize(st));
-    cudaFreeAsync(dm, st);
+    hxf_cache_free(dm, st);
     double asym;
     memcpy(&asym, &hm, sizeof(asym));
     if (asym > tol) {
@@ -1948,7 +1946,7 @@ double fp64_peak(cudaStream_t st) {
     cudaEventElapsedTime(&ms, a, b);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    cudaFreeAsync(out, st);
+    hxf_cache_free(out, st);
     HXF_CUDA(cudaGetLastError());
     const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
     return flops / (ms * 1e-3) / 1e12;
@@ -1969,7 +1967,7 @@ int frontier_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, double tau, 
         for (int64_t k = 0; k < n; ++k) cost[k] = 1.0;
     }
     for (void* p : {(void*)dcount, (void*)dledger, (void*)tr.leaf, (void*)tr.frontier})
-        if (p) cudaFreeAsync(p, st);
+        if (p) hxf_cache_free(p, st);
     HXF_CUDA(cudaStreamSynchronize(st));
     return HXF_OK;
 }

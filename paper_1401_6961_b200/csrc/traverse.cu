@@ -19,6 +19,17 @@
 #include "hxf_internal.cuh"
 #include "traverse.cuh"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
+namespace {
+// HXF_TRAV_TRACE=1: per-level host timestamps on stderr (diagnostic only)
+inline double trav_now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
 #define TRAV_STRIPES 1024
 
 namespace {
@@ -395,11 +406,8 @@ __global__ void k_root(TreeView tv, LevelView lv, uint64_t* out_expand, uint64_t
 
 template <typename T>
 T* talloc(size_t n, cudaStream_t st) {
-    void* p = nullptr;
     if (n == 0) n = 1;
-    cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
-    if (e != cudaSuccess) throw HxfError{HXF_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e)};
-    return (T*)p;
+    return (T*)hxf_cache_alloc(n * sizeof(T), st);
 }
 
 __global__ void k_unpack_counts(const int* packed, int64_t n, int64_t* leaf, int64_t* expand) {
@@ -412,7 +420,7 @@ __global__ void k_unpack_counts(const int* packed, int64_t n, int64_t* leaf, int
 }  // namespace
 
 // Run the traversal.  Returns the leaf-task list (device, caller frees with
-// cudaFreeAsync).  Counters / ledger are accumulated into the device arrays.
+// hxf_cache_free).  Counters / ledger are accumulated into the device arrays.
 // If shard_level >= 0 the expand frontier at that level is restricted to
 // [shard_begin, shard_end) (every shard_stride-th task) and, unless shard_begin == 0, counters and leaf
 // tasks produced above the cut are discarded (they belong to rank 0).
@@ -466,13 +474,13 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     int outcome = 0;
     HXF_CUDA(cudaMemcpyAsync(&outcome, d_outcome, sizeof(int), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaStreamSynchronize(st));
-    cudaFreeAsync(d_outcome, st);
+    hxf_cache_free(d_outcome, st);
     int64_t n_cur = outcome == O_EXPAND ? 1 : 0;
     if (outcome == O_LEAF) {
         leaf_parts.push_back(leaf0);
         leaf_counts.push_back(1);
     } else {
-        cudaFreeAsync(leaf0, st);
+        hxf_cache_free(leaf0, st);
     }
     res.frontier_sizes.push_back(n_cur);
     for (int L = 0; L < D && n_cur > 0; ++L) {
@@ -493,7 +501,7 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
                     cub::DeviceSelect::Flagged(tmp, tb, cur, dm, part, dn, nm, st);
                     HXF_CUDA(cudaMemcpyAsync(&cnt, dn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
                     HXF_CUDA(cudaStreamSynchronize(st));
-                    for (void* p : {(void*)dm, (void*)dn, (void*)tmp}) cudaFreeAsync(p, st);
+                    for (void* p : {(void*)dm, (void*)dn, (void*)tmp}) hxf_cache_free(p, st);
                 }
             } else {
                 const int64_t b = std::min<int64_t>(in.shard_begin, n_cur);
@@ -505,12 +513,12 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
                     HXF_CUDA(cudaMemcpy2DAsync(part, sizeof(uint64_t), cur + b, stride * sizeof(uint64_t),
                                                sizeof(uint64_t), cnt, cudaMemcpyDeviceToDevice, st));
             }
-            cudaFreeAsync(cur, st);
+            hxf_cache_free(cur, st);
             cur = part;
             n_cur = cnt;
             if (discard_top) {
                 // leaf tasks above the cut belong to shard 0
-                for (uint64_t* p : leaf_parts) cudaFreeAsync(p, st);
+                for (uint64_t* p : leaf_parts) hxf_cache_free(p, st);
                 leaf_parts.clear();
                 leaf_counts.clear();
             }
@@ -525,6 +533,8 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         const int base_ch = s->h_off[L + 1];
         LevelView ch{s->h_off[L + 2] - s->h_off[L + 1], s->node_off[L + 1], s->lv.leaf_id + base_ch,
                      s->lv.flo + base_ch};
+        static const bool trace = getenv("HXF_TRAV_TRACE") != nullptr;
+        const double tr0 = trace ? trav_now_ms() : 0.0;
         const int64_t nthreads = n_cur * 16;
         const int64_t nb = (nthreads + 255) / 256;
         int* blk = talloc<int>(nb, st);
@@ -562,34 +572,41 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         int64_t tot[2];
         HXF_CUDA(cudaMemcpyAsync(&tot[0], ol + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         HXF_CUDA(cudaMemcpyAsync(&tot[1], oe + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        const double tr1 = trace ? trav_now_ms() : 0.0;
         HXF_CUDA(cudaStreamSynchronize(st));
+        const double tr2 = trace ? trav_now_ms() : 0.0;
         uint64_t* nxt = talloc<uint64_t>(tot[1], st);
         uint64_t* lf = talloc<uint64_t>(tot[0], st);
+        if (trace) {
+            const double tr3 = trav_now_ms();
+            fprintf(stderr, "trav L=%d n=%lld enqueue %.2f sync %.2f alloc %.2f ms\n", L, (long long)n_cur,
+                    tr1 - tr0, tr2 - tr1, tr3 - tr2);
+        }
         a.out_expand = nxt;
         a.out_leaf = lf;
         if (in.sym) { k_expand<true, true><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         else { k_expand<false, true><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         HXF_CUDA(cudaGetLastError());
         for (void* p : {(void*)blk, (void*)cl, (void*)ce, (void*)ol, (void*)oe, tbuf, (void*)cur, (void*)outc})
-            cudaFreeAsync(p, st);
+            hxf_cache_free(p, st);
         if (tot[0]) {
             leaf_parts.push_back(lf);
             leaf_counts.push_back(tot[0]);
         } else {
-            cudaFreeAsync(lf, st);
+            hxf_cache_free(lf, st);
         }
         cur = nxt;
         n_cur = tot[1];
         res.frontier_sizes.push_back(n_cur);
     }
     fold_stripes(counters, ledger);
-    cudaFreeAsync(sc, st);
-    cudaFreeAsync(sl, st);
+    hxf_cache_free(sc, st);
+    hxf_cache_free(sl, st);
     if (in.frontier_only) {
         res.frontier = cur;
         res.n_frontier = n_cur;
     } else {
-        cudaFreeAsync(cur, st);
+        hxf_cache_free(cur, st);
     }
     // concatenate leaf parts
     int64_t tot = 0;
@@ -601,10 +618,10 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         HXF_CUDA(cudaMemcpyAsync(res.leaf + off, leaf_parts[k], leaf_counts[k] * sizeof(uint64_t),
                                  cudaMemcpyDeviceToDevice, st));
         off += leaf_counts[k];
-        cudaFreeAsync(leaf_parts[k], st);
+        hxf_cache_free(leaf_parts[k], st);
     }
-    if (scratch_c) cudaFreeAsync(scratch_c, st);
-    if (scratch_l) cudaFreeAsync(scratch_l, st);
+    if (scratch_c) hxf_cache_free(scratch_c, st);
+    if (scratch_l) hxf_cache_free(scratch_l, st);
     HXF_CUDA(cudaGetLastError());
     return res;
 }

@@ -248,3 +248,16 @@ def test_eightfold_matches_fourfold(case):
     assert np.array_equal(K8, K8.T)
     assert np.abs(K8 - K4).max() <= 1e-12
     assert c8.eri_shell_quartets < 0.6 * c4.eri_shell_quartets
+
+
+def test_ss_eri_precision_c1(golden):
+    """(ss|ss)-only config 1 against the reference's own K at tau = 1e-8: with the
+    identical culled set the difference is FP64 rounding only (the (ss|ss) kernel's
+    fine-grid F_0, boys_f0_fine, T from 0 past the asymptotic switch)."""
+    g = golden("c1")
+    _, pairs, P_tree = _device_setup(g)
+    for key, f in (("naive_1e-08", lambda: hx.build_exchange_naive(pairs, pairs, P_tree, 1e-8)),
+                   ("sym_1e-08", lambda: hx.build_exchange_symmetric(pairs, P_tree, 1e-8))):
+        K, _ = f()
+        err = np.abs(K - g[key + "_K"]).max()
+        assert err <= 5e-14, (key, err)
