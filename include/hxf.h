@@ -187,6 +187,12 @@ int hxf_fp64_peak(double* tflops, void* stream);
 /* Number of kernels libhxf has launched in this process (work evidence). */
 int hxf_launch_count(int64_t* n);
 
+/* Build scratch is cached across builds (per device, stream and size bucket) so
+ * steady-state builds allocate nothing.  This synchronises the current device
+ * and returns every cached block to the CUDA pool; *bytes (may be NULL)
+ * receives the bytes released. */
+int hxf_scratch_release(int64_t* bytes);
+
 /* Device timing of the last hxf_exchange on this thread (ms per stage):
  * [0] traversal, [1] leaf screen, [2] ERI stage (sort + ERI kernels), [3] epilogue,
  * [4] total, [5] ERI + contraction kernels only. */

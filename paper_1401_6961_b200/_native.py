@@ -24,7 +24,7 @@ EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_de
             "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
             "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_exchange_direct", "hxf_frontier",
             "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count",
-            "hxf_fixed_to_double")
+            "hxf_fixed_to_double", "hxf_scratch_release")
 
 
 class LogicError(RuntimeError):
@@ -113,6 +113,7 @@ def lib():
     L.hxf_fp64_peak.argtypes = [P(dbl), vp]
     L.hxf_launch_count.argtypes = [P(i64)]
     L.hxf_fixed_to_double.argtypes = [vp, i64, i32, vp, vp]
+    L.hxf_scratch_release.argtypes = [P(i64)]
     _lib = L
     return L
 
@@ -145,3 +146,12 @@ def current_stream():
     except Exception:  # pragma: no cover
         pass
     return ctypes.c_void_p(0)
+
+
+def release_scratch() -> int:
+    """Return the library's cached build scratch to the CUDA pool (syncs the device);
+    the bytes released.  Builds cache their scratch so steady-state builds allocate
+    nothing (include/hxf.h, hxf_scratch_release)."""
+    n = ctypes.c_int64(0)
+    check(lib().hxf_scratch_release(ctypes.byref(n)))
+    return int(n.value)

@@ -441,6 +441,29 @@ int hxf_fp64_peak(double* tflops, void* stream) {
     })
 }
 
+int hxf_scratch_release(int64_t* bytes) {
+    HXF_TRY({
+        int dev = 0;
+        cudaGetDevice(&dev);
+        HXF_CUDA(cudaDeviceSynchronize());
+        ScratchCache& c = scratch_cache();
+        int64_t total = 0;
+        {
+            std::lock_guard<std::mutex> g(c.mu);
+            for (auto& kv : c.free_lists) {
+                if (std::get<0>(kv.first) != dev) continue;
+                for (void* q : kv.second) {
+                    cudaFree(q);
+                    c.dev_of.erase(q);
+                    total += (int64_t)std::get<2>(kv.first);
+                }
+                kv.second.clear();
+            }
+        }
+        if (bytes) *bytes = total;
+    })
+}
+
 int hxf_launch_count(int64_t* n) {
     HXF_TRY({
         if (!n) throw HxfError{HXF_EINVAL, "NULL argument"};

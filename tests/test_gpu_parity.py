@@ -261,3 +261,16 @@ def test_ss_eri_precision_c1(golden):
         K, _ = f()
         err = np.abs(K - g[key + "_K"]).max()
         assert err <= 5e-14, (key, err)
+
+
+def test_scratch_release_between_builds():
+    """Cached build scratch can be handed back; the next build is unchanged."""
+    cfg = configs.cube_cluster(4, 3, "tiny")
+    part = hx.build_partition(cfg.system, leaf_size=6)
+    pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
+    P_tree = hx.build_matrix_tree(cfg.P, part)
+    K1, c1 = hx.build_exchange_symmetric(pairs, P_tree, 1e-9)
+    assert hx.release_scratch() > 0
+    assert hx.release_scratch() == 0
+    K2, c2 = hx.build_exchange_symmetric(pairs, P_tree, 1e-9)
+    assert np.array_equal(K1, K2) and c1.to_dict() == c2.to_dict()

@@ -10,6 +10,6 @@ ONE_BUILD_CLASSES=1 timeout 900 ncu --metrics $M --clock-control none -k regex:"
   --log-file gpurun_out/${tag}_fp64_c4.csv python tools/one_build.py c4 fourfold - 1 \
   > gpurun_out/${tag}_fp64_c4.log 2>&1
 echo "fp64 rc=$?" >> gpurun_out/${tag}_ncu.rc
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_eri<0, 0, 0, 0>" -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_eri<.int.0, .int.0, .int.0, .int.0>" -s 2 -c 1 \
   -o gpurun_out/${tag}_full_ssss_c4 python tools/one_build.py c4 fourfold - 1 > gpurun_out/${tag}_full.log 2>&1
 echo "full rc=$?" >> gpurun_out/${tag}_ncu.rc
