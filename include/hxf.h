@@ -184,6 +184,32 @@ int hxf_symmetrize(double* K_dev, int n, double tol, void* stream);
  * measured with a dependent-chain-free DFMA kernel over all SMs. */
 int hxf_fp64_peak(double* tflops, void* stream);
 
+/* Device Hilbert reordering of shells (replaces the host
+ * pre-pass hilbert_order / hilbert_index_3d, reference basis.py:275-331).
+ * centers: n x 3 float64 row-major (Bohr); bits = bits_per_axis in [1, 20]
+ * (HXF_EINVAL otherwise, same message as basis.py:311-312).  perm[k] = index of
+ * the shell placed k-th (numpy argsort(keys, kind="stable")); keys (may be
+ * NULL) receives the keys in sorted order.  on_device != 0: all three are
+ * device pointers and the call is stream-ordered on `stream`; 0: host pointers,
+ * copied in and out, returns after the copy back.  Bitwise the host result. */
+int hxf_hilbert_order(const double* centers, int64_t n, int bits, int on_device, int64_t* perm,
+                      uint64_t* keys, void* stream);
+
+/* Device partition build (replaces build_partition, reference
+ * quadtree.py:90-113): recursive bisection of the shells at the boundary nearest
+ * the function midpoint, ties left, until a span holds <= leaf_size functions.
+ * shell_nfunc: host int32 function count per shell.  Output (host buffers): the
+ * spans level by level as in Partition.levels (a leaf repeats at deeper levels):
+ * level k is span_lo/span_hi[level_off[k] .. level_off[k+1]).  *n_spans and
+ * *n_levels receive the sizes; if span_capacity or level_capacity (>= levels+1
+ * entries of level_off) is too small nothing is written but the two sizes and
+ * HXF_EINVAL is returned.  leaf_size below the largest shell: HXF_EINVAL with
+ * the reference's message.  Identical spans to the host rules. */
+int hxf_partition_build(const int32_t* shell_nfunc, int64_t n_shells, int leaf_size,
+                        int32_t* span_lo, int32_t* span_hi, int64_t span_capacity,
+                        int64_t* level_off, int level_capacity, int64_t* n_spans, int* n_levels,
+                        void* stream);
+
 /* Number of kernels libhxf has launched in this process (work evidence). */
 int hxf_launch_count(int64_t* n);
 

@@ -8,6 +8,7 @@ build_exchange_symmetric) backed by libhxf.so (hand-written sm_100a CUDA).
 from .basis import (Atom, BasisSystem, DensityModel, GaussianShell, InvalidArgumentError,
                     SplitMix64, build_density, generate_cluster, hilbert_order)
 from ._native import LogicError, release_scratch
+from .prep import hilbert_order_device
 from .exchange import (CASE_LABELS, SymmetryCase, SymmetryCounters, TraversalCounters,
                        build_exchange_eightfold, build_exchange_naive, build_exchange_symmetric,
                        classify_quartet,

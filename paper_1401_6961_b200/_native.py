@@ -24,7 +24,8 @@ EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_de
             "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
             "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_exchange_direct", "hxf_frontier",
             "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count",
-            "hxf_fixed_to_double", "hxf_scratch_release")
+            "hxf_fixed_to_double", "hxf_scratch_release", "hxf_hilbert_order",
+            "hxf_partition_build")
 
 
 class LogicError(RuntimeError):
@@ -114,6 +115,8 @@ def lib():
     L.hxf_launch_count.argtypes = [P(i64)]
     L.hxf_fixed_to_double.argtypes = [vp, i64, i32, vp, vp]
     L.hxf_scratch_release.argtypes = [P(i64)]
+    L.hxf_hilbert_order.argtypes = [vp, i64, i32, i32, vp, vp, vp]
+    L.hxf_partition_build.argtypes = [vp, i64, i32, vp, vp, i64, vp, i32, P(i64), P(i32), vp]
     _lib = L
     return L
 

@@ -22,6 +22,11 @@ void note_launch(int n) { g_launches += n; }
 
 int hxf_last_timings_impl(double* ms, int n);
 int fixed_to_double_impl(const int64_t* Kfx, int64_t n2, int S, double* K, cudaStream_t st);
+void partition_build_device(const int32_t* sizes, int n, int leaf, std::vector<int64_t>& level_off,
+                            std::vector<int32_t>& span_lo, std::vector<int32_t>& span_hi,
+                            cudaStream_t st);
+void hilbert_order_device(const double* centers, int64_t n, int bits, int64_t* perm,
+                          uint64_t* keys_out, cudaStream_t st);
 
 #define HXF_TRY(...)                                         \
     try {                                                    \
@@ -438,6 +443,76 @@ int hxf_fp64_peak(double* tflops, void* stream) {
         if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
             throw HxfError{HXF_ECUDA, "no CUDA device available (libhxf has no CPU fallback)"};
         *tflops = fp64_peak((cudaStream_t)stream);
+    })
+}
+
+int hxf_hilbert_order(const double* centers, int64_t n, int bits, int on_device, int64_t* perm,
+                      uint64_t* keys, void* stream) {
+    HXF_TRY({
+        if (bits < 1 || bits > 20) throw HxfError{HXF_EINVAL, "bits_per_axis must be in [1, 20]"};
+        if (n < 0 || n > INT32_MAX) throw HxfError{HXF_EINVAL, "bad shell count"};
+        if (n > 0 && (!centers || !perm)) throw HxfError{HXF_EINVAL, "NULL argument"};
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw HxfError{HXF_ECUDA, "no CUDA device available (libhxf has no CPU fallback)"};
+        cudaStream_t st = (cudaStream_t)stream;
+        if (on_device) {
+            hilbert_order_device(centers, n, bits, perm, keys, st);
+        } else if (n > 0) {
+            double* dc = (double*)hxf_cache_alloc(n * 3 * sizeof(double), st);
+            int64_t* dp = (int64_t*)hxf_cache_alloc(n * sizeof(int64_t), st);
+            uint64_t* dk = keys ? (uint64_t*)hxf_cache_alloc(n * sizeof(uint64_t), st) : nullptr;
+            HXF_CUDA(cudaMemcpyAsync(dc, centers, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+            hilbert_order_device(dc, n, bits, dp, dk, st);
+            HXF_CUDA(cudaMemcpyAsync(perm, dp, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            if (keys)
+                HXF_CUDA(cudaMemcpyAsync(keys, dk, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+            HXF_CUDA(cudaStreamSynchronize(st));
+            if (dk) hxf_cache_free(dk, st);
+            hxf_cache_free(dp, st);
+            hxf_cache_free(dc, st);
+        }
+    })
+}
+
+int hxf_partition_build(const int32_t* shell_nfunc, int64_t n_shells, int leaf_size,
+                        int32_t* span_lo, int32_t* span_hi, int64_t span_capacity,
+                        int64_t* level_off, int level_capacity, int64_t* n_spans, int* n_levels,
+                        void* stream) {
+    HXF_TRY({
+        if (n_shells < 0 || n_shells >= INT32_MAX) throw HxfError{HXF_EINVAL, "bad shell count"};
+        if ((n_shells > 0 && !shell_nfunc) || !span_lo || !span_hi || !level_off || !n_spans ||
+            !n_levels)
+            throw HxfError{HXF_EINVAL, "NULL argument"};
+        int32_t big = 1;
+        for (int64_t i = 0; i < n_shells; ++i) {
+            if (shell_nfunc[i] < 1) throw HxfError{HXF_EINVAL, "shell with no functions"};
+            big = std::max(big, shell_nfunc[i]);
+        }
+        if (leaf_size < big) throw HxfError{HXF_EINVAL, "leaf_size must be >= the largest shell"};
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw HxfError{HXF_ECUDA, "no CUDA device available (libhxf has no CPU fallback)"};
+        cudaStream_t st = (cudaStream_t)stream;
+        std::vector<int64_t> off;
+        std::vector<int32_t> lo, hi;
+        if (n_shells == 0) {
+            off = {0, 1};
+            lo = {0};
+            hi = {0};
+        } else {
+            int32_t* ds = (int32_t*)hxf_cache_alloc(n_shells * sizeof(int32_t), st);
+            HXF_CUDA(cudaMemcpyAsync(ds, shell_nfunc, n_shells * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+            partition_build_device(ds, (int)n_shells, leaf_size, off, lo, hi, st);
+            hxf_cache_free(ds, st);
+        }
+        *n_spans = (int64_t)lo.size();
+        *n_levels = (int)off.size() - 1;
+        if ((int64_t)lo.size() > span_capacity || (int64_t)off.size() > level_capacity)
+            throw HxfError{HXF_EINVAL, "output capacity too small (sizes returned in n_spans, n_levels)"};
+        memcpy(span_lo, lo.data(), lo.size() * sizeof(int32_t));
+        memcpy(span_hi, hi.data(), hi.size() * sizeof(int32_t));
+        memcpy(level_off, off.data(), off.size() * sizeof(int64_t));
     })
 }
 
