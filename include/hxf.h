@@ -210,6 +210,22 @@ int hxf_partition_build(const int32_t* shell_nfunc, int64_t n_shells, int leaf_s
                         int64_t* level_off, int level_capacity, int64_t* n_spans, int* n_levels,
                         void* stream);
 
+/* Block-sparse reduction of shard K accumulators (the
+ * multi-GPU all-reduce of exchange_sharded, csrc/reduce.cu).  All arrays are
+ * device arrays; K is the n x n int64 fixed-point accumulator, tiles are bs x bs
+ * (nb = ceil(n / bs), nb * nb tiles, row-major, edge tiles zero-padded).
+ * hxf_block_mask: mask[t] = 1 if tile t holds a nonzero.
+ * hxf_block_slots: slot[0..nt] = exclusive prefix sum of mask (nt + 1 entries);
+ *   *n_blocks (host) = number of flagged tiles (synchronises the stream).
+ * hxf_block_pack / hxf_block_unpack: copy flagged tiles K <-> buf (n_blocks * bs^2
+ *   int64); unpack writes only flagged tiles. */
+int hxf_block_mask(const int64_t* K, int n, int bs, uint8_t* mask, void* stream);
+int hxf_block_slots(const uint8_t* mask, int64_t n_tiles, int64_t* slot, int64_t* n_blocks, void* stream);
+int hxf_block_pack(const int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, int64_t* buf,
+                   void* stream);
+int hxf_block_unpack(int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, const int64_t* buf,
+                     void* stream);
+
 /* Number of kernels libhxf has launched in this process (work evidence). */
 int hxf_launch_count(int64_t* n);
 

@@ -25,7 +25,8 @@ EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_de
             "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_exchange_direct", "hxf_frontier",
             "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count",
             "hxf_fixed_to_double", "hxf_scratch_release", "hxf_hilbert_order",
-            "hxf_partition_build")
+            "hxf_partition_build", "hxf_block_mask", "hxf_block_slots", "hxf_block_pack",
+            "hxf_block_unpack")
 
 
 class LogicError(RuntimeError):
@@ -116,6 +117,10 @@ def lib():
     L.hxf_fixed_to_double.argtypes = [vp, i64, i32, vp, vp]
     L.hxf_scratch_release.argtypes = [P(i64)]
     L.hxf_hilbert_order.argtypes = [vp, i64, i32, i32, vp, vp, vp]
+    L.hxf_block_mask.argtypes = [vp, i32, i32, vp, vp]
+    L.hxf_block_slots.argtypes = [vp, i64, vp, P(i64), vp]
+    L.hxf_block_pack.argtypes = [vp, i32, i32, vp, vp, vp, vp]
+    L.hxf_block_unpack.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     L.hxf_partition_build.argtypes = [vp, i64, i32, vp, vp, i64, vp, i32, P(i64), P(i32), vp]
     _lib = L
     return L

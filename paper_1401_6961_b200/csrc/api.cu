@@ -22,6 +22,10 @@ void note_launch(int n) { g_launches += n; }
 
 int hxf_last_timings_impl(double* ms, int n);
 int fixed_to_double_impl(const int64_t* Kfx, int64_t n2, int S, double* K, cudaStream_t st);
+void block_mask_device(const int64_t* K, int n, int bs, uint8_t* mask, cudaStream_t st);
+int64_t block_slots_device(const uint8_t* mask, int64_t nt, int64_t* slot, cudaStream_t st);
+void block_move_device(int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, int64_t* buf,
+                       bool pack, cudaStream_t st);
 void partition_build_device(const int32_t* sizes, int n, int leaf, std::vector<int64_t>& level_off,
                             std::vector<int32_t>& span_lo, std::vector<int32_t>& span_hi,
                             cudaStream_t st);
@@ -513,6 +517,50 @@ int hxf_partition_build(const int32_t* shell_nfunc, int64_t n_shells, int leaf_s
         memcpy(span_lo, lo.data(), lo.size() * sizeof(int32_t));
         memcpy(span_hi, hi.data(), hi.size() * sizeof(int32_t));
         memcpy(level_off, off.data(), off.size() * sizeof(int64_t));
+    })
+}
+
+static void need_device() {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw HxfError{HXF_ECUDA, "no CUDA device available (libhxf has no CPU fallback)"};
+}
+
+int hxf_block_mask(const int64_t* K, int n, int bs, uint8_t* mask, void* stream) {
+    HXF_TRY({
+        if (n < 0 || bs < 1 || bs > 1024) throw HxfError{HXF_EINVAL, "bad size"};
+        if (n > 0 && (!K || !mask)) throw HxfError{HXF_EINVAL, "NULL argument"};
+        need_device();
+        block_mask_device(K, n, bs, mask, (cudaStream_t)stream);
+    })
+}
+
+int hxf_block_slots(const uint8_t* mask, int64_t n_tiles, int64_t* slot, int64_t* n_blocks, void* stream) {
+    HXF_TRY({
+        if (n_tiles < 0 || !n_blocks) throw HxfError{HXF_EINVAL, "bad arguments"};
+        if (n_tiles > 0 && (!mask || !slot)) throw HxfError{HXF_EINVAL, "NULL argument"};
+        need_device();
+        *n_blocks = block_slots_device(mask, n_tiles, slot, (cudaStream_t)stream);
+    })
+}
+
+int hxf_block_pack(const int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, int64_t* buf,
+                   void* stream) {
+    HXF_TRY({
+        if (n < 0 || bs < 1 || bs > 1024) throw HxfError{HXF_EINVAL, "bad size"};
+        if (n > 0 && (!K || !mask || !slot || !buf)) throw HxfError{HXF_EINVAL, "NULL argument"};
+        need_device();
+        block_move_device(const_cast<int64_t*>(K), n, bs, mask, slot, buf, true, (cudaStream_t)stream);
+    })
+}
+
+int hxf_block_unpack(int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, const int64_t* buf,
+                     void* stream) {
+    HXF_TRY({
+        if (n < 0 || bs < 1 || bs > 1024) throw HxfError{HXF_EINVAL, "bad size"};
+        if (n > 0 && (!K || !mask || !slot || !buf)) throw HxfError{HXF_EINVAL, "NULL argument"};
+        need_device();
+        block_move_device(K, n, bs, mask, slot, const_cast<int64_t*>(buf), false, (cudaStream_t)stream);
     })
 }
 

@@ -730,14 +730,24 @@ __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double
     k_fixed_add(e.K + ((int64_t)row * e.nfn + col), v, e.S);
 }
 
-template <int LA, int LB, int LC, int LD>
 #ifndef HXF_ERI_MINB0
 #define HXF_ERI_MINB0 3
 #endif
 #ifndef HXF_ERI_MINB1
 #define HXF_ERI_MINB1 2
 #endif
-__global__ void __launch_bounds__(128, (LA + LB + LC + LD) == 0 ? HXF_ERI_MINB0 : HXF_ERI_MINB1) k_eri(EriArgs e) {
+// classes whose bit (LA<<3 | LB<<2 | LC<<1 | LD) is set in HXF_ERI_MINB3_MASK are
+// compiled for 3 resident blocks per SM (<= 168 registers) instead of HXF_ERI_MINB1
+#ifndef HXF_ERI_MINB3_MASK
+#define HXF_ERI_MINB3_MASK 0
+#endif
+__host__ __device__ constexpr int eri_min_blocks(int la, int lb, int lc, int ld) {
+    return (la + lb + lc + ld) == 0 ? HXF_ERI_MINB0
+           : ((HXF_ERI_MINB3_MASK >> ((la << 3) | (lb << 2) | (lc << 1) | ld)) & 1) ? 3
+                                                                                   : HXF_ERI_MINB1;
+}
+template <int LA, int LB, int LC, int LD>
+__global__ void __launch_bounds__(128, eri_min_blocks(LA, LB, LC, LD)) k_eri(EriArgs e) {
     typedef Eri<LA, LB, LC, LD> E;
     constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL;
     constexpr int CLS = (LA << 3) | (LB << 2) | (LC << 1) | LD;

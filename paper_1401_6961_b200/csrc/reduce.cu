@@ -1,0 +1,102 @@
+// Block-sparse K for the multi-GPU reduction (first part).
+//
+// A shard's K is its n x n int64 fixed-point accumulator (hxf_exchange_opts.K_fixed).
+// Exchange K is block sparse at c5 scale (|K_ij| decays with the distance of i and j),
+// so instead of all-reducing n^2 int64 the ranks
+//   1. flag the bs x bs tiles holding any nonzero (hxf_block_mask),
+//   2. OR the flags over the job (a small uint8 all-reduce, max),
+//   3. number the flagged tiles (hxf_block_slots: exclusive scan, count to host),
+//   4. pack those tiles into a dense buffer (hxf_block_pack), all-reduce it (int64
+//      sum: exact), and unpack (hxf_block_unpack).
+// A tile flagged by no rank is zero on every rank, so it needs no traffic and the
+// unpacked K is bitwise the dense all-reduce.  Tiles are row-major, edge tiles
+// zero-padded.  Mask / pack / unpack are HBM-bound streaming passes: one CTA per
+// tile row strip, 64-bit loads coalesced along K rows.
+
+#include <cub/cub.cuh>
+
+#include "hxf_internal.cuh"
+
+namespace {
+
+// one block per tile: any nonzero in rows [ti*bs, ..) x cols [tj*bs, ..)
+__global__ void k_block_mask(const int64_t* __restrict__ K, int n, int bs, int nb,
+                             uint8_t* __restrict__ mask) {
+    const int64_t t = blockIdx.x;
+    const int ti = (int)(t / nb), tj = (int)(t % nb);
+    const int r0 = ti * bs, c0 = tj * bs;
+    const int rn = min(bs, n - r0), cn = min(bs, n - c0);
+    int any = 0;
+    for (int e = threadIdx.x; e < rn * cn; e += blockDim.x) {
+        const int r = e / cn, c = e % cn;
+        any |= K[(int64_t)(r0 + r) * n + c0 + c] != 0;
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) mask[t] = (uint8_t)any;
+}
+
+__global__ void k_mask_to_int(const uint8_t* __restrict__ m, int64_t nt, int64_t* __restrict__ v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = m[i] ? 1 : 0;
+}
+
+template <bool PACK>
+__global__ void k_block_move(int64_t* __restrict__ K, int n, int bs, int nb, const uint8_t* __restrict__ mask,
+                             const int64_t* __restrict__ slot, int64_t* __restrict__ buf) {
+    const int64_t t = blockIdx.x;
+    if (!mask[t]) return;
+    const int ti = (int)(t / nb), tj = (int)(t % nb);
+    const int r0 = ti * bs, c0 = tj * bs;
+    int64_t* b = buf + slot[t] * (int64_t)bs * bs;
+    for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) {
+        const int r = e / bs, c = e % bs;
+        const bool in = r0 + r < n && c0 + c < n;
+        if (PACK) {
+            b[e] = in ? K[(int64_t)(r0 + r) * n + c0 + c] : 0;
+        } else if (in) {
+            K[(int64_t)(r0 + r) * n + c0 + c] = b[e];
+        }
+    }
+}
+
+}  // namespace
+
+void block_mask_device(const int64_t* K, int n, int bs, uint8_t* mask, cudaStream_t st) {
+    const int nb = (n + bs - 1) / bs;
+    const int64_t nt = (int64_t)nb * nb;
+    if (nt == 0) return;
+    { k_block_mask<<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, mask); note_launch(); }
+    HXF_CUDA(cudaGetLastError());
+}
+
+int64_t block_slots_device(const uint8_t* mask, int64_t nt, int64_t* slot, cudaStream_t st) {
+    if (nt == 0) return 0;
+    int64_t* v = (int64_t*)hxf_cache_alloc((nt + 1) * sizeof(int64_t), st);
+    HXF_CUDA(cudaMemsetAsync(v + nt, 0, sizeof(int64_t), st));
+    { k_mask_to_int<<<(unsigned)std::min<int64_t>((nt + 255) / 256, 148 * 8), 256, 0, st>>>(mask, nt, v); note_launch(); }
+    size_t tb = 0;
+    HXF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, v, slot, nt + 1, st));
+    void* tmp = hxf_cache_alloc(tb ? tb : 1, st);
+    HXF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, v, slot, nt + 1, st));  // slot[nt] = count
+    note_launch();
+    int64_t count = 0;
+    HXF_CUDA(cudaMemcpyAsync(&count, slot + nt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HXF_CUDA(cudaStreamSynchronize(st));
+    hxf_cache_free(tmp, st);
+    hxf_cache_free(v, st);
+    return count;
+}
+
+void block_move_device(int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, int64_t* buf,
+                       bool pack, cudaStream_t st) {
+    const int nb = (n + bs - 1) / bs;
+    const int64_t nt = (int64_t)nb * nb;
+    if (nt == 0) return;
+    if (pack) {
+        k_block_move<true><<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, mask, slot, buf);
+    } else {
+        k_block_move<false><<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, mask, slot, buf);
+    }
+    note_launch();
+    HXF_CUDA(cudaGetLastError());
+}

@@ -211,13 +211,79 @@ def allreduce_partials(K, counters_vec, group=None):
     return K, counters_vec
 
 
-def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, shards=None):
+class _NativeBlockOps:
+    """Block-sparse tile ops of libhxf (csrc/reduce.cu) on CUDA int64 tensors."""
+
+    @staticmethod
+    def mask(K, bs):
+        import torch
+        n = K.shape[0]
+        nb = (n + bs - 1) // bs
+        m = torch.empty(nb * nb, dtype=torch.uint8, device=K.device)
+        _native.check(_native.lib().hxf_block_mask(ctypes.c_void_p(K.data_ptr()), n, bs,
+                                                   ctypes.c_void_p(m.data_ptr()), _native.current_stream()))
+        return m
+
+    @staticmethod
+    def slots(m):
+        import torch
+        slot = torch.empty(m.numel() + 1, dtype=torch.int64, device=m.device)
+        cnt = ctypes.c_int64(0)
+        _native.check(_native.lib().hxf_block_slots(ctypes.c_void_p(m.data_ptr()), m.numel(),
+                                                    ctypes.c_void_p(slot.data_ptr()), ctypes.byref(cnt),
+                                                    _native.current_stream()))
+        return slot, int(cnt.value)
+
+    @staticmethod
+    def pack(K, bs, m, slot, nblk):
+        import torch
+        buf = torch.empty(max(1, nblk) * bs * bs, dtype=torch.int64, device=K.device)
+        _native.check(_native.lib().hxf_block_pack(ctypes.c_void_p(K.data_ptr()), K.shape[0], bs,
+                                                   ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(slot.data_ptr()),
+                                                   ctypes.c_void_p(buf.data_ptr()), _native.current_stream()))
+        return buf
+
+    @staticmethod
+    def unpack(K, bs, m, slot, buf):
+        _native.check(_native.lib().hxf_block_unpack(ctypes.c_void_p(K.data_ptr()), K.shape[0], bs,
+                                                     ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(slot.data_ptr()),
+                                                     ctypes.c_void_p(buf.data_ptr()), _native.current_stream()))
+
+
+def allreduce_fixed_sparse(Kfx, counters_vec, group=None, block=64, ops=None):
+    """Block-sparse exact all-reduce of int64 fixed-point shard accumulators
+    (SURVEY §8(f) f4): OR of the per-rank nonzero-tile masks (uint8 max), then an
+    int64 sum of only the union's tiles.  A tile no rank flags is zero everywhere,
+    so the result is bitwise the dense all-reduce.  Returns (Kfx, counters_vec,
+    stats) with the tile count and the bytes each rank contributed."""
+    import torch.distributed as dist
+    ops = ops or _NativeBlockOps
+    m = ops.mask(Kfx, block)
+    multi = dist.is_initialized() and dist.get_world_size(group) > 1
+    if multi:
+        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(counters_vec, group=group)
+    slot, nblk = ops.slots(m)
+    if multi and nblk:
+        buf = ops.pack(Kfx, block, m, slot, nblk)
+        dist.all_reduce(buf, group=group)
+        ops.unpack(Kfx, block, m, slot, buf)
+    n = Kfx.shape[0]
+    stats = {"block": block, "tiles": int(m.numel()), "tiles_nonzero": nblk,
+             "bytes_sparse": nblk * block * block * 8 + int(m.numel()), "bytes_dense": n * n * 8}
+    return Kfx, counters_vec, stats
+
+
+def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, shards=None,
+                     sparse_block=None):
     """One rank's share of a sharded build + the all-reduce of K and counters.
 
     K_dev: torch CUDA tensor (n x n float64), overwritten with the full K on
     every rank.  Each shard's K is its 64-bit fixed-point accumulator (same
     scale on every rank); the int64 all-reduce is an exact integer sum, so the
-    reduced K is bitwise the single-device K.  Returns (counters, shard plan).
+    reduced K is bitwise the single-device K.  sparse_block=bs all-reduces only
+    the bs x bs tiles some rank holds a nonzero in (allreduce_fixed_sparse; same
+    K bit for bit).  Returns (counters, shard plan).
     """
     import torch
     import torch.distributed as dist
@@ -233,7 +299,10 @@ def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, sha
                                 shard=(level, b, e, stride), symmetrize=False,
                                 K_fixed=True)
     vec = torch.from_numpy(counters_vector(c)).to(K_dev.device)
-    allreduce_partials(Kfx, vec, group)
+    if sparse_block:
+        allreduce_fixed_sparse(Kfx, vec, group, block=int(sparse_block))
+    else:
+        allreduce_partials(Kfx, vec, group)
     _native.check(_native.lib().hxf_fixed_to_double(ctypes.c_void_p(Kfx.data_ptr()), Kfx.numel(), S,
                                                     ctypes.c_void_p(K_dev.data_ptr()),
                                                     _native.current_stream()))

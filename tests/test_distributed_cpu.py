@@ -223,3 +223,79 @@ def test_gloo_sharded_build_equals_single_process(tmp_path, world, strategy):
     ref = _vec(c)
     assert np.array_equal(res["vec"][:8], ref[:8])        # integer counters exact
     assert res["vec"][8] == pytest.approx(ref[8], rel=1e-12)
+
+
+# ------------------------------------------------ block-sparse reduction (§8(f) f4)
+
+class _TorchBlockOps:
+    """CPU stand-in for the libhxf tile kernels (test checker only): the host
+    logic of distributed.allreduce_fixed_sparse runs over gloo with these."""
+
+    @staticmethod
+    def _tiles(K, bs):
+        n = K.shape[0]
+        nb = (n + bs - 1) // bs
+        pad = torch.zeros(nb * bs, nb * bs, dtype=K.dtype)
+        pad[:n, :n] = K
+        return pad.view(nb, bs, nb, bs).permute(0, 2, 1, 3).reshape(nb * nb, bs * bs)
+
+    @classmethod
+    def mask(cls, K, bs):
+        return (cls._tiles(K, bs) != 0).any(dim=1).to(torch.uint8)
+
+    @staticmethod
+    def slots(m):
+        slot = torch.zeros(m.numel() + 1, dtype=torch.int64)
+        slot[1:] = torch.cumsum(m.to(torch.int64), 0)
+        return slot, int(slot[-1])
+
+    @classmethod
+    def pack(cls, K, bs, m, slot, nblk):
+        return cls._tiles(K, bs)[m.bool()].reshape(-1).clone()
+
+    @classmethod
+    def unpack(cls, K, bs, m, slot, buf):
+        n = K.shape[0]
+        nb = (n + bs - 1) // bs
+        t = cls._tiles(K, bs)
+        t[m.bool()] = buf.view(-1, bs * bs)
+        full = t.view(nb, nb, bs, bs).permute(0, 2, 1, 3).reshape(nb * bs, nb * bs)
+        K.copy_(full[:n, :n])
+
+
+def _sparse_worker(rank, world, port, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    K = _rank_partial(rank)
+    vec = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    K, vec, stats = distributed.allreduce_fixed_sparse(K, vec, block=8, ops=_TorchBlockOps)
+    if rank == 0:
+        np.savez(result_path, K=K.numpy(), vec=vec.numpy(), nz=stats["tiles_nonzero"], tiles=stats["tiles"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _rank_partial(rank, n=45):
+    """Banded int64 partial with rank-specific tiles (some tiles nonzero on one rank only,
+    entries cancelling to zero across ranks in one tile)."""
+    g = torch.Generator().manual_seed(100 + rank)
+    K = torch.randint(-2**40, 2**40, (n, n), generator=g, dtype=torch.int64)
+    i = torch.arange(n)
+    K[(i[:, None] - i[None, :]).abs() > 10] = 0
+    if rank == 0:
+        K[40:45, 0:3] = 7
+        K[16:24, 24:32] = 5
+    else:
+        K[0:3, 40:45] = -3
+        K[16:24, 24:32] = -5
+    return K
+
+
+def test_gloo_block_sparse_allreduce_equals_dense(tmp_path):
+    path = str(tmp_path / "sparse.npz")
+    mp.spawn(_sparse_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    res = np.load(path)
+    dense = (_rank_partial(0) + _rank_partial(1)).numpy()
+    assert np.array_equal(res["K"], dense)
+    assert res["vec"][0] == 3.0
+    assert 0 < int(res["nz"]) < int(res["tiles"])        # the band leaves tiles out
