@@ -11,7 +11,8 @@
 // A tile flagged by no rank is zero on every rank, so it needs no traffic and the
 // unpacked K is bitwise the dense all-reduce.  Tiles are row-major, edge tiles
 // zero-padded.  Mask / pack / unpack are HBM-bound streaming passes: one CTA per
-// tile row strip, 64-bit loads coalesced along K rows.
+// tile, 64-bit loads coalesced along K rows; the mask pass stops reading a tile
+// at its first nonzero chunk.
 
 #include <cub/cub.cuh>
 
@@ -26,12 +27,25 @@ __global__ void k_block_mask(const int64_t* __restrict__ K, int n, int bs, int n
     const int ti = (int)(t / nb), tj = (int)(t % nb);
     const int r0 = ti * bs, c0 = tj * bs;
     const int rn = min(bs, n - r0), cn = min(bs, n - c0);
+    // chunks of 4 loads per thread, the block leaves at the first chunk holding a
+    // nonzero: a nonzero tile (55 % at c5) is usually decided by its first chunk,
+    // so only the zero tiles are read in full
+    const int total = rn * cn;
     int any = 0;
-    for (int e = threadIdx.x; e < rn * cn; e += blockDim.x) {
-        const int r = e / cn, c = e % cn;
-        any |= K[(int64_t)(r0 + r) * n + c0 + c] != 0;
+    for (int base = 0; base < total; base += 4 * blockDim.x) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = base + u * blockDim.x + threadIdx.x;
+            if (e < total) {
+                const int r = e / cn, c = e - r * cn;
+                any |= __ldcs(K + (int64_t)(r0 + r) * n + c0 + c) != 0;
+            }
+        }
+        if (__syncthreads_or(any)) {
+            any = 1;
+            break;
+        }
     }
-    any = __syncthreads_or(any);
     if (threadIdx.x == 0) mask[t] = (uint8_t)any;
 }
 
