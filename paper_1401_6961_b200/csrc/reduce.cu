@@ -62,6 +62,20 @@ __global__ void k_block_move(int64_t* __restrict__ K, int n, int bs, int nb, con
     const int ti = (int)(t / nb), tj = (int)(t % nb);
     const int r0 = ti * bs, c0 = tj * bs;
     int64_t* b = buf + slot[t] * (int64_t)bs * bs;
+    if (((n | bs) & 1) == 0) {  // even n and bs: 16-byte aligned pairs along a row
+        longlong2* b2 = reinterpret_cast<longlong2*>(b);
+        for (int e = threadIdx.x; e < bs * bs / 2; e += blockDim.x) {
+            const int r = (2 * e) / bs, c = 2 * e - r * bs;
+            const bool in = r0 + r < n && c0 + c < n;  // c even, n even: c + 1 < n too
+            longlong2* k2 = reinterpret_cast<longlong2*>(K + (int64_t)(r0 + r) * n + c0 + c);
+            if (PACK) {
+                b2[e] = in ? __ldcs(k2) : make_longlong2(0, 0);
+            } else if (in) {
+                __stcs(k2, b2[e]);
+            }
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) {
         const int r = e / bs, c = e % bs;
         const bool in = r0 + r < n && c0 + c < n;
