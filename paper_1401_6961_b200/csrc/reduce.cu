@@ -32,6 +32,27 @@ __global__ void k_block_mask(const int64_t* __restrict__ K, int n, int bs, int n
     // so only the zero tiles are read in full
     const int total = rn * cn;
     int any = 0;
+    if (((n | bs) & 1) == 0) {  // even n and bs: 16-byte pairs, 8 KB chunks as below
+        const int half = total / 2, cp = cn / 2;
+        for (int base = 0; base < half; base += 2 * blockDim.x) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int e = base + u * blockDim.x + threadIdx.x;
+                if (e < half) {
+                    const int r = e / cp, c = 2 * (e - r * cp);
+                    const longlong2 v = __ldcs(reinterpret_cast<const longlong2*>(
+                        K + (int64_t)(r0 + r) * n + c0 + c));
+                    any |= (v.x | v.y) != 0;
+                }
+            }
+            if (__syncthreads_or(any)) {
+                any = 1;
+                break;
+            }
+        }
+        if (threadIdx.x == 0) mask[t] = (uint8_t)any;
+        return;
+    }
     for (int base = 0; base < total; base += 4 * blockDim.x) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
