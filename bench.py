@@ -7,10 +7,12 @@ screening + ERIs + contraction into K (+ NCCL all-reduce of K and the fourfold
 epilogue for N>1).  The shell-pair tree is geometry-only (built once per
 SCF) and is reported separately as `pair_tree_ms`.
 
-`--impl reference` times the reference algorithm's CPU implementation (the
-oracle port in oracle/, kind "port": the reference is pure Python and cannot
-travel to the GPU box) on a bounded sub-cluster of the same recipe with all
-host threads, rank 0 only.
+`--impl reference` times the reference's own CPU implementation (hexfock,
+installed unmodified into baseline/_ref, which travels to the GPU box) on a
+bounded s-only sub-cluster of the same recipe (the reference has no p shells),
+the faster of threads=1 and threads=cpu_count, rank 0 only; the p-capable
+oracle port on the full basis is reported beside it.  Without baseline/_ref
+the port stands in (kind "port").
 """
 
 from __future__ import annotations
@@ -79,65 +81,157 @@ def workload_desc(args, cfg):
     return d
 
 
-# --------------------------------------------------------------- CPU (oracle port)
+# --------------------------------------------------------------- CPU baselines
 
-def cpu_sample(args):
-    """Bounded sample of the workload for the CPU implementation."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _import_reference():
+    """The unmodified reference package (hexfock 0.1.0) installed into baseline/_ref
+    (pip --target from a copy of /root/reference/pkg), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "hexfock")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import hexfock  # noqa: F401
+        from hexfock import basis, exchange_naive, exchange_symmetry, quadtree
+    except Exception:
+        return None
+    return basis, quadtree, exchange_naive, exchange_symmetry
+
+
+def ref_sample(args):
+    """The reference's own CPU path needs s shells, so it runs on the
+    s-only sub-basis of the workload's recipe: the same geometry recipe, s shells
+    only, the matching rows / columns of the same density.
+    c1 is all-s and runs in full; c3-c5 use a bounded sub-cluster."""
     from paper_1401_6961_b200 import configs
     if args.config == "c1":
         cfg = configs.config1()
         desc = "full c1 (32 s shells)"
     elif args.config == "c2":
-        n = args.cpu_sample_units or 24
+        n = args.cpu_sample_units or 48
         cfg = configs.config2(n_centers=n)
         desc = f"c2 recipe, {n}-center chain"
     else:
-        n = args.cpu_sample_units or 6
+        n = args.cpu_sample_units or 16
         cfg = configs.cube_cluster(n, {"c3": 3, "c4": 4, "c5": 5}[args.config], args.config)
-        desc = f"{args.config} cube recipe, {n} units ({cfg.n_shells} shells, {cfg.n_functions} functions)"
+        desc = f"{args.config} cube recipe, {n} units"
     if args.tau is not None:
         cfg.tau_2e = args.tau
         cfg.tau_ovlp = 1e-3 * args.tau
     return cfg, desc
 
 
-def run_cpu(args, steps, warmup):
-    from oracle import hexfock_oracle as ho
-    cfg, desc = cpu_sample(args)
-    st = ho.Setup(cfg.system, cfg.P, tau_ovlp=cfg.tau_ovlp, leaf_size=cfg.leaf_size)
-    threads = os.cpu_count() or 1
-    f = st.naive if args.mode == "naive" else st.symmetric
-    for _ in range(warmup):
-        f(cfg.tau_2e, threads=threads)
-    times, quartets = [], 0
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        _, c = f(cfg.tau_2e, threads=threads)
-        times.append(time.perf_counter() - t0)
-        quartets = c.eri_shell_quartets
+def run_reference_cpu(args, steps):
+    """Time the reference's build_exchange_symmetric / build_exchange_naive
+    (exchange_symmetry.py:364, exchange_naive.py:200) on the host cores.  Trees
+    are built once, outside the timed builds (cli.py times them together; we
+    report them apart).  Both threads=1 and threads=os.cpu_count() are run (the
+    reference farms depth-1 subtrees over a thread pool, GIL-bound); the faster
+    is the reported value and the timed steps use it.  None if baseline/_ref is
+    not installed."""
+    import numpy as np
+    mods = _import_reference()
+    if mods is None:
+        return None
+    hb, hq, hn, hs = mods
+    cfg, desc = ref_sample(args)
+    sh = cfg.system.shells
+    fn = np.concatenate([[0], np.cumsum([s.n_functions for s in sh])])
+    keep = [k for k, s in enumerate(sh) if int(getattr(s, "l", 0)) == 0]
+    fidx = np.asarray([fn[k] for k in keep])
+    shells = [hb.GaussianShell(center=sh[k].center, primitives=list(sh[k].primitives)) for k in keep]
+    system = hb.BasisSystem(shells=hb._assign_offsets(shells), atoms=[])
+    P = np.ascontiguousarray(np.asarray(cfg.P)[np.ix_(fidx, fidx)])
+    t0 = time.perf_counter()
+    part = hq.build_partition(system, cfg.leaf_size)
+    pairs = hq.build_pair_tree(system, part, tau_ovlp=cfg.tau_ovlp)
+    P_tree = hq.build_matrix_tree(P, part)
+    tree_ms = 1e3 * (time.perf_counter() - t0)
+    naive = args.mode == "naive"
+
+    def build(threads):
+        t = time.perf_counter()
+        if naive:
+            _, c = hn.build_exchange_naive(pairs, pairs, P_tree, tau_2e=cfg.tau_2e, threads=threads)
+        else:
+            _, c = hs.build_exchange_symmetric(pairs, P_tree, tau_2e=cfg.tau_2e, threads=threads)
+        return time.perf_counter() - t, c.eri_shell_quartets
+
+    nall = os.cpu_count() or 1
+    t1, q = build(1)
+    tall, _ = build(nall)
+    best = 1 if t1 <= tall else nall
+    times = [build(best)[0] for _ in range(steps)] if steps else [min(t1, tall)]
     tot = sum(times)
-    return {"value": quartets * steps / tot, "unit": "quartets/s", "cores": threads,
-            "kind": "port", "sample": desc + f"; {quartets} surviving quartets per build, "
-                                             f"{1e3 * tot / steps:.0f} ms per build"}
+    return {"value": q * len(times) / tot, "unit": "quartets/s", "cores": best, "kind": "reference",
+            "sample": (desc + f", s-only sub-basis: {len(shells)} s shells of {cfg.n_shells}, "
+                       f"{len(shells)} functions; {q} surviving quartets per build, "
+                       f"{1e3 * tot / len(times):.0f} ms per build"),
+            "impl": ("hexfock 0.1.0 (unmodified, baseline/_ref) "
+                     + ("build_exchange_naive" if naive else "build_exchange_symmetric")),
+            "threads_1": {"quartets_per_s": q / t1, "ms_per_build": 1e3 * t1},
+            "threads_all": {"cores": nall, "quartets_per_s": q / tall, "ms_per_build": 1e3 * tall},
+            "tree_build_ms": tree_ms,
+            "note": "the faster of threads=1 / threads=cpu_count is reported; the reference cannot "
+                    "evaluate p shells, so its rate is on the s-only sub-basis"}
+
+
+def port_sample(args):
+    """Bounded sample of the full (p-shell) workload for the oracle port."""
+    from paper_1401_6961_b200 import configs
+    if args.config == "c1":
+        return configs.config1(), "full c1 (32 s shells)"
+    if args.config == "c2":
+        n = 24
+        return configs.config2(n_centers=n), f"c2 recipe, {n}-center chain"
+    n = 6
+    cfg = configs.cube_cluster(n, {"c3": 3, "c4": 4, "c5": 5}[args.config], args.config)
+    return cfg, f"{args.config} cube recipe, {n} units ({cfg.n_shells} shells, {cfg.n_functions} functions)"
+
+
+def run_port_cpu(args):
+    """One build of the oracle port (oracle/hexfock_oracle.py, p-capable) with the
+    full basis, single-threaded (its thread pool is GIL-bound)."""
+    from oracle import hexfock_oracle as ho
+    cfg, desc = port_sample(args)
+    if args.tau is not None:
+        cfg.tau_2e, cfg.tau_ovlp = args.tau, 1e-3 * args.tau
+    st = ho.Setup(cfg.system, cfg.P, tau_ovlp=cfg.tau_ovlp, leaf_size=cfg.leaf_size)
+    f = st.naive if args.mode == "naive" else st.symmetric
+    t0 = time.perf_counter()
+    _, c = f(cfg.tau_2e, threads=1)
+    dt = time.perf_counter() - t0
+    return {"value": c.eri_shell_quartets / dt, "unit": "quartets/s", "cores": 1, "kind": "port",
+            "sample": desc + f"; {c.eri_shell_quartets} surviving quartets per build, {1e3 * dt:.0f} ms per build"}
 
 
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = make_config(args) if args.config in ("c1", "c2") else None
     steps, warmup = args.steps, min(args.warmup, 1)
-    cb = run_cpu(args, steps, warmup)
+    cb = run_reference_cpu(args, steps)
+    port = None
+    if cb is None:   # baseline/_ref absent: the oracle port stands in
+        cb = run_port_cpu(args)
+        note = "oracle port of the reference algorithm (baseline/_ref not installed)"
+    else:
+        port = run_port_cpu(args)
+        note = ("the reference's own CPU implementation (" + cb["impl"] + ") on a bounded s-only "
+                "sample of the workload; warm-up = one threads=1 and one threads=cpu_count build")
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "quartets/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "mode": args.mode,
-                       "note": "CPU oracle port of the reference algorithm on a bounded sample"},
+            "config": {"workload": args.config, "mode": "naive" if args.mode == "naive" else "fourfold",
+                       "note": note},
             "cpu_baseline": cb,
+            "port_full_basis": port,
             "e2e": {"value": cb["value"], "unit": "quartets/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    del cfg
     print(json.dumps(line), flush=True)
 
 
@@ -446,9 +540,12 @@ def native_arm(args):
                          "fourfold_quartets_per_s = the fourfold surviving-quartet count / this K-build time"}
         del K4, K8
 
-    cpu = None
+    cpu = port = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = run_cpu(args, 1, 0)
+        cpu = run_reference_cpu(args, 0)
+        port = run_port_cpu(args)
+        if cpu is None:
+            cpu, port = port, None
 
     if rank == 0:
         stage_med = [statistics.median([s[k] for s in stage]) for k in range(6)] if stage else tm
@@ -502,6 +599,7 @@ def native_arm(args):
                     "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8,
                     "ms_per_step": float(et.item()) / max(args.e2e_steps, 1)},
             "cpu_baseline": cpu,
+            "cpu_port_full_basis": port,
             "eightfold": eight,
             "gpu_launches": int(lc1.value - lc0.value),
             "clocks": clk,

@@ -218,7 +218,10 @@ int hxf_partition_build(const int32_t* shell_nfunc, int64_t n_shells, int leaf_s
  * hxf_block_slots: slot[0..nt] = exclusive prefix sum of mask (nt + 1 entries);
  *   *n_blocks (host) = number of flagged tiles (synchronises the stream).
  * hxf_block_pack / hxf_block_unpack: copy flagged tiles K <-> buf (n_blocks * bs^2
- *   int64); unpack writes only flagged tiles. */
+ *   int64); unpack writes only flagged tiles.
+ * Any 8-byte aligned K / buf is accepted (16-byte accesses are used only when
+ * n and bs are even and both pointers are 16-byte aligned); more than
+ * 2^31 - 1 tiles is HXF_EINVAL. */
 int hxf_block_mask(const int64_t* K, int n, int bs, uint8_t* mask, void* stream);
 int hxf_block_slots(const uint8_t* mask, int64_t n_tiles, int64_t* slot, int64_t* n_blocks, void* stream);
 int hxf_block_pack(const int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, int64_t* buf,

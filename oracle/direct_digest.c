@@ -25,6 +25,10 @@
  *               the naive set -- the four-fold driver's quartet_log
  *               (exchange_symmetry.py:332-340; checked against the Python
  *               oracle in tests/test_direct_digest.py)
+ *   eightfold : (fourfold == 2) the fourfold tuples with (i,j) <= (k,l)
+ *               lexicographically -- the fourfold set folded bra <-> ket,
+ *               the set the optional 8-fold driver evaluates (SURVEY.md 8(a)
+ *               S8); the device digest orients each quartet the same way
  *
  * Sampling: only tuples whose first index i satisfies i % mod == rem.
  *
@@ -77,9 +81,10 @@ static void* worker(void* arg) {
         pthread_mutex_unlock(&J->lock);
         if (a >= ns) break;
         if (!J->fourfold && J->mod > 1 && a % J->mod != J->rem) continue;
+        const int eight = J->fourfold == 2;
         for (int64_t qb = J->qo[a]; qb < J->qo[a + 1]; ++qb) {
             const int b = J->qc[qb];
-            if (J->fourfold && J->mod > 1 && (a < b ? a : b) % J->mod != J->rem) continue;
+            if (J->fourfold == 1 && J->mod > 1 && (a < b ? a : b) % J->mod != J->rem) continue;
             const double fab = J->fq[a * (int64_t)ns + b];
             for (int64_t pk = J->po[b]; pk < J->po[b + 1]; ++pk) {
                 const int k = J->pc[pk];
@@ -106,6 +111,10 @@ static void* worker(void* arg) {
                         }
                         if (!first) continue;
                         i = ci; j = cj; kk = ck; ll = cl;
+                        if (eight) {
+                            if (ci > ck || (ci == ck && cj > cl)) continue;
+                            if (J->mod > 1 && (int)(i % (uint64_t)J->mod) != J->rem) continue;
+                        }
                     }
                     const uint64_t h = mix64(((i * ns + j) * ns + kk) * ns + ll);
                     c += 1;

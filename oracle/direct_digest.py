@@ -32,12 +32,13 @@ def _load():
     return _lib
 
 
-def digest(q, pmax, tau, mode="schwarz", fourfold=False, sample=(1, 0), threads=None):
+def digest(q, pmax, tau, mode="schwarz", fourfold=False, sample=(1, 0), threads=None, eightfold=False):
     """(count, sum h, sum h(h)) of the direct-SCF evaluated set.
 
     q: (ns, ns) canonical Q (<= 0 where the pair is absent); pmax: (ns, ns)
     max |P| per shell block; fourfold: canonical tuples (the four-fold
-    driver's quartet_log) instead of ordered ones.
+    driver's quartet_log) instead of ordered ones; eightfold: the canonical
+    tuples with (i,j) <= (k,l) (the fourfold set folded bra <-> ket).
     """
     q = np.ascontiguousarray(q, dtype=np.float64)
     pmax = np.ascontiguousarray(pmax, dtype=np.float64)
@@ -46,7 +47,7 @@ def digest(q, pmax, tau, mode="schwarz", fourfold=False, sample=(1, 0), threads=
     out = np.zeros(3, dtype=np.uint64)
     nt = threads or max(1, os.cpu_count() or 1)
     rc = _load().direct_digest(ns, q.ctypes.data, pmax.ctypes.data, float(tau),
-                               0 if mode == "schwarz" else 1, 1 if fourfold else 0,
+                               0 if mode == "schwarz" else 1, 2 if eightfold else (1 if fourfold else 0),
                                int(sample[0]), int(sample[1]), nt, out.ctypes.data)
     if rc:
         raise MemoryError("direct_digest: allocation failed")

@@ -21,7 +21,7 @@
 namespace {
 
 // one block per tile: any nonzero in rows [ti*bs, ..) x cols [tj*bs, ..)
-__global__ void k_block_mask(const int64_t* __restrict__ K, int n, int bs, int nb,
+__global__ void k_block_mask(const int64_t* __restrict__ K, int n, int bs, int nb, bool v16,
                              uint8_t* __restrict__ mask) {
     const int64_t t = blockIdx.x;
     const int ti = (int)(t / nb), tj = (int)(t % nb);
@@ -32,7 +32,7 @@ __global__ void k_block_mask(const int64_t* __restrict__ K, int n, int bs, int n
     // so only the zero tiles are read in full
     const int total = rn * cn;
     int any = 0;
-    if (((n | bs) & 1) == 0) {  // even n and bs: 16-byte pairs, 8 KB chunks as below
+    if (v16) {  // even n and bs, 16-byte aligned K: 16-byte pairs, 8 KB chunks as below
         const int half = total / 2, cp = cn / 2;
         for (int base = 0; base < half; base += 2 * blockDim.x) {
 #pragma unroll
@@ -76,14 +76,15 @@ __global__ void k_mask_to_int(const uint8_t* __restrict__ m, int64_t nt, int64_t
 }
 
 template <bool PACK>
-__global__ void k_block_move(int64_t* __restrict__ K, int n, int bs, int nb, const uint8_t* __restrict__ mask,
-                             const int64_t* __restrict__ slot, int64_t* __restrict__ buf) {
+__global__ void k_block_move(int64_t* __restrict__ K, int n, int bs, int nb, bool v16,
+                             const uint8_t* __restrict__ mask, const int64_t* __restrict__ slot,
+                             int64_t* __restrict__ buf) {
     const int64_t t = blockIdx.x;
     if (!mask[t]) return;
     const int ti = (int)(t / nb), tj = (int)(t % nb);
     const int r0 = ti * bs, c0 = tj * bs;
     int64_t* b = buf + slot[t] * (int64_t)bs * bs;
-    if (((n | bs) & 1) == 0) {  // even n and bs: 16-byte aligned pairs along a row
+    if (v16) {  // even n and bs, 16-byte aligned K and buf: aligned pairs along a row
         longlong2* b2 = reinterpret_cast<longlong2*>(b);
         for (int e = threadIdx.x; e < bs * bs / 2; e += blockDim.x) {
             const int r = (2 * e) / bs, c = 2 * e - r * bs;
@@ -108,13 +109,26 @@ __global__ void k_block_move(int64_t* __restrict__ K, int n, int bs, int nb, con
     }
 }
 
+// 16-byte accesses need even n and bs (pairs never straddle a row or tile edge)
+// and 16-byte aligned base pointers
+bool use_v16(int n, int bs, const void* a, const void* b) {
+    return ((n | bs) & 1) == 0 && ((((uintptr_t)a) | ((uintptr_t)b)) & 15) == 0;
+}
+
+// one CTA per tile: the grid must fit the launch limit
+void check_tiles(int64_t nt) {
+    if (nt > 0x7fffffffll)
+        throw HxfError{HXF_EINVAL, "block size too small for n: more than 2^31-1 tiles"};
+}
+
 }  // namespace
 
 void block_mask_device(const int64_t* K, int n, int bs, uint8_t* mask, cudaStream_t st) {
     const int nb = (n + bs - 1) / bs;
     const int64_t nt = (int64_t)nb * nb;
     if (nt == 0) return;
-    { k_block_mask<<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, mask); note_launch(); }
+    check_tiles(nt);
+    { k_block_mask<<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, use_v16(n, bs, K, K), mask); note_launch(); }
     HXF_CUDA(cudaGetLastError());
 }
 
@@ -141,10 +155,12 @@ void block_move_device(int64_t* K, int n, int bs, const uint8_t* mask, const int
     const int nb = (n + bs - 1) / bs;
     const int64_t nt = (int64_t)nb * nb;
     if (nt == 0) return;
+    check_tiles(nt);
+    const bool v16 = use_v16(n, bs, K, buf);
     if (pack) {
-        k_block_move<true><<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, mask, slot, buf);
+        k_block_move<true><<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, v16, mask, slot, buf);
     } else {
-        k_block_move<false><<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, mask, slot, buf);
+        k_block_move<false><<<(unsigned)nt, 256, 0, st>>>(K, n, bs, nb, v16, mask, slot, buf);
     }
     note_launch();
     HXF_CUDA(cudaGetLastError());

@@ -483,8 +483,10 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         hxf_cache_free(leaf0, st);
     }
     res.frontier_sizes.push_back(n_cur);
+    bool cut_reached = false;
     for (int L = 0; L < D && n_cur > 0; ++L) {
         if (sharded && L == in.shard_level) {
+            cut_reached = true;
             // restrict the frontier to this shard; from here on counters are real
             int64_t cnt = 0;
             uint64_t* part = nullptr;
@@ -496,9 +498,9 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
                     int64_t* dn = talloc<int64_t>(1, st);
                     HXF_CUDA(cudaMemcpyAsync(dm, in.shard_mask, nm, cudaMemcpyHostToDevice, st));
                     size_t tb = 0;
-                    cub::DeviceSelect::Flagged(nullptr, tb, cur, dm, part, dn, nm, st);
+                    HXF_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, cur, dm, part, dn, nm, st));
                     char* tmp = talloc<char>(tb, st);
-                    cub::DeviceSelect::Flagged(tmp, tb, cur, dm, part, dn, nm, st);
+                    HXF_CUDA(cub::DeviceSelect::Flagged(tmp, tb, cur, dm, part, dn, nm, st));
                     HXF_CUDA(cudaMemcpyAsync(&cnt, dn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
                     HXF_CUDA(cudaStreamSynchronize(st));
                     for (void* p : {(void*)dm, (void*)dn, (void*)tmp}) hxf_cache_free(p, st);
@@ -565,10 +567,10 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         HXF_CUDA(cudaMemsetAsync(cl + nb, 0, sizeof(int64_t), st));
         HXF_CUDA(cudaMemsetAsync(ce + nb, 0, sizeof(int64_t), st));
         size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, cl, ol, nb + 1, st);
+        HXF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cl, ol, nb + 1, st));
         void* tbuf = talloc<char>(tb, st);
-        cub::DeviceScan::ExclusiveSum(tbuf, tb, cl, ol, nb + 1, st);
-        cub::DeviceScan::ExclusiveSum(tbuf, tb, ce, oe, nb + 1, st);
+        HXF_CUDA(cub::DeviceScan::ExclusiveSum(tbuf, tb, cl, ol, nb + 1, st));
+        HXF_CUDA(cub::DeviceScan::ExclusiveSum(tbuf, tb, ce, oe, nb + 1, st));
         int64_t tot[2];
         HXF_CUDA(cudaMemcpyAsync(&tot[0], ol + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         HXF_CUDA(cudaMemcpyAsync(&tot[1], oe + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -602,6 +604,13 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     fold_stripes(counters, ledger);
     hxf_cache_free(sc, st);
     hxf_cache_free(sl, st);
+    if (discard_top && !cut_reached) {
+        // the traversal ended above the cut (a single-leaf system, or a frontier that
+        // emptied first): every leaf task belongs to shard 0, none to this shard
+        for (uint64_t* p : leaf_parts) hxf_cache_free(p, st);
+        leaf_parts.clear();
+        leaf_counts.clear();
+    }
     if (in.frontier_only) {
         res.frontier = cur;
         res.n_frontier = n_cur;

@@ -215,8 +215,14 @@ class _NativeBlockOps:
     """Block-sparse tile ops of libhxf (csrc/reduce.cu) on CUDA int64 tensors."""
 
     @staticmethod
+    def _check(K):
+        from .exchange import check_device_matrix
+        check_device_matrix(K, K.shape[0] if K.dim() == 2 else -1, "int64", None, "K")
+
+    @staticmethod
     def mask(K, bs):
         import torch
+        _NativeBlockOps._check(K)
         n = K.shape[0]
         nb = (n + bs - 1) // bs
         m = torch.empty(nb * nb, dtype=torch.uint8, device=K.device)
@@ -237,6 +243,7 @@ class _NativeBlockOps:
     @staticmethod
     def pack(K, bs, m, slot, nblk):
         import torch
+        _NativeBlockOps._check(K)
         buf = torch.empty(max(1, nblk) * bs * bs, dtype=torch.int64, device=K.device)
         _native.check(_native.lib().hxf_block_pack(ctypes.c_void_p(K.data_ptr()), K.shape[0], bs,
                                                    ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(slot.data_ptr()),
@@ -245,6 +252,7 @@ class _NativeBlockOps:
 
     @staticmethod
     def unpack(K, bs, m, slot, buf):
+        _NativeBlockOps._check(K)
         _native.check(_native.lib().hxf_block_unpack(ctypes.c_void_p(K.data_ptr()), K.shape[0], bs,
                                                      ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(slot.data_ptr()),
                                                      ctypes.c_void_p(buf.data_ptr()), _native.current_stream()))
@@ -294,6 +302,8 @@ def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, sha
         shards = plan(bra, ket, P, tau_2e, mode, symmetry, world)
     level, ranges = shards
     b, e, stride = ranges[rank]
+    from .exchange import check_device_matrix
+    check_device_matrix(K_dev, bra.row.n_functions, "float64", bra._t.ds.device_index, "K_dev")
     Kfx = K_dev.view(torch.int64)          # the FP64 buffer reused for the accumulator
     (_, S), c, _ = run_exchange(bra, ket, P, tau_2e, mode, symmetry, True, None, K_out=Kfx,
                                 shard=(level, b, e, stride), symmetrize=False,

@@ -219,6 +219,21 @@ def _check_same_partition(bra, ket, p):
         raise InvalidArgumentError("bra, ket and P must be built over the same partition")
 
 
+def check_device_matrix(K, n, dtype, device=None, what="K_out"):
+    """A device output buffer must be a contiguous CUDA (n, n) tensor of `dtype`
+    on the system's device: the library writes n*n elements through its pointer."""
+    if not (hasattr(K, "is_cuda") and K.is_cuda):
+        raise InvalidArgumentError(f"{what} must be a CUDA tensor")
+    if tuple(K.shape) != (n, n):
+        raise InvalidArgumentError(f"{what} must have shape ({n}, {n}), got {tuple(K.shape)}")
+    if str(K.dtype) != f"torch.{dtype}":
+        raise InvalidArgumentError(f"{what} must be {dtype}, got {K.dtype}")
+    if not K.is_contiguous():
+        raise InvalidArgumentError(f"{what} must be contiguous")
+    if device is not None and K.device.index != device:
+        raise InvalidArgumentError(f"{what} is on cuda:{K.device.index}, the system on cuda:{device}")
+
+
 def _require_root(node, what):
     if node._level != 0:
         raise InvalidArgumentError(f"{what}: the device drivers start from the tree root")
@@ -278,6 +293,8 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
             raise InvalidArgumentError("digest must be a contiguous numpy uint64[3]")
         opts.digest = digest.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
         opts.digest_mod, opts.digest_rem = int(digest_sample[0]), int(digest_sample[1])
+    if K_out is not None:
+        check_device_matrix(K_out, n, "int64" if K_fixed else "float64", bra._t.ds.device_index)
     log_count = ctypes.c_int64(0)
     cap = 0
     if quartet_log is not None and evaluate:
@@ -291,7 +308,7 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
             opts.log_capacity = cap
             opts.log_count = ctypes.pointer(log_count)
         if K_out is None:
-            K = np.empty((n, n)) if True else None
+            K = np.empty((n, n))
             opts.K_on_device = 0
             kptr = K.ctypes.data_as(ctypes.c_void_p)
         else:

@@ -187,6 +187,7 @@ class _DeviceSystem:
             _native.ptr(arr["fhi"]), _native.ptr(arr["k0"]), _native.ptr(arr["k1"]),
             ctypes.byref(h)))
         self.handle = h
+        self.device_index = int(device)
         self.n_shells = ns
         self.n_functions = int(nfn.sum())
         self.shell_fn = np.concatenate([[0], np.cumsum(nfn)]).astype(np.int64)

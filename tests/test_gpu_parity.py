@@ -274,3 +274,32 @@ def test_scratch_release_between_builds():
     assert hx.release_scratch() == 0
     K2, c2 = hx.build_exchange_symmetric(pairs, P_tree, 1e-9)
     assert np.array_equal(K1, K2) and c1.to_dict() == c2.to_dict()
+
+
+@pytest.mark.parametrize("sym", [False, True])
+@pytest.mark.parametrize("case", ["single_leaf", "cut_below_frontier"])
+def test_shards_above_unreached_cut_hold_no_work(sym, case):
+    """A shard with shard_begin != 0 whose cut level is never reached (a single
+    leaf span, or a cut deeper than where the frontier empties) owns no leaf task:
+    the shards still sum to the unsharded build (traverse.cu)."""
+    from paper_1401_6961_b200 import exchange
+    if case == "single_leaf":
+        cfg = configs.cube_cluster(1, 3, "one")
+        part = hx.build_partition(cfg.system, leaf_size=10)
+        assert len(part.levels) == 1
+        level, tau = 0, 1e-8
+    else:
+        cfg = configs.cube_cluster(8, 3, "tiny")
+        part = hx.build_partition(cfg.system, leaf_size=6)
+        level, tau = len(part.levels) + 3, 1e-9     # the traversal ends above this cut
+    pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
+    P_tree = hx.build_matrix_tree(cfg.P, part)
+    K_full, c_full, _ = exchange.run_exchange(pairs, pairs, P_tree, tau, "schwarz", sym, symmetrize=False)
+    K0, c0, _ = exchange.run_exchange(pairs, pairs, P_tree, tau, "schwarz", sym, shard=(level, 0, 1 << 20),
+                                      symmetrize=False)
+    K1, c1, _ = exchange.run_exchange(pairs, pairs, P_tree, tau, "schwarz", sym, shard=(level, 1, 1 << 20),
+                                      symmetrize=False)
+    assert not np.any(K1)
+    assert c1.eri_shell_quartets == 0 and c1.leaf_contractions == 0
+    assert np.array_equal(K0 + K1, K_full)
+    assert c0.eri_shell_quartets == c_full.eri_shell_quartets
