@@ -15,6 +15,12 @@ contraction in registers; then the horizontal transfer
 (a,b+1_i| = (a+1_i,b| + AB_i (a,b| on the contracted values.
 Output layout out[((i*NJ + j)*NK + k)*NL + l], p components ordered x,y,z.
 
+Far-field quartets (every primitive quartet's Boys argument T above the
+table range, decided per quartet in leaf.cu) run core<NKC, true>: the
+asymptotic F_m only (boys_far, the same values the branch-free evaluation
+selects there), and for (ss|ss) the closed form c'_b c'_k sqrt(pi)/2 / |P-Q|
+with c' = c / sqrt(p) stored per primitive pair (PrimPair.cs).
+
 Light classes (L <= 1) get a compile-time ket primitive count: eval()
 dispatches on nk (warp-uniform, survivors are sorted by primitive counts) to
 core<NKC>, which caches the ket primitives in registers and fully unrolls the
@@ -108,18 +114,18 @@ class Gen:
 
 
 def prim_body(w, la, lb, lc, ld, accs, ind, fold=False):
-    """Statements for one primitive quartet (bp, kp in scope)."""
+    """Statements for one primitive quartet (bp, kp in scope).  FAR (a template
+    parameter of core) selects the asymptotic Boys branch only (boys_far)."""
     L = la + lb + lc + ld
     p = " " * ind
-    if L == 0 and fold:  # (ss|ss): bra coefficient applied once per bra primitive (accb)
-        w(p + "const double ps = bp.p + kp.p;")
-        w(p + "const double r = rsqrt_pos(ps);")
-        w(p + "const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;")
-        w(p + "const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
-        w(p + "const double T = bp.p * kp.p * (r * r) * R2;")
-        w(p + "double F[1];")
-        w(p + "boys_eval<0>(T, F, tab);")
-        w(p + "accb = fma(kp.c * r, F[0], accb);")
+    if L == 0 and fold:  # (ss|ss) far: c'_b c'_k sqrt(pi)/2 / |P - Q| (c' = c / sqrt(p), PrimPair.cs)
+        w(p + "if constexpr (FAR) {")
+        w(p + "  const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;")
+        w(p + "  const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
+        w(p + "  accb = fma(kp.cs, rsqrt_pos(R2), accb);")
+        w(p + "} else {")
+        prim_body_ss(w, p + "  ")
+        w(p + "}")
         return
     w(p + "const double ps = bp.p + kp.p;")
     w(p + "const double r = rsqrt_pos(ps);")
@@ -129,7 +135,28 @@ def prim_body(w, la, lb, lc, ld, accs, ind, fold=False):
     w(p + "const double T = bp.p * kp.p * r2 * R2;")
     w(p + "const double pref = bp.c * kp.c * r;")
     w(p + f"double F[{L + 1}];")
-    w(p + f"boys_eval<{L}>(T, F, tab);")
+    w(p + "if constexpr (FAR) {")
+    w(p + f"  boys_far<{L}>(T, F);")
+    w(p + "} else {")
+    w(p + f"  boys_eval<{L}>(T, F, tab);")
+    w(p + "}")
+    prim_rest(w, la, lb, lc, ld, accs, p)
+
+
+def prim_body_ss(w, p):
+    if True:  # (ss|ss): bra coefficient applied once per bra primitive (accb)
+        w(p + "const double ps = bp.p + kp.p;")
+        w(p + "const double r = rsqrt_pos(ps);")
+        w(p + "const double PQx = bp.x - kp.x, PQy = bp.y - kp.y, PQz = bp.z - kp.z;")
+        w(p + "const double R2 = PQx * PQx + PQy * PQy + PQz * PQz;")
+        w(p + "const double T = bp.p * kp.p * (r * r) * R2;")
+        w(p + "double F[1];")
+        w(p + "boys_eval<0>(T, F, tab);")
+        w(p + "accb = fma(kp.c * r, F[0], accb);")
+
+
+def prim_rest(w, la, lb, lc, ld, accs, p):
+    L = la + lb + lc + ld
     for m in range(L + 1):
         w(p + f"const double bm{m} = pref * F[{m}];")
     if L > 0:
@@ -161,12 +188,14 @@ def gen_class(la, lb, lc, ld):
     accs = [(e, f) for e in es for f in fs]
     cached = L <= 1
     need_ip = lc + ld > 0
+    # (ss|ss) far path reads only {cs, x, y, z}
+    load = "(FAR ? load_pp_far : load_pp)" if L == 0 else "load_pp"
     out = []
     w = out.append
     w(f"template <> struct Eri<{la},{lb},{lc},{ld}> {{")
     w(f"  static constexpr int NI = {ni}, NJ = {nj}, NK = {nk}, NL = {nl}, L = {L};")
     # ---- core<NKC>: NKC > 0 compile-time ket primitive count (register cache)
-    w("  template <int NKC>")
+    w("  template <int NKC, bool FAR>")
     w("  __device__ __forceinline__ static void core(const PrimPair* __restrict__ bra, int nb,")
     w("      const PrimPair* __restrict__ ket, int nk, const double3 A, const double3 B,")
     w("      const double3 C, const double3 D, const double* __restrict__ tab,")
@@ -177,11 +206,11 @@ def gen_class(la, lb, lc, ld):
         w("    if constexpr (NKC > 0) {")
         w("      PrimPair kq[NKC > 0 ? NKC : 1];")
         w("#pragma unroll")
-        w("      for (int t = 0; t < NKC; ++t) kq[t] = load_pp(ket + t);")
-        w("      PrimPair bn = load_pp(bra);")
+        w(f"      for (int t = 0; t < NKC; ++t) kq[t] = {load}(ket + t);")
+        w(f"      PrimPair bn = {load}(bra);")
         w("      for (int ib = 0; ib < nb; ++ib) {")
         w("        const PrimPair bp = bn;")
-        w("        if (ib + 1 < nb) bn = load_pp(bra + ib + 1);  // prefetch the next bra primitive")
+        w(f"        if (ib + 1 < nb) bn = {load}(bra + ib + 1);  // prefetch the next bra primitive")
         if la + lb > 0:
             w("        const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
             w("        const double o2p = 0.5 * bp.ip;")
@@ -193,27 +222,29 @@ def gen_class(la, lb, lc, ld):
         prim_body(w, la, lb, lc, ld, accs, 10, fold=True)
         w("        }")
         if L == 0:
-            w("        acc_000_000 = fma(bp.c, accb, acc_000_000);")
+            w("        acc_000_000 = fma(FAR ? bp.cs : bp.c, accb, acc_000_000);")
         w("      }")
         w("    } else {")
     w("      for (int ib = 0; ib < nb; ++ib) {")
-    w("        const PrimPair bp = load_pp(bra + ib);")
+    w(f"        const PrimPair bp = {load}(bra + ib);")
     if la + lb > 0:
         w("        const double PAx = bp.x - A.x, PAy = bp.y - A.y, PAz = bp.z - A.z;")
         w("        const double o2p = 0.5 * bp.ip;")
-    w("        PrimPair kn = load_pp(ket);")
+    w(f"        PrimPair kn = {load}(ket);")
     if L == 0:
         w("        double accb = 0.0;")
     w("        for (int ik = 0; ik < nk; ++ik) {")
     w("          const PrimPair kp = kn;")
-    w("          if (ik + 1 < nk) kn = load_pp(ket + ik + 1);  // prefetch: hide the L1/L2 latency")
+    w(f"          if (ik + 1 < nk) kn = {load}(ket + ik + 1);  // prefetch: hide the L1/L2 latency")
     prim_body(w, la, lb, lc, ld, accs, 10, fold=True)
     w("        }")
     if L == 0:
-        w("        acc_000_000 = fma(bp.c, accb, acc_000_000);")
+        w("        acc_000_000 = fma(FAR ? bp.cs : bp.c, accb, acc_000_000);")
     w("      }")
     if cached:
         w("    }")
+    if L == 0:
+        w("    if constexpr (FAR) acc_000_000 *= HALF_SQRT_PI;")
     # horizontal recursion on contracted values
     memo = {}
     hl = []
@@ -258,6 +289,7 @@ def gen_class(la, lb, lc, ld):
         w(f"    out[{idx}] = {v};")
     w("  }")
     # ---- eval: dispatch on the (warp-uniform) ket primitive count
+    w("  template <bool FAR>")
     w("  __device__ __forceinline__ static void eval(const PrimPair* __restrict__ bra, int nb,")
     w("      const PrimPair* __restrict__ ket, int nk, const double3 A, const double3 B,")
     w("      const double3 C, const double3 D, const double* __restrict__ tab,")
@@ -265,11 +297,11 @@ def gen_class(la, lb, lc, ld):
     if cached:
         w("    switch (nk) {")
         for k in range(1, MAXK + 1):
-            w(f"      case {k}: core<{k}>(bra, nb, ket, nk, A, B, C, D, tab, out); return;")
-        w("      default: core<0>(bra, nb, ket, nk, A, B, C, D, tab, out); return;")
+            w(f"      case {k}: core<{k}, FAR>(bra, nb, ket, nk, A, B, C, D, tab, out); return;")
+        w("      default: core<0, FAR>(bra, nb, ket, nk, A, B, C, D, tab, out); return;")
         w("    }")
     else:
-        w("    core<0>(bra, nb, ket, nk, A, B, C, D, tab, out);")
+        w("    core<0, FAR>(bra, nb, ket, nk, A, B, C, D, tab, out);")
     w("  }")
     w("};")
     del need_ip

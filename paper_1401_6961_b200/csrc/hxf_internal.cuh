@@ -31,8 +31,9 @@ struct HxfError {
 // device): exponent sum p, 1/p, product centre, and
 // c = w_a w_b exp(-ab/p |AB|^2) / p * sqrt(2 pi^{5/2}), so the primitive
 // (ss|ss) is c_bra c_ket F0(T) / sqrt(p+q).  64-byte aligned record.
+// cs = c / sqrt(p): the far-field (ss|ss) closed form c'_b c'_k sqrt(pi)/2 / |P-Q|
 struct __align__(16) PrimPair {
-    double p, ip, c, x, y, z, pad0, pad1;
+    double p, ip, c, x, y, z, cs, pad1;
 };
 
 // Partition levels on device (quadtree.py:55-84): spans of every level,
@@ -102,6 +103,8 @@ struct hxf_pairs {
     double maxq;
     double amax;       // max over shells s of sum_{pairs (s,t) or (t,s)} n_f(t) sqrt(Q) (K scale bound)
     PrimPair* epp;     // ERI primitive table: each pair's primitives sorted by Schwarz factor, descending
+    float4* geo;       // per pair: centroid of the primitive centres, radius (conservative, far-field test)
+    float* gip;        // per pair: max 1/p over its primitives (rounded up)
     double* eS;        // per entry of epp: primitive Schwarz factor sqrt(max_comp (ab|ab))
     double smax_prim;  // max eS
     int* ncid;         // per leaf pair node (nleaf^2): compact live-node id, -1 if pruned
@@ -160,7 +163,17 @@ __device__ __forceinline__ PrimPair load_pp(const PrimPair* p) {
     double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
     PrimPair r;
     r.p = a.x; r.ip = a.y; r.c = b.x; r.x = b.y; r.y = c.x; r.z = c.y;
-    r.pad0 = 0.0; r.pad1 = 0.0;
+    r.cs = 0.0; r.pad1 = 0.0;
+    return r;
+}
+
+// the fields the far-field (ss|ss) path reads: c, centre, cs
+__device__ __forceinline__ PrimPair load_pp_far(const PrimPair* p) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
+    PrimPair r;
+    r.p = 0.0; r.ip = 0.0; r.c = b.x; r.x = b.y; r.y = c.x; r.z = c.y;
+    r.cs = d.x; r.pad1 = 0.0;
     return r;
 }
 

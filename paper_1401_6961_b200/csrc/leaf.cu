@@ -31,6 +31,10 @@
 #include "eri_classes.cuh"
 #include "traverse.cuh"
 
+#ifndef HXF_ERI_NOFAR   // 1: A/B build without the far-field path (every quartet on the table path)
+#define HXF_ERI_NOFAR 0
+#endif
+
 #define MAXS 10  // shells per leaf span (leaf_size <= 10 functions; checked in api.cu)
 #define MAXP (MAXS * MAXS)
 #define SCREEN_WARPS 4
@@ -73,7 +77,28 @@ struct ScreenArgs {
     const int* ncidk;
     const double* nveck;
     const double* nveck_tri;
+    const float4* bgeo;       // far-field test per emitted quartet (k_pair_geo, trees.cu)
+    const float4* kgeo;
+    const float* bgip;
+    const float* kgip;
 };
+
+// Far field: every primitive quartet of the shell quartet (bra pair pb, ket pair
+// pk) has Boys argument T = |P-Q|^2 / (1/p + 1/q) >= boys_far_t(L), from the
+// conservative per-pair centroid / radius / max 1/p (k_pair_geo).  Such quartets
+// sort into their own ERI range (key bit 12) whose kernels evaluate only the
+// asymptotic Boys branch -- the values the table path selects there.
+__device__ __forceinline__ bool quartet_far(const float4* bgeo, const float* bgip, const float4* kgeo,
+                                            const float* kgip, int64_t pb, int64_t pk, int L) {
+    const float4 gb = __ldg(bgeo + pb), gk = __ldg(kgeo + pk);
+    const float ip = __ldg(bgip + pb) + __ldg(kgip + pk);
+    const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
+    const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
+    return d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip;
+}
+#define KEY_FAR 0x1000
+#define KEY_BITS 13
+#define KEY_RANGES (1 << KEY_BITS)
 
 struct WarpSmem {
     double fa[MAXP], sa[MAXP], fb[MAXP], sb[MAXP];
@@ -607,8 +632,12 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                         const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
                         // bit 60: eightfold self-mirror quartet (bra pair == ket pair), weight 1/2
                         const uint64_t selfm = (EIGHT && pb == pk) ? 1ull : 0ull;
+                        const int L = __popc(ca & 3) + __popc(cb & 3);
+                        const bool far = keep_any && !HXF_ERI_NOFAR &&
+                                         quartet_far(a.bgeo, a.bgip, a.kgeo, a.kgip, (int64_t)pb, (int64_t)pk, L);
                         slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56) | (selfm << 60),
-                                  (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2)), lane);
+                                  (uint16_t)((far ? KEY_FAR : 0) | (cls << 8) | ((ca >> 2) << 4) | (cb >> 2)),
+                                  lane);
                     }
                 }
             }
@@ -733,6 +762,7 @@ __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double
 #ifndef HXF_ERI_MINB0
 #define HXF_ERI_MINB0 3
 #endif
+
 #ifndef HXF_ERI_MINB1
 #define HXF_ERI_MINB1 2
 #endif
@@ -746,19 +776,32 @@ __host__ __device__ constexpr int eri_min_blocks(int la, int lb, int lc, int ld)
            : ((HXF_ERI_MINB3_MASK >> ((la << 3) | (lb << 2) | (lc << 1) | ld)) & 1) ? 3
                                                                                    : HXF_ERI_MINB1;
 }
-template <int LA, int LB, int LC, int LD>
-__global__ void __launch_bounds__(128, eri_min_blocks(LA, LB, LC, LD)) k_eri(EriArgs e) {
+// far-field kernels: no Boys table and shorter dependency chains, so more
+// resident blocks ((ss|ss): 4 = <= 128 registers; p classes 2, as measured: 3 spills)
+#ifndef HXF_ERI_FAR_MINB0
+#define HXF_ERI_FAR_MINB0 4
+#endif
+#ifndef HXF_ERI_FAR_MINB1
+#define HXF_ERI_FAR_MINB1 2
+#endif
+__host__ __device__ constexpr int eri_far_min_blocks(int la, int lb, int lc, int ld) {
+    return (la + lb + lc + ld) == 0 ? HXF_ERI_FAR_MINB0 : HXF_ERI_FAR_MINB1;
+}
+template <int LA, int LB, int LC, int LD, bool FAR>
+__global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) : eri_min_blocks(LA, LB, LC, LD))
+    k_eri(EriArgs e) {
     typedef Eri<LA, LB, LC, LD> E;
     constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL;
     constexpr int CLS = (LA << 3) | (LB << 2) | (LC << 1) | LD;
+    constexpr int K0 = (FAR ? KEY_FAR : 0) | (CLS << 8);
     if (e.dbounds) {  // asynchronous launch: range from the sorted keys' bounds
-        const int64_t b0 = e.dbounds[CLS << 8];
-        e.n = e.dbounds[(CLS + 1) << 8] - b0;
+        const int64_t b0 = e.dbounds[K0];
+        e.n = e.dbounds[K0 + 256] - b0;
         e.rec += b0;
         if (e.n <= 0) return;
     }
     extern __shared__ __align__(16) double s_tab[];
-    boys_eri_table_to_smem<E::L>(s_tab);
+    if (!FAR) boys_eri_table_to_smem<E::L>(s_tab);
     long long nprim = 0, nq = 0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < e.n;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -778,7 +821,7 @@ __global__ void __launch_bounds__(128, eri_min_blocks(LA, LB, LC, LD)) k_eri(Eri
 #ifdef HXF_EXP_NOPRIM  // timing experiment: skip the primitive loops (results wrong)
             for (int q = 0; q < NI * NJ * NK * NL; ++q) out[q] = e.bpp[ib.z].c * e.kpp[ik.z].c;
 #else
-            E::eval(e.bpp + ib.z, nb, e.kpp + ik.z, nk, A, B, C, D, s_tab, out);
+            E::template eval<FAR>(e.bpp + ib.z, nb, e.kpp + ik.z, nk, A, B, C, D, s_tab, out);
 #endif
             const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
             const int64_t n = e.nfn;
@@ -834,13 +877,17 @@ __global__ void __launch_bounds__(128, eri_min_blocks(LA, LB, LC, LD)) k_eri(Eri
         atomic_add_ll(&e.counters[C_PRIMQ], nprim);
         atomic_add_ll(&e.counters[C_CLSPQ0 + CLS], nprim);
         atomic_add_ll(&e.counters[C_CLSQ0 + CLS], nq);
+        if (FAR) {
+            atomic_add_ll(&e.counters[C_DBG0 + 0], nq);
+            atomic_add_ll(&e.counters[C_DBG0 + 1], nprim);
+        }
     }
 }
 
 // lower bounds of every 12-bit key value in the sorted key array
 __global__ void k_key_bounds(const uint16_t* keys, int64_t n, int64_t* bounds) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > 4096) return;
+    if (c > KEY_RANGES) return;
     int64_t lo = 0, hi = n;
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
@@ -887,18 +934,23 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-// order-independent digest of the evaluated tuples (the k_log tuples)
+// order-independent digest of the evaluated tuples (the k_log tuples);
+// eightfold: each quartet oriented with (i,j) <= (k,l) (oracle/direct_digest.c)
 __global__ void k_digest(const uint64_t* rec, int64_t n, const int* bpi, const int* bpj, const int* kpi,
-                         const int* kpj, uint64_t ns, int mod, int rem, unsigned long long* dg) {
+                         const int* kpj, uint64_t ns, int mod, int rem, int eight, unsigned long long* dg) {
     unsigned long long c = 0, h1 = 0, h2 = 0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t r = rec[t];
         if (r == SENTINEL_REC) continue;
         const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
-        const uint64_t i = bpi[pb];
+        uint64_t i = bpi[pb], j = bpj[pb], k = kpi[pk], l = kpj[pk];
+        if (eight && (i > k || (i == k && j > l))) {
+            uint64_t x = i; i = k; k = x;
+            x = j; j = l; l = x;
+        }
         if (mod > 1 && (int)(i % (uint64_t)mod) != rem) continue;
-        const uint64_t h = mix64(((i * ns + (uint64_t)bpj[pb]) * ns + (uint64_t)kpi[pk]) * ns + (uint64_t)kpj[pk]);
+        const uint64_t h = mix64(((i * ns + j) * ns + k) * ns + l);
         c += 1;
         h1 += h;
         h2 += mix64(h);
@@ -969,30 +1021,32 @@ T* lalloc(size_t n, cudaStream_t st) {
 }
 
 // persistent grid: every block stages its Boys table once, then strides
-template <int A, int B, int C, int D>
+template <int A, int B, int C, int D, bool FAR>
 void launch_eri(const EriArgs& e, cudaStream_t st) {
-    constexpr int TB = boys_eri_tab_bytes(A + B + C + D);
+    // the far-field kernels need no Boys table
+    constexpr int TB = FAR ? 0 : boys_eri_tab_bytes(A + B + C + D);
     static int per_sm = -1, sms = 0;
     if (per_sm < 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_eri<A, B, C, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri<A, B, C, D>, 128, TB);
+        cudaFuncSetAttribute(k_eri<A, B, C, D, FAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, TB);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eri<A, B, C, D, FAR>, 128, TB);
         if (const char* cap = getenv("HXF_ERI_PERSM")) per_sm = std::min(per_sm, atoi(cap));
         per_sm = std::max(per_sm, 1);
     }
     const int64_t want = e.dbounds ? (int64_t)sms * per_sm : (e.n + 127) / 128;
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
-    k_eri<A, B, C, D><<<g, 128, TB, st>>>(e);
+    k_eri<A, B, C, D, FAR><<<g, 128, TB, st>>>(e);
     note_launch();
 }
 
-void launch_eri_class(int cls, const EriArgs& e, cudaStream_t st) {
+void launch_eri_class(int cls, bool far, const EriArgs& e, cudaStream_t st) {
     if (!e.n && !e.dbounds) return;
     switch (cls) {
 #define C(a, b, c, d) \
-    case (a << 3) | (b << 2) | (c << 1) | d: launch_eri<a, b, c, d>(e, st); break;
+    case (a << 3) | (b << 2) | (c << 1) | d: \
+        if (far) launch_eri<a, b, c, d, true>(e, st); else launch_eri<a, b, c, d, false>(e, st); break;
         C(0, 0, 0, 0) C(0, 0, 0, 1) C(0, 0, 1, 0) C(0, 0, 1, 1)
         C(0, 1, 0, 0) C(0, 1, 0, 1) C(0, 1, 1, 0) C(0, 1, 1, 1)
         C(1, 0, 0, 0) C(1, 0, 0, 1) C(1, 0, 1, 0) C(1, 0, 1, 1)
@@ -1036,12 +1090,13 @@ struct Timer {
 // exit at once)
 void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cudaStream_t st) {
     size_t tb = b.sort_tb;
-    cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, 12, st);
-    { k_key_bounds<<<17, 256, 0, st>>>(b.keys2, nrec, b.dbounds); note_launch(); }
+    HXF_CUDA(cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, KEY_BITS, st));
+    { k_key_bounds<<<KEY_RANGES / 256 + 1, 256, 0, st>>>(b.keys2, nrec, b.dbounds); note_launch(); }
     e.rec = b.rec2;
     e.n = 0;
     e.dbounds = b.dbounds;
-    for (int c = 0; c < 16; ++c) launch_eri_class(c, e, st);
+    for (int c = 0; c < 16; ++c) launch_eri_class(c, false, e, st);
+    for (int c = 0; c < 16; ++c) launch_eri_class(c, true, e, st);
     HXF_CUDA(cudaGetLastError());
 }
 
@@ -1205,6 +1260,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.ncidk = ket->ncid;
     sa.nveck = ket->nvec;
     sa.nveck_tri = ket->nvec_tri;
+    sa.bgeo = bra->geo;
+    sa.kgeo = ket->geo;
+    sa.bgip = bra->gip;
+    sa.kgip = ket->gip;
     sa.ns = s->ns;
     sa.fn = s->basis.fn;
     sa.nf = s->basis.nf;
@@ -1323,10 +1382,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sb[b].keys = lalloc<uint16_t>(cap, st);
             sb[b].keys2 = lalloc<uint16_t>(cap, st);
             sb[b].sort_tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, sb[b].sort_tb, sb[b].keys, sb[b].keys2, sb[b].rec,
-                                            sb[b].rec2, cap, 0, 12, st);
+            HXF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb[b].sort_tb, sb[b].keys, sb[b].keys2, sb[b].rec,
+                                            sb[b].rec2, cap, 0, KEY_BITS, st));
             sb[b].sort_tmp = lalloc<char>(sb[b].sort_tb, st);
-            sb[b].dbounds = lalloc<int64_t>(4097, st);
+            sb[b].dbounds = lalloc<int64_t>(KEY_RANGES + 1, st);
             bfill[b] = b == 0 ? dfill : lalloc<unsigned long long>(1, st);
             bcount[b] = b == 0 ? scount : lalloc<long long>(C_NCOUNTERS, st);
             bledger[b] = b == 0 ? sledger : lalloc<unsigned long long>(LEDGER_LIMBS, st);
@@ -1426,7 +1485,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                 if (want_digest)
                     { k_digest<<<(unsigned)std::min<int64_t>((nrec + 255) / 256, 4096), 256, 0, se>>>(
                           sb[cur].rec2, nrec, bra->pi, bra->pj, ket->pi, ket->pj, (uint64_t)s->ns, o->digest_mod,
-                          o->digest_rem, ddigest); note_launch(); }
+                          o->digest_rem, eight, ddigest); note_launch(); }
                 if (pipe) {
                     HXF_CUDA(cudaEventRecord(ev_eri[cur], se));
                     used[cur] = true;
@@ -1570,6 +1629,11 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         c.class_prim_quartets[k] = acc_c[C_CLSPQ0 + k];
     }
     c.culled_bound_ledger = fx_to_double<LEDGER_LIMBS>(acc_l, LEDGER_SCALE);
+    static const bool eri_stats = getenv("HXF_ERI_STATS") != nullptr;
+    if (eri_stats)
+        fprintf(stderr, "eri: quartets %lld far %lld (%.1f%%), primitive quartets %lld far %lld (%.1f%%)\n",
+                acc_c[C_ERIQ], acc_c[C_DBG0], 100.0 * acc_c[C_DBG0] / std::max(1ll, acc_c[C_ERIQ]),
+                acc_c[C_PRIMQ], acc_c[C_DBG0 + 1], 100.0 * acc_c[C_DBG0 + 1] / std::max(1ll, acc_c[C_PRIMQ]));
 #ifdef HXF_PROF_SCREEN
     fprintf(stderr, "screen cycles (warp-summed): staging %.3e tables %.3e phase1 %.3e phase2 %.3e\n",
             (double)acc_c[C_DBG0], (double)acc_c[C_DBG0 + 1], (double)acc_c[C_DBG0 + 2],
@@ -1742,13 +1806,13 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     int* nq = lalloc<int>(ns, st);
     int* np = lalloc<int>(ns, st);
     size_t tb = 0;
-    cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, fq, skeys, iota, lq, n2, ns, roff, roff + 1, 0, 64, st);
+    HXF_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tb, fq, skeys, iota, lq, n2, ns, roff, roff + 1, 0, 64, st));
     void* stmp = lalloc<char>(tb, st);
     size_t tb2 = tb;
-    cub::DeviceSegmentedRadixSort::SortPairsDescending(stmp, tb2, fq, skeys, iota, lq, n2, ns, roff, roff + 1, 0, 64, st);
+    HXF_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(stmp, tb2, fq, skeys, iota, lq, n2, ns, roff, roff + 1, 0, 64, st));
     { k_row_nnz<<<(ns + 255) / 256, 256, 0, st>>>(skeys, ns, nq); note_launch(); }
     tb2 = tb;
-    cub::DeviceSegmentedRadixSort::SortPairsDescending(stmp, tb2, dens->pmax, skeys, iota, lp, n2, ns, roff, roff + 1, 0, 64, st);
+    HXF_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(stmp, tb2, dens->pmax, skeys, iota, lp, n2, ns, roff, roff + 1, 0, 64, st));
     { k_row_nnz<<<(ns + 255) / 256, 256, 0, st>>>(skeys, ns, np); note_launch(); }
     HXF_CUDA(cudaGetLastError());
     for (void* p : {(void*)stmp, (void*)skeys, (void*)iota, (void*)roff}) hxf_cache_free(p, st);
@@ -1783,9 +1847,9 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     const unsigned grid_all = (unsigned)((npr * 32 + 255) / 256);
     if (npr) { k_direct<false><<<grid_all, 256, 0, st>>>(da, 0, npr); note_launch(); }
     size_t stb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, stb, cnt, off, npr + 1, st);
+    HXF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, stb, cnt, off, npr + 1, st));
     void* scan_tmp = lalloc<char>(stb, st);
-    cub::DeviceScan::ExclusiveSum(scan_tmp, stb, cnt, off, npr + 1, st);
+    HXF_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, stb, cnt, off, npr + 1, st));
     std::vector<int64_t> hoff(npr + 1);
     HXF_CUDA(cudaMemcpyAsync(hoff.data(), off, (npr + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaStreamSynchronize(st));
@@ -1817,9 +1881,9 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         sb.keys = lalloc<uint16_t>(cap, st);
         sb.keys2 = lalloc<uint16_t>(cap, st);
         sb.sort_tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, sb.sort_tb, sb.keys, sb.keys2, sb.rec, sb.rec2, cap, 0, 12, st);
+        HXF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb.sort_tb, sb.keys, sb.keys2, sb.rec, sb.rec2, cap, 0, KEY_BITS, st));
         sb.sort_tmp = lalloc<char>(sb.sort_tb, st);
-        sb.dbounds = lalloc<int64_t>(4097, st);
+        sb.dbounds = lalloc<int64_t>(KEY_RANGES + 1, st);
         EriArgs e;
         e.dbounds = nullptr;
         e.bpi = e.kpi = pairs->pi;
@@ -1851,7 +1915,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
                 eri_sorted_stage_async(e, sb, nrec, st);
                 if (want_digest)
                     { k_digest<<<(unsigned)std::min<int64_t>((nrec + 255) / 256, 4096), 256, 0, st>>>(
-                          sb.rec2, nrec, pairs->pi, pairs->pj, pairs->pi, pairs->pj, (uint64_t)ns, mod, rem,
+                          sb.rec2, nrec, pairs->pi, pairs->pj, pairs->pi, pairs->pj, (uint64_t)ns, mod, rem, 0,
                           ddigest); note_launch(); }
                 HXF_CUDA(cudaStreamSynchronize(st));
                 g_timings[2] += teri.stop();

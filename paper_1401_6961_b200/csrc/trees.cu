@@ -126,7 +126,7 @@ __global__ void k_fill_pairs(DevBasis B, const double* smax, double tau, const i
                     q.x = __ddiv_rn(__dadd_rn(__dmul_rn(ea, A.x), __dmul_rn(eb, C.x)), p);
                     q.y = __ddiv_rn(__dadd_rn(__dmul_rn(ea, A.y), __dmul_rn(eb, C.y)), p);
                     q.z = __ddiv_rn(__dadd_rn(__dmul_rn(ea, A.z), __dmul_rn(eb, C.z)), p);
-                    q.pad0 = 0.0;
+                    q.cs = q.c * sqrt(q.ip);
                     q.pad1 = 0.0;
                     pp[po] = q;
                 }
@@ -138,7 +138,7 @@ template <int LA, int LB>
 __device__ double diag_q(const PrimPair* pp, int64_t b0, int64_t b1, double3 A, double3 Bc) {
     typedef Eri<LA, LB, LA, LB> E;
     double out[E::NI * E::NJ * E::NK * E::NL];
-    E::eval(pp, (int)(b1 - b0), pp, (int)(b1 - b0), A, Bc, A, Bc, boys_table_global(E::L), out);
+    E::template eval<false>(pp, (int)(b1 - b0), pp, (int)(b1 - b0), A, Bc, A, Bc, boys_table_global(E::L), out);
     double q = 0.0;
     for (int x = 0; x < E::NI; ++x)
         for (int y = 0; y < E::NJ; ++y) q = fmax(q, out[((x * E::NJ + y) * E::NK + x) * E::NL + y]);
@@ -207,6 +207,34 @@ __global__ void k_prim_schwarz_sort(DevBasis B, int64_t n_pairs, const int* pi, 
         epp[b0 + u] = pp[b0 + idx[u]];
         eS[b0 + u] = sv[u];
     }
+}
+
+// Far-field geometry per pair (the ERI stage's per-quartet asymptotic test,
+// leaf.cu): centroid c of the primitive centres, radius r with every centre
+// within r of c, and ip = max 1/p, all as floats rounded outward (r and ip up,
+// r also absorbs the centroid's float rounding), so that for any primitive
+// pair b of a bra pair and k of a ket pair |P_b - Q_k| >= |c_B - c_K| - r_B - r_K
+// and 1/p_b + 1/q_k <= ip_B + ip_K.
+__global__ void k_pair_geo(int64_t n_pairs, const int64_t* ppoff, const PrimPair* pp, float4* geo, float* gip) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_pairs) return;
+    const int64_t b0 = ppoff[t], b1 = ppoff[t + 1];
+    double cx = 0.0, cy = 0.0, cz = 0.0, ip = 0.0;
+    for (int64_t u = b0; u < b1; ++u) {
+        cx += pp[u].x;
+        cy += pp[u].y;
+        cz += pp[u].z;
+        ip = fmax(ip, pp[u].ip);
+    }
+    const double inv = 1.0 / (double)(b1 - b0);
+    const float fx = (float)(cx * inv), fy = (float)(cy * inv), fz = (float)(cz * inv);
+    double r = 0.0;
+    for (int64_t u = b0; u < b1; ++u) {
+        const double dx = pp[u].x - fx, dy = pp[u].y - fy, dz = pp[u].z - fz;
+        r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz));
+    }
+    geo[t] = make_float4(fx, fy, fz, __double2float_ru(r * (1.0 + 1e-6) + 1e-4));
+    gip[t] = __double2float_ru(ip * (1.0 + 1e-6));
 }
 
 // per pair: sqrt(Q) once (screening uses it for every quartet) and the class /
@@ -509,11 +537,11 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     { k_leaf_pair_counts<<<nblk(nl2), 256, 0, st>>>(lsmax, pr->tau_ovlp, lt.lslo, lt.lshi, lt.lplo,
                                                   lt.lphi, nl, npairs, nprims); note_launch(); }
     size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, npairs, pbase, nl2 + 1, st);
+    HXF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, npairs, pbase, nl2 + 1, st));
     void* tbuf = dalloc<char>(tb, st);
     tmp.push_back(tbuf);
-    cub::DeviceScan::ExclusiveSum(tbuf, tb, npairs, pbase, nl2 + 1, st);
-    cub::DeviceScan::ExclusiveSum(tbuf, tb, nprims, ppbase, nl2 + 1, st);
+    HXF_CUDA(cub::DeviceScan::ExclusiveSum(tbuf, tb, npairs, pbase, nl2 + 1, st));
+    HXF_CUDA(cub::DeviceScan::ExclusiveSum(tbuf, tb, nprims, ppbase, nl2 + 1, st));
     int64_t tot[2];
     HXF_CUDA(cudaMemcpyAsync(&tot[0], pbase + nl2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaMemcpyAsync(&tot[1], ppbase + nl2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -543,6 +571,12 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     pr->eS = dalloc<double>(pr->n_prim_pairs, st);
     { k_prim_schwarz_sort<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
                                                                  pr->pp, pr->epp, pr->eS); note_launch(); }
+    pr->geo = dalloc<float4>(std::max<int64_t>(pr->n_pairs, 1), st);
+    pr->gip = dalloc<float>(std::max<int64_t>(pr->n_pairs, 1), st);
+    if (pr->n_pairs) {
+        k_pair_geo<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(pr->n_pairs, pr->ppoff, pr->pp, pr->geo, pr->gip);
+        note_launch();
+    }
     unsigned long long* dsmax = dalloc<unsigned long long>(1, st);
     tmp.push_back(dsmax);
     HXF_CUDA(cudaMemsetAsync(dsmax, 0, sizeof(unsigned long long), st));
@@ -560,10 +594,10 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
         { k_live_flags<<<nblk(nl2), 256, 0, st>>>(pr->leaf_base, nl2, flag); note_launch(); }
         pr->ncid = dalloc<int>(nl2 + 1, st);
         size_t tb2 = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag, pr->ncid, nl2 + 1, st);
+        HXF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag, pr->ncid, nl2 + 1, st));
         void* tbuf2 = dalloc<char>(tb2, st);
         tmp.push_back(tbuf2);
-        cub::DeviceScan::ExclusiveSum(tbuf2, tb2, flag, pr->ncid, nl2 + 1, st);
+        HXF_CUDA(cub::DeviceScan::ExclusiveSum(tbuf2, tb2, flag, pr->ncid, nl2 + 1, st));
         int nlive = 0;
         HXF_CUDA(cudaMemcpyAsync(&nlive, pr->ncid + nl2, sizeof(int), cudaMemcpyDeviceToHost, st));
         HXF_CUDA(cudaStreamSynchronize(st));
