@@ -5,8 +5,8 @@ Drop-in for the reference package's exchange path: the same entry points
 build_exchange_symmetric) backed by libhxf.so (hand-written sm_100a CUDA).
 """
 
-from .basis import (Atom, BasisSystem, DensityModel, GaussianShell, InvalidArgumentError,
-                    SplitMix64, build_density, generate_cluster, hilbert_order)
+from .basis import Atom, BasisSystem, GaussianShell, InvalidArgumentError, assign_offsets
+from .inputs import DensityModel, SplitMix64, build_density, generate_cluster, hilbert_order
 from ._native import LogicError, release_scratch
 from .prep import hilbert_order_device
 from .exchange import (CASE_LABELS, SymmetryCase, SymmetryCounters, TraversalCounters,

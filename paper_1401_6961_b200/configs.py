@@ -23,8 +23,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .basis import (BOHR_PER_ANGSTROM, Atom, BasisSystem, GaussianShell, SplitMix64,
-                    assign_offsets, hilbert_order)
+from .basis import BOHR_PER_ANGSTROM, Atom, BasisSystem, GaussianShell, assign_offsets
+from .inputs import SplitMix64, hilbert_order
 
 LIGHT_S3 = [(3.42525, 0.15433), (0.62391, 0.53533), (0.16886, 0.44463)]
 HEAVY_S3 = [(5.0, 0.15433), (1.2, 0.53533), (0.35, 0.44463)]

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from conftest import ROOT, has_cuda
-from paper_1401_6961_b200 import _native
+from paper_1401_6961_b200 import _native, basis, inputs
 from paper_1401_6961_b200.basis import InvalidArgumentError
 
 HEADER = os.path.join(ROOT, "include", "hxf.h")
@@ -59,7 +59,7 @@ def test_version():
 @pytest.mark.skipif(has_cuda(), reason="checks the no-device path")
 def test_no_device_fails_loudly():
     from paper_1401_6961_b200 import basis, quadtree
-    system = basis.generate_cluster(1, seed=3)
+    system = inputs.generate_cluster(1, seed=3)
     part = quadtree.build_partition(system)
     with pytest.raises(RuntimeError, match="no CUDA device"):
         quadtree.build_pair_tree(system, part)

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from conftest import has_cuda, load_golden
-from paper_1401_6961_b200 import _native, basis, prep, quadtree
+from paper_1401_6961_b200 import _native, basis, inputs, prep, quadtree
 from paper_1401_6961_b200.basis import InvalidArgumentError
 
 
@@ -26,14 +26,14 @@ def _host_keys(centers, bits):
     for ax in range(3):
         if extent[ax] > 0.0:
             lattice[:, ax] = np.rint((centers[:, ax] - lo[ax]) / extent[ax] * side)
-    keys = np.array([basis.hilbert_index_3d(pt, bits) for pt in lattice], dtype=np.uint64)
+    keys = inputs.hilbert_keys(lattice, bits).astype(np.uint64)
     perm = np.argsort(keys, kind="stable")
     return keys[perm], perm
 
 
 @pytest.mark.parametrize("bits", [0, 21, -3])
 def test_bad_bits_rejected(bits):
-    s = basis.generate_cluster(2, seed=1)
+    s = inputs.generate_cluster(2, seed=1)
     with pytest.raises(InvalidArgumentError, match="bits_per_axis"):
         prep.hilbert_order_device(s, bits)
     with pytest.raises(InvalidArgumentError, match="bits_per_axis"):
@@ -54,8 +54,8 @@ def test_no_device_fails_loudly():
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,seed", [(1, 3), (3, 3), (10, 5), (64, 11)])
 def test_cluster_perm_matches_host(n, seed):
-    s = basis.generate_cluster(n, seed=seed)
-    s_h, p_h = basis.hilbert_order(s)
+    s = inputs.generate_cluster(n, seed=seed)
+    s_h, p_h = inputs.hilbert_order(s)
     s_d, p_d = prep.hilbert_order_device(s)
     assert np.array_equal(p_h, p_d)
     assert [sh.function_offset for sh in s_h.shells] == [sh.function_offset for sh in s_d.shells]
@@ -67,7 +67,7 @@ def test_cluster_perm_matches_host(n, seed):
 def test_golden_perms():
     g = load_golden("integrals")
     for k in range(3):
-        s = basis.generate_cluster(int(g[f"geo{k}_n"]), seed=int(g[f"geo{k}_seed"]))
+        s = inputs.generate_cluster(int(g[f"geo{k}_n"]), seed=int(g[f"geo{k}_seed"]))
         _, perm = prep.hilbert_order_device(s)
         assert np.array_equal(perm, g[f"geo{k}_perm"])
 
@@ -173,7 +173,7 @@ def test_partition_ties_and_small_cases():
 
 @pytest.mark.gpu
 def test_partition_cluster_and_c5_size():
-    s, _ = basis.hilbert_order(basis.generate_cluster(40, seed=7))
+    s, _ = inputs.hilbert_order(inputs.generate_cluster(40, seed=7))
     assert _tree(prep.build_partition_device(s).root) == _tree(quadtree.build_partition(s).root)
     sizes = [1, 1, 1, 3, 3] * 4096   # 20480 shells, 28672 functions (config 5's basis mix)
     s = _system_of_sizes(sizes)

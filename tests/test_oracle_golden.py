@@ -11,7 +11,7 @@ import pytest
 
 from conftest import (CASES, counters_vec, quartet_bits, system_from_arrays, tree_walk)
 from oracle import hexfock_oracle as ho
-from paper_1401_6961_b200 import basis, configs
+from paper_1401_6961_b200 import basis, configs, inputs
 
 FIXTURES = ["cluster1", "cluster3", "cluster5", "cluster10", "ragged0", "ragged1",
             "ragged2", "ragged3", "identity3", "c1"]
@@ -108,9 +108,9 @@ def test_overlap_pins(golden):
 def test_generator_and_hilbert_match_reference(golden):
     g = golden("integrals")
     for k in range(3):
-        s = basis.generate_cluster(int(g[f"geo{k}_n"]), seed=int(g[f"geo{k}_seed"]))
+        s = inputs.generate_cluster(int(g[f"geo{k}_n"]), seed=int(g[f"geo{k}_seed"]))
         assert np.array_equal(np.array([sh.center for sh in s.shells]), g[f"geo{k}_centers"])
-        _, perm = basis.hilbert_order(s)
+        _, perm = inputs.hilbert_order(s)
         assert np.array_equal(perm, g[f"geo{k}_perm"])
 
 
@@ -127,7 +127,7 @@ def test_case_label_table_matches():
 
 
 def test_splitmix_block_matches_sequential():
-    rng = basis.SplitMix64(12345)
+    rng = inputs.SplitMix64(12345)
     seq = [rng.next_u64() for _ in range(50)]
     blk = configs.splitmix64_block(12345, 0, 50)
     assert [int(x) for x in blk] == seq

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from oracle import hexfock_oracle as ho
-from paper_1401_6961_b200 import basis, configs
+from paper_1401_6961_b200 import basis, configs, inputs
 
 
 def _shell(rng, l, center=None):
@@ -135,6 +135,6 @@ def test_p_direct_scf_set_identity():
 
 def test_hilbert_order_keeps_l():
     system, _ = _small_p_system(2)
-    s2, _ = basis.hilbert_order(system)
+    s2, _ = inputs.hilbert_order(system)
     assert sorted(sh.l for sh in s2.shells) == sorted(sh.l for sh in system.shells)
     assert s2.n_functions == system.n_functions

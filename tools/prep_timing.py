@@ -1,7 +1,7 @@
 """Host vs device Hilbert reordering on BASELINE config 5's system.
 
 python tools/prep_timing.py [out.json]: generates a 4096-molecule water-like
-cluster (16384 shells), times basis.hilbert_order (host pre-pass, reference
+cluster (16384 shells), times inputs.hilbert_order (host pre-pass, reference
 basis.py:309-331) once and prep.hilbert_keys_and_perm (device, host buffers in
 and out) over 20 calls after warm-up, checks the permutations are equal; then the
 same for the partition build (quadtree.py:90-113; device time includes the Span
@@ -16,15 +16,15 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_1401_6961_b200 import basis, prep, quadtree  # noqa: E402
+from paper_1401_6961_b200 import basis, inputs, prep, quadtree  # noqa: E402
 
 
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else None
-    s = basis.generate_cluster(4096, seed=5)
+    s = inputs.generate_cluster(4096, seed=5)
     c = np.array([sh.center for sh in s.shells])
     t0 = time.perf_counter()
-    _, p_h = basis.hilbert_order(s)
+    _, p_h = inputs.hilbert_order(s)
     host_s = time.perf_counter() - t0
     for _ in range(3):
         prep.hilbert_keys_and_perm(c, 10)
@@ -37,7 +37,7 @@ def main():
            "device_hilbert_order_s": dev_s, "speedup": host_s / dev_s,
            "perm_equal": bool(np.array_equal(p_h, p_d)),
            "note": "device time includes the H2D of the centres and D2H of the permutation"}
-    s2, _ = basis.hilbert_order(s)
+    s2, _ = inputs.hilbert_order(s)
     t0 = time.perf_counter()
     ph = quadtree.build_partition(s2, 10)
     rec["host_build_partition_s"] = time.perf_counter() - t0
