@@ -77,25 +77,17 @@ struct ScreenArgs {
     const int* ncidk;
     const double* nveck;
     const double* nveck_tri;
-    const float4* bgeo;       // far-field test per emitted quartet (k_pair_geo, trees.cu)
-    const float4* kgeo;
-    const float* bgip;
-    const float* kgip;
+    const float4* bngeo;      // far-field test per leaf task (k_node_geo, trees.cu)
+    const float4* kngeo;
+    const float* bngip;
+    const float* kngip;
 };
 
-// Far field: every primitive quartet of the shell quartet (bra pair pb, ket pair
-// pk) has Boys argument T = |P-Q|^2 / (1/p + 1/q) >= boys_far_t(L), from the
-// conservative per-pair centroid / radius / max 1/p (k_pair_geo).  Such quartets
-// sort into their own ERI range (key bit 12) whose kernels evaluate only the
-// asymptotic Boys branch -- the values the table path selects there.
-__device__ __forceinline__ bool quartet_far(const float4* bgeo, const float* bgip, const float4* kgeo,
-                                            const float* kgip, int64_t pb, int64_t pk, int L) {
-    const float4 gb = __ldg(bgeo + pb), gk = __ldg(kgeo + pk);
-    const float ip = __ldg(bgip + pb) + __ldg(kgip + pk);
-    const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
-    const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
-    return d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip;
-}
+// Far field (ERI key bit 12): every primitive quartet of a shell quartet has
+// Boys argument T = |P-Q|^2 / (1/p + 1/q) >= boys_far_t(L); decided per leaf
+// task from the nodes' enclosing spheres (k_node_geo).  Such quartets sort into
+// their own ERI range whose kernels evaluate only the asymptotic Boys branch --
+// the values the table path selects there.
 #define KEY_FAR 0x1000
 #define KEY_BITS 13
 #define KEY_RANGES (1 << KEY_BITS)
@@ -397,32 +389,61 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         // count whole blocks, so such tasks take the per-quartet path throughout
         const bool diag8 = EIGHT && mu == lam && nu == sig;
         const float inv_nnu = c_inv[nnu], inv_nsig = c_inv[nsig], inv_nlam = c_inv[nlam];
-        // ---- stage density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
+        // ---- stage density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig],
+        // and the node vectors of the bra and ket leaf nodes (row / column max f, sums of s).
+        // Every load of the task is issued before the first use (one memory latency per
+        // task instead of one per loop trip).
         const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
         const int cs[4] = {slam, slam, ssig, ssig}, cn[4] = {nlam, nlam, nsig, nsig};
-#pragma unroll
-        for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
-            if (!((live >> g) & 1)) continue;
-            const float inv = c_inv[cn[g]];
-#pragma unroll 1
-            for (int i = lane; i < rn[g] * cn[g]; i += 32) {
-                const int x = fdiv(i, cn[g], inv), y = i - x * cn[g];
-                sm.pm[g][i] = a.pmax[(int64_t)(rs[g] + x) * a.ns + cs[g] + y];
-            }
-        }
-        // ---- node vectors of the bra and ket leaf nodes (row / column max f, sums of s)
         {
+            constexpr int NG = Smem2<SYM, MS>::NG, NIT = (MS * MS + 31) / 32, NVI = (8 * MS + 31) / 32;
+            double vp[NG][NIT], vn[NVI];
             const double* vb = bdiag ? a.nvecb_tri + (int64_t)mu * NVEC
                                      : a.nvecb + (int64_t)a.ncidb[(int64_t)mu * a.nleaf + nu] * NVEC;
             const double* vk = kdiag ? a.nveck_tri + (int64_t)lam * NVEC
                                      : a.nveck + (int64_t)a.ncidk[(int64_t)lam * a.nleaf + sig] * NVEC;
-#pragma unroll 1
-            for (int i = lane; i < 8 * MS; i += 32) {
-                const int h = i < 4 * MS ? i : i - 4 * MS;
-                const int o = h / MS, r = h - o * MS;
-                double v = __ldg((i < 4 * MS ? vb : vk) + o * NV_MAXS + r);
-                if (schwarz && o < 2) v = sqrt(v);   // max sqrt(Q) = sqrt(max Q) (monotone, correctly rounded)
-                (i < 4 * MS ? sm.nvb : sm.nvk)[h] = v;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                const bool lg = (live >> g) & 1;
+                const float inv = c_inv[cn[g]];
+#pragma unroll
+                for (int u = 0; u < NIT; ++u) {
+                    const int i = lane + 32 * u;
+                    vp[g][u] = 0.0;
+                    if (lg && i < rn[g] * cn[g]) {
+                        const int x = fdiv(i, cn[g], inv), y = i - x * cn[g];
+                        vp[g][u] = __ldg(a.pmax + (int64_t)(rs[g] + x) * a.ns + cs[g] + y);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NVI; ++u) {
+                const int i = lane + 32 * u;
+                vn[u] = 0.0;
+                if (i < 8 * MS) {
+                    const int h = i < 4 * MS ? i : i - 4 * MS;
+                    const int o = h / MS, r = h - o * MS;
+                    vn[u] = __ldg((i < 4 * MS ? vb : vk) + o * NV_MAXS + r);
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+#pragma unroll
+                for (int u = 0; u < NIT; ++u) {
+                    const int i = lane + 32 * u;
+                    if (((live >> g) & 1) && i < rn[g] * cn[g]) sm.pm[g][i] = vp[g][u];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NVI; ++u) {
+                const int i = lane + 32 * u;
+                if (i < 8 * MS) {
+                    const int h = i < 4 * MS ? i : i - 4 * MS;
+                    const int o = h / MS;
+                    double v = vn[u];
+                    if (schwarz && o < 2) v = sqrt(v);   // max sqrt(Q) = sqrt(max Q) (monotone, correctly rounded)
+                    (i < 4 * MS ? sm.nvb : sm.nvk)[h] = v;
+                }
             }
         }
         __syncwarp();
@@ -457,34 +478,66 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                 continue;
             }
         }
-        // ---- stage pair factors
-#pragma unroll 1
-        for (int i = lane; i < ma; i += 32) {
-            int x, y;
-            if (bdiag) tri_decode(i, nmu, &x, &y);
-            else { x = fdiv(i, nnu, inv_nnu); y = i - x * nnu; }
-            const int64_t pid = bb + x * nnu + y;
-            const double sq = a.sqb[pid];
-            sm.sa[i] = sq;
-            sm.fa[i] = schwarz ? sq : a.qb[pid];
-            sm.ax[i] = x;
-            sm.ay[i] = y;
-            sm.apl[i] = x * nnu + y;
-            sm.acl[i] = a.metab[pid];
+        // ---- task-level far field (ERI key bit 12): the enclosing spheres of the
+        // bra and ket leaf nodes (k_node_geo) are separated enough for every
+        // primitive quartet of the task: far0 for (ss|ss), far1 for the p classes
+        bool far0 = false, far1 = false;
+        if (!HXF_ERI_NOFAR) {
+            const int cb_ = a.ncidb[(int64_t)mu * a.nleaf + nu], ck_ = a.ncidk[(int64_t)lam * a.nleaf + sig];
+            const float4 gb = __ldg(a.bngeo + cb_), gk = __ldg(a.kngeo + ck_);
+            const float ip = __ldg(a.bngip + cb_) + __ldg(a.kngip + ck_);
+            const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
+            const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
+            far0 = d > 0.0f && d * d >= (float)(boys_far_t(0) * 1.0001) * ip;
+            far1 = d > 0.0f && d * d >= (float)(boys_far_t(1) * 1.0001) * ip;
         }
-#pragma unroll 1
-        for (int i = lane; i < mb; i += 32) {
-            int x, y;
-            if (kdiag) tri_decode(i, nlam, &x, &y);
-            else { x = fdiv(i, nsig, inv_nsig); y = i - x * nsig; }
-            const int64_t pid = kb + x * nsig + y;
-            const double sq = a.sqk[pid];
-            sm.sb[i] = sq;
-            sm.fb[i] = schwarz ? sq : a.qk[pid];
-            sm.bx[i] = x;
-            sm.by[i] = y;
-            sm.bpl[i] = x * nsig + y;
-            sm.bcl[i] = a.metak[pid];
+        // ---- stage pair factors (all loads first)
+        {
+            constexpr int NIT = (MS * MS + 31) / 32;
+            double sqa[NIT], qa[NIT], sqk[NIT], qk[NIT];
+            int mta[NIT], mtk[NIT], xa[NIT], ya[NIT], xk[NIT], yk[NIT];
+#pragma unroll
+            for (int u = 0; u < NIT; ++u) {
+                const int i = lane + 32 * u;
+                sqa[u] = qa[u] = sqk[u] = qk[u] = 0.0;
+                mta[u] = mtk[u] = xa[u] = ya[u] = xk[u] = yk[u] = 0;
+                if (i < ma) {
+                    if (bdiag) tri_decode(i, nmu, &xa[u], &ya[u]);
+                    else { xa[u] = fdiv(i, nnu, inv_nnu); ya[u] = i - xa[u] * nnu; }
+                    const int64_t pid = bb + xa[u] * nnu + ya[u];
+                    sqa[u] = __ldg(a.sqb + pid);
+                    if (!schwarz) qa[u] = __ldg(a.qb + pid);
+                    mta[u] = __ldg(a.metab + pid);
+                }
+                if (i < mb) {
+                    if (kdiag) tri_decode(i, nlam, &xk[u], &yk[u]);
+                    else { xk[u] = fdiv(i, nsig, inv_nsig); yk[u] = i - xk[u] * nsig; }
+                    const int64_t pid = kb + xk[u] * nsig + yk[u];
+                    sqk[u] = __ldg(a.sqk + pid);
+                    if (!schwarz) qk[u] = __ldg(a.qk + pid);
+                    mtk[u] = __ldg(a.metak + pid);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NIT; ++u) {
+                const int i = lane + 32 * u;
+                if (i < ma) {
+                    sm.sa[i] = sqa[u];
+                    sm.fa[i] = schwarz ? sqa[u] : qa[u];
+                    sm.ax[i] = xa[u];
+                    sm.ay[i] = ya[u];
+                    sm.apl[i] = xa[u] * nnu + ya[u];
+                    sm.acl[i] = mta[u];
+                }
+                if (i < mb) {
+                    sm.sb[i] = sqk[u];
+                    sm.fb[i] = schwarz ? sqk[u] : qk[u];
+                    sm.bx[i] = xk[u];
+                    sm.by[i] = yk[u];
+                    sm.bpl[i] = xk[u] * nsig + yk[u];
+                    sm.bcl[i] = mtk[u];
+                }
+            }
         }
         // ket rows: L_k = ket pairs with row shell k (contiguous in the pair order);
         // max f and sum s over L_k are the ket node's row vectors
@@ -632,9 +685,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                         const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
                         // bit 60: eightfold self-mirror quartet (bra pair == ket pair), weight 1/2
                         const uint64_t selfm = (EIGHT && pb == pk) ? 1ull : 0ull;
-                        const int L = __popc(ca & 3) + __popc(cb & 3);
-                        const bool far = keep_any && !HXF_ERI_NOFAR &&
-                                         quartet_far(a.bgeo, a.bgip, a.kgeo, a.kgip, (int64_t)pb, (int64_t)pk, L);
+                        const bool far = (ca & 3) == 0 && (cb & 3) == 0 ? far0 : far1;
                         slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56) | (selfm << 60),
                                   (uint16_t)((far ? KEY_FAR : 0) | (cls << 8) | ((ca >> 2) << 4) | (cb >> 2)),
                                   lane);
@@ -884,6 +935,28 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
     }
 }
 
+// Per-quartet far-field test over one chunk of survivor records, before the
+// sort: sets key bit 12 for the quartets the screen's task-level test left
+// near.  A streaming pass (8 + 2 bytes per record; the per-pair spheres are
+// gathered with the locality of the screen's task order) instead of the same
+// test inside the screen's emission path, where it cost 11 % of the screen.
+__global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __restrict__ keys, int64_t n,
+                               const float4* __restrict__ bgeo, const float* __restrict__ bgip,
+                               const float4* __restrict__ kgeo, const float* __restrict__ kgip) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint16_t key = keys[t];
+        if (key == SENTINEL_KEY || (key & KEY_FAR)) continue;
+        const uint64_t r = rec[t];
+        const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
+        const int L = __popc((key >> 8) & 15);
+        const float4 gb = __ldg(bgeo + pb), gk = __ldg(kgeo + pk);
+        const float ip = __ldg(bgip + pb) + __ldg(kgip + pk);
+        const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
+        const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
+        if (d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip) keys[t] = key | KEY_FAR;
+    }
+}
+
 // lower bounds of every 12-bit key value in the sorted key array
 __global__ void k_key_bounds(const uint16_t* keys, int64_t n, int64_t* bounds) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1063,6 +1136,11 @@ struct SurvivorBufs {
     void* sort_tmp;
     size_t sort_tb;
     int64_t* dbounds;
+    // per-pair spheres for the per-quartet far-field pass (NULL: skip it)
+    const float4* bgeo = nullptr;
+    const float4* kgeo = nullptr;
+    const float* bgip = nullptr;
+    const float* kgip = nullptr;
 };
 
 struct Timer {
@@ -1089,6 +1167,14 @@ struct Timer {
 // kernel reads its record range from the device-side key bounds (empty classes
 // exit at once)
 void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cudaStream_t st) {
+    if (b.bgeo && !HXF_ERI_NOFAR) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrec + 255) / 256, (int64_t)sms * 8));
+        k_classify_far<<<g, 256, 0, st>>>(b.rec, b.keys, nrec, b.bgeo, b.bgip, b.kgeo, b.kgip);
+        note_launch();
+    }
     size_t tb = b.sort_tb;
     HXF_CUDA(cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, KEY_BITS, st));
     { k_key_bounds<<<KEY_RANGES / 256 + 1, 256, 0, st>>>(b.keys2, nrec, b.dbounds); note_launch(); }
@@ -1260,10 +1346,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.ncidk = ket->ncid;
     sa.nveck = ket->nvec;
     sa.nveck_tri = ket->nvec_tri;
-    sa.bgeo = bra->geo;
-    sa.kgeo = ket->geo;
-    sa.bgip = bra->gip;
-    sa.kgip = ket->gip;
+    sa.bngeo = bra->ngeo;
+    sa.kngeo = ket->ngeo;
+    sa.bngip = bra->ngip;
+    sa.kngip = ket->ngip;
     sa.ns = s->ns;
     sa.fn = s->basis.fn;
     sa.nf = s->basis.nf;
@@ -1386,6 +1472,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                                             sb[b].rec2, cap, 0, KEY_BITS, st));
             sb[b].sort_tmp = lalloc<char>(sb[b].sort_tb, st);
             sb[b].dbounds = lalloc<int64_t>(KEY_RANGES + 1, st);
+            sb[b].bgeo = bra->geo;
+            sb[b].kgeo = ket->geo;
+            sb[b].bgip = bra->gip;
+            sb[b].kgip = ket->gip;
             bfill[b] = b == 0 ? dfill : lalloc<unsigned long long>(1, st);
             bcount[b] = b == 0 ? scount : lalloc<long long>(C_NCOUNTERS, st);
             bledger[b] = b == 0 ? sledger : lalloc<unsigned long long>(LEDGER_LIMBS, st);
