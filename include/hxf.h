@@ -114,6 +114,14 @@ typedef struct hxf_exchange_opts {
        stride fields are then ignored except that work above the cut is counted
        only when shard_begin == 0 */
     const uint8_t* shard_mask;
+    /* Start node of the traversal: the diagonal node (root_index, root_index) of
+       partition level root_level (0, 0 = the tree root).  The reference's drivers
+       accept any node with bra.row is bra.col is ket.row ... is P.col
+       (exchange_naive.py:105-108 _check_same_partition); K_out is then the
+       n_S x n_S block of that span's functions (n_S = its function count, local
+       indices fn - fn_lo).  K_fixed requires the tree root. */
+    int root_level;
+    int root_index;
 } hxf_exchange_opts;
 
 const char* hxf_last_error(void);
@@ -132,6 +140,13 @@ void hxf_system_destroy(hxf_system* sys);
 int hxf_system_info(const hxf_system* sys, int64_t* n_functions, int64_t* n_leaves);
 
 int hxf_pairs_build(hxf_system* sys, double tau_ovlp, void* stream, hxf_pairs** out);
+/* build_pair_tree(..., overlap_matrix=S) (quadtree.py:284-293): pruning from the
+ * caller's |S| (n_shells x n_shells row-major, float64, absolute values; host or
+ * device per on_device) instead of the computed overlaps: a node is pruned iff
+ * max |S| over its (row span, column span) block < tau_ovlp.  S is not assumed
+ * symmetric.  Q, the primitive tables and the ERIs are unchanged. */
+int hxf_pairs_build_ovlp(hxf_system* sys, double tau_ovlp, const double* s_abs, int on_device,
+                         void* stream, hxf_pairs** out);
 void hxf_pairs_destroy(hxf_pairs* pairs);
 /* node arrays of one level (n_spans(level)^2 entries, row-major (r, c)):
  * diag_norm, rowsum_max, colsum_max, pruned flag (1 = pruned). */

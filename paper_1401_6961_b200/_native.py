@@ -20,7 +20,7 @@ HXF_OK, HXF_EINVAL, HXF_ELOGIC, HXF_ECUDA, HXF_ENOMEM = 0, 1, 2, 3, 4
 NCASES = 9
 
 EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_destroy",
-            "hxf_system_info", "hxf_pairs_build", "hxf_pairs_destroy", "hxf_pairs_download",
+            "hxf_system_info", "hxf_pairs_build", "hxf_pairs_build_ovlp", "hxf_pairs_destroy", "hxf_pairs_download",
             "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
             "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_exchange_direct", "hxf_frontier",
             "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count",
@@ -73,7 +73,9 @@ class ExchangeOpts(ctypes.Structure):
                 ("K_fixed", ctypes.c_int),
                 ("K_scale", ctypes.POINTER(ctypes.c_int)),
                 ("shard_stride", ctypes.c_int64),
-                ("shard_mask", ctypes.POINTER(ctypes.c_uint8))]
+                ("shard_mask", ctypes.POINTER(ctypes.c_uint8)),
+                ("root_level", ctypes.c_int),
+                ("root_index", ctypes.c_int)]
 
 
 _lib = None
@@ -97,6 +99,7 @@ def lib():
     L.hxf_system_destroy.restype = None
     L.hxf_system_info.argtypes = [vp, P(i64), P(i64)]
     L.hxf_pairs_build.argtypes = [vp, dbl, vp, P(vp)]
+    L.hxf_pairs_build_ovlp.argtypes = [vp, dbl, vp, i32, vp, P(vp)]
     L.hxf_pairs_destroy.argtypes = [vp]
     L.hxf_pairs_destroy.restype = None
     L.hxf_pairs_download.argtypes = [vp, i32, vp, vp, vp, vp]

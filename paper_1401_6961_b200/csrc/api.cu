@@ -210,8 +210,6 @@ int hxf_system_create(int device, int ns, const double* centers, const int* l, c
         for (int k = s->h_off[D]; k < s->h_off[D + 1]; ++k) {
             s->h_leaf_id[k] = k - s->h_off[D];
             s->max_leaf_shells = std::max(s->max_leaf_shells, s->h_shi[k] - s->h_slo[k]);
-            if (s->h_shi[k] - s->h_slo[k] > 10)
-                throw HxfError{HXF_EINVAL, "leaf spans hold at most 10 shells on the device path"};
         }
         for (int L = D - 1; L >= 0; --L)
             for (int k = s->h_off[L]; k < s->h_off[L + 1]; ++k)
@@ -267,23 +265,46 @@ int hxf_system_info(const hxf_system* s, int64_t* n_functions, int64_t* n_leaves
     })
 }
 
-int hxf_pairs_build(hxf_system* s, double tau_ovlp, void* stream, hxf_pairs** out) {
-    HXF_TRY({
-        if (!s || !out) throw HxfError{HXF_EINVAL, "NULL argument"};
-        if (!(tau_ovlp >= 0.0)) throw HxfError{HXF_EINVAL, "tau_ovlp must be non-negative"};
-        set_device(s->device);
-        hxf_pairs* p = new hxf_pairs();
-        memset(p, 0, sizeof(*p));
-        p->sys = s;
-        p->device = s->device;
-        p->tau_ovlp = tau_ovlp;
-        try {
-            trees_build_pairs(p, (cudaStream_t)stream);
-        } catch (...) {
-            hxf_pairs_destroy(p);
-            throw;
+static void pairs_build(hxf_system* s, double tau_ovlp, const double* s_abs, int on_device, void* stream,
+                        hxf_pairs** out) {
+    if (!s || !out) throw HxfError{HXF_EINVAL, "NULL argument"};
+    if (!(tau_ovlp >= 0.0)) throw HxfError{HXF_EINVAL, "tau_ovlp must be non-negative"};
+    set_device(s->device);
+    const cudaStream_t st = (cudaStream_t)stream;
+    hxf_pairs* p = new hxf_pairs();
+    memset(p, 0, sizeof(*p));
+    p->sys = s;
+    p->device = s->device;
+    p->tau_ovlp = tau_ovlp;
+    double* s_dev = nullptr;
+    try {
+        if (s_abs && !on_device) {  // the caller's |S| (host): staged for the leaf block maxima
+            const size_t bytes = (size_t)s->ns * s->ns * sizeof(double);
+            HXF_CUDA(cudaMalloc(&s_dev, bytes));
+            HXF_CUDA(cudaMemcpyAsync(s_dev, s_abs, bytes, cudaMemcpyHostToDevice, st));
         }
-        *out = p;
+        trees_build_pairs(p, st, s_abs ? (on_device ? s_abs : s_dev) : nullptr);
+        if (s_dev) {
+            HXF_CUDA(cudaStreamSynchronize(st));
+            cudaFree(s_dev);
+        }
+    } catch (...) {
+        if (s_dev) cudaFree(s_dev);
+        hxf_pairs_destroy(p);
+        throw;
+    }
+    *out = p;
+}
+
+int hxf_pairs_build(hxf_system* s, double tau_ovlp, void* stream, hxf_pairs** out) {
+    HXF_TRY({ pairs_build(s, tau_ovlp, nullptr, 0, stream, out); })
+}
+
+int hxf_pairs_build_ovlp(hxf_system* s, double tau_ovlp, const double* s_abs, int on_device, void* stream,
+                         hxf_pairs** out) {
+    HXF_TRY({
+        if (!s_abs) throw HxfError{HXF_EINVAL, "NULL overlap matrix"};
+        pairs_build(s, tau_ovlp, s_abs, on_device, stream, out);
     })
 }
 
@@ -293,7 +314,7 @@ void hxf_pairs_destroy(hxf_pairs* p) {
     void* ptrs[] = {p->norm, p->rowsum, p->colsum, p->smax, p->leaf_base, p->pi,
                     p->pj,   p->ppoff,  p->q,      p->pp,       p->info, p->sq, p->meta,
                     p->ncid, p->nvec,   p->nvec_tri, p->epp, p->eS, p->snorm, p->srow, p->scol,
-                    p->geo, p->gip, p->ngeo, p->ngip};
+                    p->geo, p->gip};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     delete p;

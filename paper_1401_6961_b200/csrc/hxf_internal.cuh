@@ -105,8 +105,6 @@ struct hxf_pairs {
     PrimPair* epp;     // ERI primitive table: each pair's primitives sorted by Schwarz factor, descending
     float4* geo;       // per pair: centroid of the primitive centres, radius (conservative, far-field test)
     float* gip;        // per pair: max 1/p over its primitives (rounded up)
-    float4* ngeo;      // per live leaf pair node (ncid): enclosing sphere of its pairs' spheres
-    float* ngip;       // per live leaf pair node: max 1/p
     double* eS;        // per entry of epp: primitive Schwarz factor sqrt(max_comp (ab|ab))
     double smax_prim;  // max eS
     int* ncid;         // per leaf pair node (nleaf^2): compact live-node id, -1 if pruned
@@ -363,7 +361,7 @@ void note_launch(int n = 1);
 // (defined in the .cu files)
 
 void launch_boys_init();
-void trees_build_pairs(hxf_pairs* pr, cudaStream_t st);
+void trees_build_pairs(hxf_pairs* pr, cudaStream_t st, const double* s_user = nullptr);
 void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStream_t st);
 
 struct ExchangeCtx;

@@ -35,9 +35,8 @@
 #define HXF_ERI_NOFAR 0
 #endif
 
-#define MAXS 10  // shells per leaf span (leaf_size <= 10 functions; checked in api.cu)
-#define MAXP (MAXS * MAXS)
-#define SCREEN_WARPS 4
+#define SCREEN_WARPS 4     // k_screen (any span size)
+#define STAGED_MAXS 10     // k_screen2 stages spans of <= 10 shells (NV_MAXS node vectors)
 
 namespace {
 
@@ -77,37 +76,16 @@ struct ScreenArgs {
     const int* ncidk;
     const double* nveck;
     const double* nveck_tri;
-    const float4* bngeo;      // far-field test per leaf task (k_node_geo, trees.cu)
-    const float4* kngeo;
-    const float* bngip;
-    const float* kngip;
 };
 
 // Far field (ERI key bit 12): every primitive quartet of a shell quartet has
-// Boys argument T = |P-Q|^2 / (1/p + 1/q) >= boys_far_t(L); decided per leaf
-// task from the nodes' enclosing spheres (k_node_geo).  Such quartets sort into
-// their own ERI range whose kernels evaluate only the asymptotic Boys branch --
-// the values the table path selects there.
+// Boys argument T = |P-Q|^2 / (1/p + 1/q) >= boys_far_t(L); decided per shell
+// quartet from the two pairs' enclosing spheres (k_pair_geo, k_classify_far).
+// Such quartets sort into their own ERI range whose kernels evaluate only the
+// asymptotic Boys branch (the branch the table path selects there).
 #define KEY_FAR 0x1000
 #define KEY_BITS 13
 #define KEY_RANGES (1 << KEY_BITS)
-
-struct WarpSmem {
-    double fa[MAXP], sa[MAXP], fb[MAXP], sb[MAXP];
-    double pm[4][MAXP];
-    unsigned char ax[MAXP], ay[MAXP], bx[MAXP], by[MAXP], acl[MAXP], bcl[MAXP];
-    unsigned short apl[MAXP], bpl[MAXP];
-};
-
-// max |P| over the function block of shells (s, t) (|P_jk| for s shells)
-__device__ __forceinline__ double pblock_max(const ScreenArgs& a, int s, int t) {
-    const int f0 = a.fn[s], g0 = a.fn[t];
-    const int nfs = a.nf[s], nft = a.nf[t];
-    double m = 0.0;
-    for (int x = 0; x < nfs; ++x)
-        for (int y = 0; y < nft; ++y) m = fmax(m, fabs(a.P[(int64_t)(f0 + x) * a.nfn + g0 + y]));
-    return m;
-}
 
 // Survivor emission through per-warp slabs: one global atomic reserves SLAB
 // record slots; a slab that cannot take the next ballot is padded with
@@ -165,17 +143,22 @@ __device__ __forceinline__ void tri_decode(int a, int n, int* x, int* y) {
     *y = r + a;
 }
 
-template <bool SYM, bool EMIT>
+// Per-quartet leaf screen for any leaf span size (the reference's --leaf-size
+// takes any value, cli.py:289): one warp per leaf task, every quartet tested
+// from global memory (no per-warp staging, so no bound on the span size).
+// The path for partitions whose leaf spans exceed the staged screen's 10
+// shells, and the A/B reference of k_screen2 (HXF_SCREEN=flat); same
+// decisions, counters and ledger.
+template <bool SYM, bool EMIT, bool EIGHT = false>
 __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
-    __shared__ WarpSmem sm_all[SCREEN_WARPS];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpSmem& sm = sm_all[wid];
-    const int64_t gw = blockIdx.x * (int64_t)SCREEN_WARPS + wid;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = blockIdx.x * (int64_t)SCREEN_WARPS + (threadIdx.x >> 5);
     const int64_t W = (int64_t)gridDim.x * SCREEN_WARPS;
     long long n_eri = 0, n_cull = 0, n_tie = 0;
     Slab slab{0ull, SLAB};
     double ledger = 0.0;
     const bool schwarz = a.mode == HXF_MODE_SCHWARZ;
+    const double tie_lo = a.tau * (1.0 - 1e-12), tie_hi = a.tau * (1.0 + 1e-12);
     for (int64_t t = a.t0 + gw; t < a.t1; t += W) {
         const uint64_t task = a.tasks[t];
         const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
@@ -187,97 +170,66 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
         const int64_t bb = a.bra_base[(int64_t)mu * a.nleaf + nu];
         const int64_t kb = a.ket_base[(int64_t)lam * a.nleaf + sig];
         const bool bdiag = SYM && mu == nu, kdiag = SYM && lam == sig;
-        const int ma = bdiag ? nmu * (nmu + 1) / 2 : nmu * nnu;
-        const int mb = kdiag ? nlam * (nlam + 1) / 2 : nlam * nsig;
-        const float inv_nnu = 1.0f / nnu, inv_nsig = 1.0f / nsig, inv_mb = 1.0f / mb;
-        for (int i = lane; i < ma; i += 32) {
-            int x, y;
-            if (bdiag) tri_decode(i, nmu, &x, &y);
-            else { x = __float2int_rz(((float)i + 0.5f) * inv_nnu); y = i - x * nnu; }
-            const int64_t pid = bb + x * nnu + y;
-            const double sq = a.sqb[pid];
-            sm.sa[i] = sq;
-            sm.fa[i] = schwarz ? sq : a.qb[pid];
-            sm.ax[i] = x;
-            sm.ay[i] = y;
-            sm.apl[i] = x * nnu + y;
-            sm.acl[i] = a.metab[pid];
-        }
-        for (int i = lane; i < mb; i += 32) {
-            int x, y;
-            if (kdiag) tri_decode(i, nlam, &x, &y);
-            else { x = __float2int_rz(((float)i + 0.5f) * inv_nsig); y = i - x * nsig; }
-            const int64_t pid = kb + x * nsig + y;
-            const double sq = a.sqk[pid];
-            sm.sb[i] = sq;
-            sm.fb[i] = schwarz ? sq : a.qk[pid];
-            sm.bx[i] = x;
-            sm.by[i] = y;
-            sm.bpl[i] = x * nsig + y;
-            sm.bcl[i] = a.metak[pid];
-        }
-        // density factors per live slot: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
-        const int rs[4] = {snu, smu, snu, smu}, rn[4] = {nnu, nmu, nnu, nmu};
-        const int cs[4] = {slam, slam, ssig, ssig}, cn[4] = {nlam, nlam, nsig, nsig};
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            if (!((live >> g) & 1)) continue;
-            const float inv = 1.0f / cn[g];
-            for (int i = lane; i < rn[g] * cn[g]; i += 32) {
-                const int x = __float2int_rz(((float)i + 0.5f) * inv), y = i - x * cn[g];
-                sm.pm[g][i] = a.pmax[(int64_t)(rs[g] + x) * a.ns + cs[g] + y];
-            }
-        }
-        __syncwarp();
-        const int total = ma * mb;
-        const double tie_lo = a.tau * (1.0 - 1e-12), tie_hi = a.tau * (1.0 + 1e-12);
-        for (int q0 = 0; q0 < total; q0 += 32) {
-            const int q = q0 + lane;
+        const bool diag8 = EIGHT && mu == lam && nu == sig;   // keep bra pair <= ket pair
+        const int64_t ma = bdiag ? nmu * (nmu + 1) / 2 : nmu * nnu;
+        const int64_t mb = kdiag ? nlam * (nlam + 1) / 2 : nlam * nsig;
+        // slot density blocks: g0 P[nu,lam] g1 P[mu,lam] g2 P[nu,sig] g3 P[mu,sig]
+        const int rs[4] = {snu, smu, snu, smu}, cs[4] = {slam, slam, ssig, ssig};
+        const int64_t total = ma * mb;
+        for (int64_t q0 = 0; q0 < total; q0 += 32) {
+            const int64_t q = q0 + lane;
             bool keep_any = false;
             int mask = 0;
-            int ia = 0, ib = 0;
+            int64_t pa = 0, pb = 0;
+            int ca = 0, cb = 0;
             if (q < total) {
-                ia = __float2int_rz(((float)q + 0.5f) * inv_mb);
-                ib = q - ia * mb;
-                const double fa = sm.fa[ia], fb = sm.fb[ib];
-                const int x = sm.ax[ia], y = sm.ay[ia], z = sm.bx[ib], w = sm.by[ib];
-                const int rowv[4] = {y, x, y, x}, colv[4] = {z, z, w, w};
+                const int ia = (int)(q / mb), ib = (int)(q - (int64_t)ia * mb);
+                int x, y, z, w;
+                if (bdiag) tri_decode(ia, nmu, &x, &y);
+                else { x = ia / nnu; y = ia - x * nnu; }
+                if (kdiag) tri_decode(ib, nlam, &z, &w);
+                else { z = ib / nsig; w = ib - z * nsig; }
+                pa = bb + x * nnu + y;
+                pb = kb + z * nsig + w;
+                if (!(diag8 && ib < ia)) {
+                    const double sqa = __ldg(a.sqb + pa), sqk = __ldg(a.sqk + pb);
+                    const double fa = schwarz ? sqa : __ldg(a.qb + pa), fb = schwarz ? sqk : __ldg(a.qk + pb);
+                    ca = a.metab[pa];
+                    cb = a.metak[pb];
+                    const int rowv[4] = {y, x, y, x}, colv[4] = {z, z, w, w};
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    if (!((live >> g) & 1)) continue;
-                    const double pm = sm.pm[g][rowv[g] * cn[g] + colv[g]];
-                    const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
-                    n_tie += bound >= tie_lo && bound <= tie_hi && a.tau > 0.0;
-                    if (bound > a.tau) {
-                        keep_any = true;
-                        mask |= 1 << g;
-                    } else {
-                        ++n_cull;
-                        ledger += schwarz ? bound : __dmul_rn(__dmul_rn(sm.sa[ia], pm), sm.sb[ib]);
+                    for (int g = 0; g < 4; ++g) {
+                        if (!((live >> g) & 1)) continue;
+                        const double pm = __ldg(a.pmax + (int64_t)(rs[g] + rowv[g]) * a.ns + cs[g] + colv[g]);
+                        const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
+                        n_tie += bound >= tie_lo && bound <= tie_hi && a.tau > 0.0;
+                        if (bound > a.tau) {
+                            keep_any = true;
+                            mask |= 1 << g;
+                        } else {
+                            ++n_cull;
+                            ledger += schwarz ? bound : __dmul_rn(__dmul_rn(sqa, pm), sqk);
+                        }
                     }
+                    if (SYM) {
+                        // diagonal-pair weights: g1/g3 need i != j, g2/g3 need k != l
+                        if (bdiag && x == y) mask &= ~0xa;
+                        if (kdiag && z == w) mask &= ~0xc;
+                    }
+                    n_eri += keep_any;
                 }
-                if (SYM) {
-                    // diagonal-pair weights: g1/g3 need i != j, g2/g3 need k != l
-                    const bool ij = !(bdiag && x == y), kl = !(kdiag && z == w);
-                    if (!ij) mask &= ~0xa;
-                    if (!kl) mask &= ~0xc;
-                }
-                n_eri += keep_any;
             }
             if (EMIT) {
                 const unsigned bal = __ballot_sync(0xffffffffu, keep_any);
                 if (bal) {
-                    const uint64_t pb = (uint64_t)(bb + sm.apl[ia]);
-                    const uint64_t pk = (uint64_t)(kb + sm.bpl[ib]);
-                    const int ca = sm.acl[ia], cb = sm.bcl[ib];
                     const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
-                    // sort key: class, bra / ket primitive-pair counts (uniform warps)
-                    slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56),
+                    const uint64_t selfm = (EIGHT && pa == pb) ? 1ull : 0ull;   // weight 1/2 (eightfold)
+                    slab_emit(slab, a, bal, keep_any,
+                              (uint64_t)pa | ((uint64_t)pb << 28) | ((uint64_t)mask << 56) | (selfm << 60),
                               (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2)), lane);
                 }
             }
         }
-        __syncwarp();
     }
     if (EMIT) slab_pad(slab, a, lane);
     // per-lane totals; counters are integers (order independent); the warp's
@@ -478,19 +430,6 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                 continue;
             }
         }
-        // ---- task-level far field (ERI key bit 12): the enclosing spheres of the
-        // bra and ket leaf nodes (k_node_geo) are separated enough for every
-        // primitive quartet of the task: far0 for (ss|ss), far1 for the p classes
-        bool far0 = false, far1 = false;
-        if (!HXF_ERI_NOFAR) {
-            const int cb_ = a.ncidb[(int64_t)mu * a.nleaf + nu], ck_ = a.ncidk[(int64_t)lam * a.nleaf + sig];
-            const float4 gb = __ldg(a.bngeo + cb_), gk = __ldg(a.kngeo + ck_);
-            const float ip = __ldg(a.bngip + cb_) + __ldg(a.kngip + ck_);
-            const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
-            const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
-            far0 = d > 0.0f && d * d >= (float)(boys_far_t(0) * 1.0001) * ip;
-            far1 = d > 0.0f && d * d >= (float)(boys_far_t(1) * 1.0001) * ip;
-        }
         // ---- stage pair factors (all loads first)
         {
             constexpr int NIT = (MS * MS + 31) / 32;
@@ -685,10 +624,8 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                         const uint64_t cls = (uint64_t)(((ca & 3) << 2) | (cb & 3));
                         // bit 60: eightfold self-mirror quartet (bra pair == ket pair), weight 1/2
                         const uint64_t selfm = (EIGHT && pb == pk) ? 1ull : 0ull;
-                        const bool far = (ca & 3) == 0 && (cb & 3) == 0 ? far0 : far1;
                         slab_emit(slab, a, bal, keep_any, pb | (pk << 28) | ((uint64_t)mask << 56) | (selfm << 60),
-                                  (uint16_t)((far ? KEY_FAR : 0) | (cls << 8) | ((ca >> 2) << 4) | (cb >> 2)),
-                                  lane);
+                                  (uint16_t)((cls << 8) | ((ca >> 2) << 4) | (cb >> 2)), lane);
                     }
                 }
             }
@@ -936,16 +873,18 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
 }
 
 // Per-quartet far-field test over one chunk of survivor records, before the
-// sort: sets key bit 12 for the quartets the screen's task-level test left
-// near.  A streaming pass (8 + 2 bytes per record; the per-pair spheres are
-// gathered with the locality of the screen's task order) instead of the same
-// test inside the screen's emission path, where it cost 11 % of the screen.
+// sort: sets key bit 12 for the quartets whose every primitive quartet has a
+// Boys argument past the table range (per-pair enclosing spheres, k_pair_geo).
+// The decision is a function of the quartet alone, so every driver (naive,
+// fourfold, eightfold, the direct twin) evaluates a given quartet with the same
+// arithmetic and their K agree bit for bit.  A streaming pass (8 + 2 bytes per
+// record; the spheres are gathered with the locality of the screen's order).
 __global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __restrict__ keys, int64_t n,
                                const float4* __restrict__ bgeo, const float* __restrict__ bgip,
                                const float4* __restrict__ kgeo, const float* __restrict__ kgip) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const uint16_t key = keys[t];
-        if (key == SENTINEL_KEY || (key & KEY_FAR)) continue;
+        if (key == SENTINEL_KEY) continue;
         const uint64_t r = rec[t];
         const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
         const int L = __popc((key >> 8) & 15);
@@ -1298,6 +1237,20 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     Timer ttrav(st);
     TravInput ti{s, bra, ket, dens, o->tau_2e, o->mode, eight ? 2 : sym, o->shard_level, o->shard_begin,
                  o->shard_end, o->shard_stride, o->shard_mask, 0, 0, dcount, dledger};
+    ti.root_level = o->root_level;
+    ti.root_index = o->root_index;
+    // a diagonal subtree start: K_out is the block of the start span's functions
+    const bool subtree = o->root_level != 0 || o->root_index != 0;
+    int64_t sub_f0 = 0, sub_n = s->nfn;
+    if (subtree) {
+        if (o->root_level < 0 || o->root_level >= s->n_levels || o->root_index < 0 ||
+            o->root_index >= s->h_off[o->root_level + 1] - s->h_off[o->root_level])
+            throw HxfError{HXF_EINVAL, "traversal start node outside the partition"};
+        if (o->K_fixed) throw HxfError{HXF_EINVAL, "K_fixed requires the tree root as the start node"};
+        const int k = s->h_off[o->root_level] + o->root_index;
+        sub_f0 = s->h_flo[k];
+        sub_n = s->h_fhi[k] - s->h_flo[k];
+    }
     TraversalResult tr = traverse(ti, st);
     g_timings[0] = ttrav.stop();
 
@@ -1346,10 +1299,6 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.ncidk = ket->ncid;
     sa.nveck = ket->nvec;
     sa.nveck_tri = ket->nvec_tri;
-    sa.bngeo = bra->ngeo;
-    sa.kngeo = ket->ngeo;
-    sa.bngip = bra->ngip;
-    sa.kngip = ket->ngip;
     sa.ns = s->ns;
     sa.fn = s->basis.fn;
     sa.nf = s->basis.nf;
@@ -1364,7 +1313,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     // so every per-warp ledger partial, is reproducible
     // HXF_SCREEN=flat selects the per-quartet screen (A/B reference)
     const char* sv = getenv("HXF_SCREEN");
-    const bool flat = sv && !strcmp(sv, "flat");
+    const bool flat = (sv && !strcmp(sv, "flat")) || s->max_leaf_shells > STAGED_MAXS;
     const bool ms8 = s->max_leaf_shells <= 8;
     const int sw = flat ? SCREEN_WARPS
                         : (ms8 ? (sym ? screen2_warps<true, 8>() : screen2_warps<false, 8>())
@@ -1373,8 +1322,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * (sym ? 12 : 8)));
     auto launch_screen = [&](bool emit) {
         if (flat) {
-            if (eight) throw HxfError{HXF_EINVAL, "HXF_SCREEN=flat does not implement the eightfold driver"};
-            if (sym) { if (emit) k_screen<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
+            if (eight) { if (emit) k_screen<true, true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false, true><<<screen_grid, sw * 32, 0, st>>>(sa); }
+            else if (sym) { if (emit) k_screen<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
             else { if (emit) k_screen<false, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<false, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
         } else {
             const dim3 g(screen_grid), b(sw * 32);
@@ -1637,7 +1586,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         else HXF_CUDA(cudaMemsetAsync(K_out, 0, n2 * sizeof(unsigned long long), st));
         if (o->K_scale) *o->K_scale = S;
     } else if (K_out) {
-        double* Kd = o->K_on_device ? K_out : lalloc<double>(n2, st);
+        double* Kd = (o->K_on_device && !subtree) ? K_out : lalloc<double>(n2, st);
         if (Kfx) {
             { k_fx_to_double<<<1024, 256, 0, st>>>(Kfx, n2, S, Kd); note_launch(); }
             if (sym && !eight && o->symmetrize) {
@@ -1660,7 +1609,12 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         } else {
             HXF_CUDA(cudaMemsetAsync(Kd, 0, n2 * sizeof(double), st));
         }
-        if (!o->K_on_device) {
+        if (subtree) {  // the start span's block, local indices
+            HXF_CUDA(cudaMemcpy2DAsync(K_out, sub_n * sizeof(double), Kd + sub_f0 * s->nfn + sub_f0,
+                                       s->nfn * sizeof(double), sub_n * sizeof(double), sub_n,
+                                       o->K_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+            hxf_cache_free(Kd, st);
+        } else if (!o->K_on_device) {
             HXF_CUDA(cudaMemcpyAsync(K_out, Kd, n2 * sizeof(double), cudaMemcpyDeviceToHost, st));
             hxf_cache_free(Kd, st);
         }
@@ -1974,6 +1928,8 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         HXF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb.sort_tb, sb.keys, sb.keys2, sb.rec, sb.rec2, cap, 0, KEY_BITS, st));
         sb.sort_tmp = lalloc<char>(sb.sort_tb, st);
         sb.dbounds = lalloc<int64_t>(KEY_RANGES + 1, st);
+        sb.bgeo = sb.kgeo = pairs->geo;   // the same far-field decisions as the hierarchical drivers
+        sb.bgip = sb.kgip = pairs->gip;
         EriArgs e;
         e.dbounds = nullptr;
         e.bpi = e.kpi = pairs->pi;

@@ -377,10 +377,12 @@ __global__ void k_fold_stripes(const long long* sc, const unsigned long long* sl
     }
 }
 
+// the start task: the diagonal node (r, r) of the start level visited against
+// itself (the root, or a diagonal subtree the caller passed as bra = ket = P)
 template <bool SYM>
-__global__ void k_root(TreeView tv, LevelView lv, uint64_t* out_expand, uint64_t* out_leaf,
+__global__ void k_root(TreeView tv, LevelView lv, int r, uint64_t* out_expand, uint64_t* out_leaf,
                        int* outcome, long long* counters, unsigned long long* ledger) {
-    Visit v = SYM ? visit_sym(tv, lv, 0, 0, 0, 0, 0xf) : visit_naive(tv, lv, 0, 0, 0, 0);
+    Visit v = SYM ? visit_sym(tv, lv, r, r, r, r, 0xf) : visit_naive(tv, lv, r, r, r, r);
     counters[C_VISITED] += 1;
     counters[C_CULL_SCREEN] += v.outcome == O_SCREEN;
     counters[C_CULL_ABSENT] += v.outcome == O_ABSENT;
@@ -398,9 +400,9 @@ __global__ void k_root(TreeView tv, LevelView lv, uint64_t* out_expand, uint64_t
         fx_from_double<LEDGER_LIMBS>(v.ledger, LEDGER_SCALE, limb);
         fx_atomic_add<LEDGER_LIMBS>(ledger, limb);
     }
-    if (v.outcome == O_EXPAND) out_expand[0] = pack_task(0, 0, 0, 0, v.live);
+    if (v.outcome == O_EXPAND) out_expand[0] = pack_task(r, r, r, r, v.live);
     if (v.outcome == O_LEAF)
-        out_leaf[0] = pack_task(lv.leaf_id[0], lv.leaf_id[0], lv.leaf_id[0], lv.leaf_id[0], v.live);
+        out_leaf[0] = pack_task(lv.leaf_id[r], lv.leaf_id[r], lv.leaf_id[r], lv.leaf_id[r], v.live);
     *outcome = v.outcome;
 }
 
@@ -462,15 +464,19 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     };
     zero_stripes();
     const int D = s->n_levels - 1;
+    const int L0 = in.root_level;
+    if (L0 < 0 || L0 > D || in.root_index < 0 || in.root_index >= s->h_off[L0 + 1] - s->h_off[L0])
+        throw HxfError{HXF_EINVAL, "traversal start node outside the partition"};
     std::vector<uint64_t*> leaf_parts;
     std::vector<int64_t> leaf_counts;
     uint64_t* cur = talloc<uint64_t>(1, st);
     uint64_t* leaf0 = talloc<uint64_t>(1, st);
     int* d_outcome = talloc<int>(1, st);
-    LevelView lv0{s->h_off[1] - s->h_off[0], s->node_off[0], s->lv.leaf_id + s->h_off[0],
-                  s->lv.flo + s->h_off[0]};
-    if (in.sym) { k_root<true><<<1, 1, 0, st>>>(tv, lv0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
-    else { k_root<false><<<1, 1, 0, st>>>(tv, lv0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
+    LevelView lv0{s->h_off[L0 + 1] - s->h_off[L0], s->node_off[L0], s->lv.leaf_id + s->h_off[L0],
+                  s->lv.flo + s->h_off[L0]};
+    const int r0 = in.root_index;
+    if (in.sym) { k_root<true><<<1, 1, 0, st>>>(tv, lv0, r0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
+    else { k_root<false><<<1, 1, 0, st>>>(tv, lv0, r0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
     int outcome = 0;
     HXF_CUDA(cudaMemcpyAsync(&outcome, d_outcome, sizeof(int), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaStreamSynchronize(st));
@@ -484,7 +490,7 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     }
     res.frontier_sizes.push_back(n_cur);
     bool cut_reached = false;
-    for (int L = 0; L < D && n_cur > 0; ++L) {
+    for (int L = L0; L < D && n_cur > 0; ++L) {
         if (sharded && L == in.shard_level) {
             cut_reached = true;
             // restrict the frontier to this shard; from here on counters are real

@@ -22,6 +22,8 @@ struct TravInput {
     int frontier_level;
     long long* counters;   // device C_NCOUNTERS
     unsigned long long* ledger;  // device LEDGER_LIMBS
+    int root_level = 0;    // the traversal starts at the diagonal node (root_index, root_index)
+    int root_index = 0;    // of this level (a diagonal subtree; 0, 0 = the tree root)
 };
 
 struct TraversalResult {

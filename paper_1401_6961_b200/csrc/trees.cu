@@ -77,6 +77,19 @@ __global__ void k_leaf_smax(DevBasis B, DevLevels lv, const int* lslo, const int
     smax[(int64_t)c * nleaf + r] = m;
 }
 
+// overlap_matrix override (quadtree.py:284-293): block max of the caller's |S|
+// over the leaf spans (r, c), both orientations (not assumed symmetric)
+__global__ void k_leaf_smax_user(const double* __restrict__ S, int ns, const int* lslo, const int* lshi, int nleaf,
+                                 double* smax) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nleaf * nleaf) return;
+    const int r = (int)(t / nleaf), c = (int)(t % nleaf);
+    double m = 0.0;
+    for (int i = lslo[r]; i < lshi[r]; ++i)
+        for (int j = lslo[c]; j < lshi[c]; ++j) m = fmax(m, fabs(S[(int64_t)i * ns + j]));
+    smax[t] = m;
+}
+
 __global__ void k_leaf_pair_counts(const double* smax, double tau, const int* lslo,
                                    const int* lshi, const int* lplo, const int* lphi, int nleaf,
                                    int64_t* npairs, int64_t* nprims) {
@@ -424,36 +437,6 @@ __global__ void k_node_vectors(const int* lslo, const int* lshi, int nl, const i
     }
 }
 
-// Far-field geometry per live leaf pair node (compact id ncid): the enclosing
-// sphere of its pairs' spheres (k_pair_geo) and the max 1/p, rounded outward.
-// The leaf screen tests a whole leaf task with it (leaf.cu, task_far).
-__global__ void k_node_geo(int nl, const int* lslo, const int* lshi, const int64_t* leaf_base, const int* ncid,
-                           const float4* geo, const float* gip, float4* ngeo, float* ngip) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= (int64_t)nl * nl) return;
-    const int64_t bb = leaf_base[t];
-    if (bb < 0) return;
-    const int mu = (int)(t / nl), nu = (int)(t % nl);
-    const int np = (lshi[mu] - lslo[mu]) * (lshi[nu] - lslo[nu]);
-    double cx = 0.0, cy = 0.0, cz = 0.0, ip = 0.0;
-    for (int k = 0; k < np; ++k) {
-        const float4 g = geo[bb + k];
-        cx += g.x;
-        cy += g.y;
-        cz += g.z;
-        ip = fmax(ip, (double)gip[bb + k]);
-    }
-    const float fx = (float)(cx / np), fy = (float)(cy / np), fz = (float)(cz / np);
-    double r = 0.0;
-    for (int k = 0; k < np; ++k) {
-        const float4 g = geo[bb + k];
-        const double dx = (double)g.x - fx, dy = (double)g.y - fy, dz = (double)g.z - fz;
-        r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz) + g.w);
-    }
-    ngeo[ncid[t]] = make_float4(fx, fy, fz, __double2float_ru(r * (1.0 + 1e-6) + 1e-5));
-    ngip[ncid[t]] = __double2float_ru(ip);
-}
-
 __global__ void k_live_flags(const int64_t* leaf_base, int64_t n, int* flag) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t < n) flag[t] = leaf_base[t] >= 0 ? 1 : 0;
@@ -548,7 +531,7 @@ static LeafTables make_leaf_tables(hxf_system* s, cudaStream_t st, std::vector<v
     return t;
 }
 
-void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
+void trees_build_pairs(hxf_pairs* pr, cudaStream_t st, const double* s_user) {
     hxf_system* s = pr->sys;
     std::vector<void*> tmp;
     const int nl = s->n_leaves;
@@ -556,7 +539,8 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
     LeafTables lt = make_leaf_tables(s, st, tmp);
     double* lsmax = dalloc<double>(nl2, st);
     tmp.push_back(lsmax);
-    { k_leaf_smax<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, s->lv, lt.lslo, lt.lshi, nl, lsmax); note_launch(); }
+    if (s_user) { k_leaf_smax_user<<<nblk(nl2, 128), 128, 0, st>>>(s_user, s->ns, lt.lslo, lt.lshi, nl, lsmax); note_launch(); }
+    else { k_leaf_smax<<<nblk(nl2, 128), 128, 0, st>>>(s->basis, s->lv, lt.lslo, lt.lshi, nl, lsmax); note_launch(); }
     int64_t* npairs = dalloc<int64_t>(nl2 + 1, st);
     int64_t* nprims = dalloc<int64_t>(nl2 + 1, st);
     int64_t* pbase = dalloc<int64_t>(nl2 + 1, st);
@@ -635,12 +619,11 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st) {
         pr->nvec = dalloc<double>((int64_t)std::max(nlive, 1) * NVEC, st);
         pr->nvec_tri = dalloc<double>((int64_t)nl * NVEC, st);
         HXF_CUDA(cudaMemsetAsync(pr->nvec_tri, 0, (int64_t)nl * NVEC * sizeof(double), st));
-        { k_node_vectors<<<nblk(nl2, 128), 128, 0, st>>>(lt.lslo, lt.lshi, nl, pr->leaf_base, pr->ncid, pr->q,
-                                                       pr->sq, pr->nvec, pr->nvec_tri); note_launch(); }
-        pr->ngeo = dalloc<float4>((int64_t)std::max(nlive, 1), st);
-        pr->ngip = dalloc<float>((int64_t)std::max(nlive, 1), st);
-        { k_node_geo<<<nblk(nl2, 128), 128, 0, st>>>(nl, lt.lslo, lt.lshi, pr->leaf_base, pr->ncid, pr->geo,
-                                                   pr->gip, pr->ngeo, pr->ngip); note_launch(); }
+        // the staged leaf screen's node vectors (spans of <= NV_MAXS shells; larger
+        // partitions take the unstaged screen, which does not read them)
+        if (s->max_leaf_shells <= NV_MAXS)
+            { k_node_vectors<<<nblk(nl2, 128), 128, 0, st>>>(lt.lslo, lt.lshi, nl, pr->leaf_base, pr->ncid, pr->q,
+                                                           pr->sq, pr->nvec, pr->nvec_tri); note_launch(); }
     }
     double* lnorm = dalloc<double>(nl2, st);
     double* lrow = dalloc<double>(nl2, st);

@@ -239,6 +239,20 @@ def _require_root(node, what):
         raise InvalidArgumentError(f"{what}: the device drivers start from the tree root")
 
 
+def _start_node(bra, ket, P):
+    """(level, index) of the diagonal start node.  The reference accepts any
+    bra/ket/P whose six spans are one Span object (_check_same_partition,
+    exchange_naive.py:105-108): the root or a diagonal subtree (r, r).  A ragged
+    leaf repeats at deeper levels; every view of it denotes the same node."""
+    nodes = (bra, ket, P)
+    for nd in nodes:
+        if nd._r != nd._c:
+            raise InvalidArgumentError("bra, ket and P must be built over the same partition")
+    lv = min(nd._level for nd in nodes)
+    idx = bra._t.ds.index[lv][id(bra.row)]
+    return lv, idx
+
+
 def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log=None,
                  K_out=None, shard=None, symmetrize=True, digest=None, digest_sample=(1, 0),
                  K_fixed=False):
@@ -262,13 +276,11 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
     if mode not in ("schwarz", "literal"):
         raise InvalidArgumentError(f"unknown screening mode {mode!r}")
     _check_same_partition(bra, ket, P)
-    _require_root(bra, "bra")
-    _require_root(ket, "ket")
-    if P._level != 0:
-        raise InvalidArgumentError("P: the device drivers start from the tree root")
+    root_level, root_index = _start_node(bra, ket, P)
     L = _native.lib()
     n = bra.row.n_functions
     opts = _native.ExchangeOpts()
+    opts.root_level, opts.root_index = root_level, root_index
     opts.tau_2e = float(tau_2e)
     opts.mode = 0 if mode == "schwarz" else 1
     # symmetry: False / True (fourfold) / "eightfold"

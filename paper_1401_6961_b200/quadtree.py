@@ -362,14 +362,20 @@ def build_matrix_tree(dense, partition: Partition, zero_drop: float = 0.0) -> Ma
 # ----------------------------------------------------------------- pair tree
 
 class _PairTree:
-    def __init__(self, partition, tau_ovlp):
+    def __init__(self, partition, tau_ovlp, s_abs=None):
         ds = partition.device()
         self.partition = partition
         self.ds = ds
         self.tau_ovlp = tau_ovlp
         h = ctypes.c_void_p()
-        _native.check(_native.lib().hxf_pairs_build(ds.handle, float(tau_ovlp),
-                                                    _native.current_stream(), ctypes.byref(h)))
+        if s_abs is None:
+            _native.check(_native.lib().hxf_pairs_build(ds.handle, float(tau_ovlp),
+                                                        _native.current_stream(), ctypes.byref(h)))
+        else:
+            on_dev = 1 if (hasattr(s_abs, "is_cuda") and s_abs.is_cuda) else 0
+            _native.check(_native.lib().hxf_pairs_build_ovlp(ds.handle, float(tau_ovlp), _native.ptr(s_abs),
+                                                             on_dev, _native.current_stream(),
+                                                             ctypes.byref(h)))
         self.handle = h
         weakref.finalize(self, _native.lib().hxf_pairs_destroy, h)
         self._lvl = {}
@@ -473,17 +479,27 @@ def build_pair_tree(system: BasisSystem, partition: Partition, tau_ovlp: float =
     """Shell-pair quadtree with overlap pruning, built on the device.
 
     A node is pruned iff every shell-pair overlap magnitude in its span is
-    below tau_ovlp (quadtree.py:284-337).  ``overlap_matrix`` overrides are
-    not supported on the device path (the overlap is computed there).
+    below tau_ovlp (quadtree.py:284-337).  ``overlap_matrix`` (n_shells x
+    n_shells, host array or CUDA tensor) replaces the computed overlaps for the
+    pruning decisions, as in the reference (|S| of the given matrix, block max
+    per node, not assumed symmetric); Q and the ERIs are unaffected.
     """
+    s_abs = None
     if overlap_matrix is not None:
-        raise InvalidArgumentError("overlap_matrix overrides are not supported on the device path")
+        ns = len(system.shells)
+        if hasattr(overlap_matrix, "is_cuda") and overlap_matrix.is_cuda:
+            import torch
+            s_abs = overlap_matrix.detach().to(torch.float64).abs().contiguous()
+        else:
+            s_abs = np.ascontiguousarray(np.abs(np.asarray(overlap_matrix, dtype=float)))
+        if tuple(s_abs.shape) != (ns, ns):
+            raise InvalidArgumentError(f"overlap_matrix must be ({ns}, {ns}), got {tuple(s_abs.shape)}")
     if partition.system is None:
         partition.system = system
     elif partition.system is not system:
         if len(partition.system.shells) != len(system.shells):
             raise InvalidArgumentError("system does not match the partition")
-    t = _PairTree(partition, tau_ovlp)
+    t = _PairTree(partition, tau_ovlp, s_abs)
     return t.view(0, 0, 0)
 
 

@@ -235,8 +235,78 @@ def golden_integrals():
     save("integrals", out)
 
 
+def golden_boundary():
+    """Reference behaviours at the edges of the drop-in boundary: leaf spans
+    above 10 shells (--leaf-size accepts any value, cli.py:289), the
+    overlap_matrix override of build_pair_tree (quadtree.py:284-293) and a
+    diagonal subtree as the start node (any bra/ket/P with one shared span,
+    exchange_naive.py:105-108)."""
+    for leaf in (16, 32):
+        system = rb.generate_cluster(20, seed=5)
+        system, perm = rb.hilbert_order(system)
+        part = rq.build_partition(system, leaf_size=leaf)
+        pairs = rq.build_pair_tree(system, part, tau_ovlp=1e-11)
+        P = hexfock.build_density(system, hexfock.DensityModel())
+        P_tree = rq.build_matrix_tree(P, part)
+        centers, prims, nprim = system_arrays(system)
+        out = {"centers": centers, "prims": prims, "nprim": nprim, "P": P,
+               "leaf_size": np.int64(leaf), "tau_ovlp": np.float64(1e-11),
+               "pair_walk": np.array(walk(pairs)), "p_walk": np.array(walk(P_tree))}
+        run_drivers(system, pairs, P_tree, (0.0, 1e-8), out, (1e-8,))
+        save(f"leaf{leaf}", out)
+    # overlap_matrix override: a non-symmetric |S| (computed overlaps times a
+    # seeded factor in [0.01, 3]) prunes a different set of nodes
+    rng = np.random.default_rng(77)
+    system = rb.generate_cluster(8, seed=9)
+    system, _ = rb.hilbert_order(system)
+    part = rq.build_partition(system, leaf_size=4)
+    S = rq.shell_overlap_matrix(system) * rng.uniform(0.01, 3.0, size=(system.n_shells,) * 2)
+    pairs = rq.build_pair_tree(system, part, tau_ovlp=1e-3, overlap_matrix=S)
+    P = hexfock.build_density(system, hexfock.DensityModel())
+    P_tree = rq.build_matrix_tree(P, part)
+    centers, prims, nprim = system_arrays(system)
+    out = {"centers": centers, "prims": prims, "nprim": nprim, "P": P, "S": S,
+           "leaf_size": np.int64(4), "tau_ovlp": np.float64(1e-3),
+           "pair_walk": np.array(walk(pairs)), "p_walk": np.array(walk(P_tree))}
+    run_drivers(system, pairs, P_tree, (0.0, 1e-8), out, (1e-8,))
+    save("ovlp_override", out)
+    # diagonal subtree start: the root's first (left, left) child and its
+    # (left, left) grandchild, spans starting at function 0
+    system = rb.generate_cluster(10, seed=3)
+    system, _ = rb.hilbert_order(system)
+    part = rq.build_partition(system, leaf_size=4)
+    pairs = rq.build_pair_tree(system, part, tau_ovlp=1e-11)
+    P = hexfock.build_density(system, hexfock.DensityModel())
+    P_tree = rq.build_matrix_tree(P, part)
+    centers, prims, nprim = system_arrays(system)
+    out = {"centers": centers, "prims": prims, "nprim": nprim, "P": P,
+           "leaf_size": np.int64(4), "tau_ovlp": np.float64(1e-11)}
+    for depth in (1, 2):
+        b, p = pairs, P_tree
+        for _ in range(depth):
+            b, p = b.children[(0, 0)], p.children[(0, 0)]
+        for tau in (0.0, 1e-8):
+            for sym in (False, True):
+                log = []
+                if sym:
+                    K, c = build_exchange_symmetric(b, p, tau, quartet_log=log)
+                else:
+                    K, c = build_exchange_naive(b, b, p, tau, quartet_log=log)
+                pre = f"d{depth}_" + ("sym" if sym else "naive") + f"_{tau:g}"
+                out[pre + "_K"] = K
+                out[pre + "_counters"] = counters_vec(c, sym)
+                out[pre + "_ledger"] = np.float64(c.culled_bound_ledger)
+                out[pre + "_log"] = np.asarray(sorted(log), dtype=np.int64).reshape(-1, 4)
+    save("subtree", out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()["golden_" + name]()
+        sys.exit(0)
     golden_integrals()
     golden_ragged()
     golden_clusters()
     golden_c1()
+    golden_boundary()

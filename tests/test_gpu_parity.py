@@ -19,7 +19,10 @@ from paper_1401_6961_b200 import configs
 pytestmark = pytest.mark.gpu
 
 FIXTURES = ["cluster1", "cluster3", "cluster5", "cluster10", "ragged0", "ragged1",
-            "ragged2", "ragged3", "identity3", "c1"]
+            "ragged2", "ragged3", "identity3", "c1",
+            # boundary edges (tests/golden/make_golden.py golden_boundary): leaf spans of
+            # up to 16 / 32 shells (the unstaged screen) and the overlap_matrix override
+            "leaf16", "leaf32", "ovlp_override"]
 K_TOL = 1e-10
 
 
@@ -28,9 +31,53 @@ def _device_setup(g):
     leaf = int(g["leaf_size"]) if "leaf_size" in g else 10
     tau_ovlp = float(g["tau_ovlp"]) if "tau_ovlp" in g else 1e-11
     part = hx.build_partition(system, leaf_size=leaf)
-    pairs = hx.build_pair_tree(system, part, tau_ovlp=tau_ovlp)
+    pairs = hx.build_pair_tree(system, part, tau_ovlp=tau_ovlp, overlap_matrix=g.get("S"))
     P_tree = hx.build_matrix_tree(g["P"], part)
     return system, pairs, P_tree
+
+
+def test_subtree_start_matches_reference(golden):
+    """A diagonal subtree as bra = ket = P (the reference accepts any node with
+    one shared span, exchange_naive.py:105-108): counters, ledger, evaluated
+    set and K (the span's block) equal the reference's at depths 1 and 2."""
+    g = golden("subtree")
+    system, pairs, P_tree = _device_setup(g)
+    keys = sorted({k.rsplit("_", 1)[0] for k in g if k.endswith("_counters")})
+    assert len(keys) == 8
+    for key in keys:
+        depth, drv, tag = key.split("_")
+        b, p = pairs, P_tree
+        for _ in range(int(depth[1:])):
+            b, p = b.children[(0, 0)], p.children[(0, 0)]
+        sym = drv == "sym"
+        log = []
+        if sym:
+            K, c = hx.build_exchange_symmetric(b, p, float(tag), quartet_log=log)
+        else:
+            K, c = hx.build_exchange_naive(b, b, p, float(tag), quartet_log=log)
+        assert K.shape == g[key + "_K"].shape, key
+        assert np.array_equal(counters_vec(c, sym), g[key + "_counters"]), key
+        assert c.culled_bound_ledger == pytest.approx(float(g[key + "_ledger"]), rel=1e-12, abs=1e-300)
+        assert np.abs(K - g[key + "_K"]).max() <= K_TOL, key
+        assert np.array_equal(np.asarray(sorted(log), dtype=np.int64).reshape(-1, 4), g[key + "_log"]), key
+
+
+def test_leaf_spans_above_ten_shells_use_unstaged_screen():
+    """leaf_size 32 on a p-shell cube: spans of > 10 shells take the unstaged
+    screen; the eightfold driver is supported there too and its K equals the
+    fourfold K."""
+    cfg = configs.cube_cluster(6, 3, "tiny")
+    part = hx.build_partition(cfg.system, leaf_size=32)
+    assert max(s.shell_hi - s.shell_lo for s in part.leaves) > 10
+    pairs = hx.build_pair_tree(cfg.system, part, tau_ovlp=1e-11)
+    P_tree = hx.build_matrix_tree(cfg.P, part)
+    st = ho.Setup(cfg.system, cfg.P, tau_ovlp=1e-11, leaf_size=32)
+    K4, c4 = hx.build_exchange_symmetric(pairs, P_tree, 1e-8)
+    K4r, c4r = st.symmetric(1e-8)
+    assert np.array_equal(counters_vec(c4, True), counters_vec(c4r, True))
+    assert np.abs(K4 - K4r).max() <= K_TOL
+    K8, _ = hx.build_exchange_eightfold(pairs, P_tree, 1e-8)
+    assert np.abs(K8 - K4).max() <= 1e-12
 
 
 @pytest.mark.parametrize("name", FIXTURES)

@@ -61,6 +61,26 @@ def test_drivers_match_reference(golden, name):
             assert np.array_equal(bits, ref), key
 
 
+@pytest.mark.parametrize("name", ["leaf16", "leaf32"])
+def test_large_leaf_spans_match_reference(golden, name):
+    """Leaf spans of up to 16 / 32 shells (the reference's --leaf-size takes any
+    value): tree, counters, ledger, K and the evaluated set at tau = 1e-8 (the
+    tau = 0 keys are checked on the GPU only: the oracle needs minutes there)."""
+    g = golden(name)
+    system, st = _setup(g)
+    pw = np.array(tree_walk(st.pairs))
+    assert np.array_equal(pw[:, :7], g["pair_walk"][:, :7])
+    n_sh = system.n_shells
+    for sym in (False, True):
+        key = ("sym" if sym else "naive") + "_1e-08"
+        log = []
+        K, c = (st.symmetric if sym else st.naive)(1e-8, quartet_log=log)
+        assert np.array_equal(counters_vec(c, sym), g[key + "_counters"]), key
+        assert c.culled_bound_ledger == pytest.approx(float(g[key + "_ledger"]), rel=1e-12, abs=0)
+        assert np.abs(K - g[key + "_K"]).max() <= 1e-13, key
+        assert np.array_equal(quartet_bits(log, n_sh), np.unpackbits(g[key + "_qbits"])[:n_sh ** 4].astype(bool))
+
+
 def test_c1_fold_identity(golden):
     # SURVEY A5b: the 4-fold set is the canonical image of the naive set
     g = golden("c1")
