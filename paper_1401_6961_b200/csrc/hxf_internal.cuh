@@ -128,7 +128,11 @@ struct hxf_pairs {
 #define NV_FC NV_MAXS
 #define NV_SR (2 * NV_MAXS)
 #define NV_SC (3 * NV_MAXS)
-#define NVEC (4 * NV_MAXS)
+//   [NV_GR + x] = sqrt(max_y Q) = max_y sqrtQ   [NV_GC + y] likewise (sqrt is monotone and
+//   correctly rounded): the Schwarz-mode cell factors, so the screen takes no square root
+#define NV_GR (4 * NV_MAXS)
+#define NV_GC (5 * NV_MAXS)
+#define NVEC (6 * NV_MAXS)
 
 // Stream-ordered caching allocator for the builds' scratch (api.cu).  Freed blocks
 // go to a per-(device, stream, size-bucket) free list instead of back to the CUDA
@@ -192,8 +196,13 @@ __device__ __forceinline__ double sorted_product3(double a, double b, double c) 
 // Correctly rounded sum (Shewchuk partials + CPython's final half-way
 // correction), so device norms match math.fsum (quadtree.py:20-25) bit for
 // bit given identical inputs.  Partials live in local memory.
+// Capacity: the partials are non-overlapping doubles; sums of squares that reach down
+// into the denormals were seen to need 48-49 of them (a 20 x 20-shell leaf block), so
+// the array holds 96, and if it ever fills the running sum is folded into the top
+// partial (inexact by an ulp of that partial) instead of being dropped.
+#define FSUM_CAP 96
 struct FSum {
-    double part[48];
+    double part[FSUM_CAP];
     int n;
     __device__ __forceinline__ FSum() : n(0) {}
     __device__ __forceinline__ void add(double x) {
@@ -206,7 +215,8 @@ struct FSum {
             if (lo != 0.0) part[i++] = lo;
             x = hi;
         }
-        if (i < 48) part[i++] = x;
+        if (i < FSUM_CAP) part[i++] = x;
+        else part[FSUM_CAP - 1] = __dadd_rn(part[FSUM_CAP - 1], x);
         n = i;
     }
     __device__ __forceinline__ double result() const {

@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         const uint64_t task = a.tasks[t];
         const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
                   sig = (task >> 45) & 0x7fff;
-        const int live = SYM ? (int)(task >> 60) : 1;
+        int live = SYM ? (int)(task >> 60) : 1;
         const int smu = a.lslo[mu], snu = a.lslo[nu], slam = a.lslo[lam], ssig = a.lslo[sig];
         const int nmu = a.lshi[mu] - smu, nnu = a.lshi[nu] - snu, nlam = a.lshi[lam] - slam,
                   nsig = a.lshi[sig] - ssig;
@@ -375,7 +375,8 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                 if (i < 8 * MS) {
                     const int h = i < 4 * MS ? i : i - 4 * MS;
                     const int o = h / MS, r = h - o * MS;
-                    vn[u] = __ldg((i < 4 * MS ? vb : vk) + o * NV_MAXS + r);
+                    // F entries: max Q (literal) or its square root (Schwarz: NV_GR / NV_GC)
+                    vn[u] = __ldg((i < 4 * MS ? vb : vk) + ((schwarz && o < 2) ? o + 4 : o) * NV_MAXS + r);
                 }
             }
 #pragma unroll
@@ -391,10 +392,7 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                 const int i = lane + 32 * u;
                 if (i < 8 * MS) {
                     const int h = i < 4 * MS ? i : i - 4 * MS;
-                    const int o = h / MS;
-                    double v = vn[u];
-                    if (schwarz && o < 2) v = sqrt(v);   // max sqrt(Q) = sqrt(max Q) (monotone, correctly rounded)
-                    (i < 4 * MS ? sm.nvb : sm.nvk)[h] = v;
+                    (i < 4 * MS ? sm.nvb : sm.nvk)[h] = vn[u];
                 }
             }
         }
@@ -403,12 +401,15 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         // quartet bound fl(fl(f_a p) f_b) <= F_A(r) p(r,c) F_B(c) (1 + 4 eps).  A task
         // with no passing cell in any live slot is culled whole (no quartet can be a
         // tie); its ledger is sum_{r,c} S_A(r) p(r,c) S_B(c) per slot.
-        {
-            bool anyp = false;
-            double lcell = 0.0;
+        // A slot with no passing cell is closed for the whole task (its count and
+        // ledger are added here), so the later phases stage and test the open slots only.
+        if (!diag8) {
+            int closed = 0;
 #pragma unroll
             for (int g = 0; g < Smem2<SYM, MS>::NG; ++g) {
                 if (!((live >> g) & 1)) continue;
+                bool anyp = false;
+                double lcell = 0.0;
                 const int fo = (g == 0 || g == 2) ? MS : 0, so = fo + 2 * MS;   // F_C / F_R, S_C / S_R
                 const int fk = g < 2 ? 0 : MS, sk = fk + 2 * MS;
                 const float inv = c_inv[cn[g]];
@@ -419,10 +420,14 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
                     if (!(sm.nvb[fo + r] * pm * sm.nvk[fk + c] * (1.0 + 1e-14) <= tau_skip)) anyp = true;
                     lcell += sm.nvb[so + r] * pm * sm.nvk[sk + c];
                 }
+                if (!__any_sync(0xffffffffu, anyp)) {
+                    closed |= 1 << g;
+                    if (lane == 0) n_cull += (long long)ma * mb;
+                    ledger += lcell;
+                }
             }
-            if (!__any_sync(0xffffffffu, anyp) && !diag8) {
-                if (lane == 0) n_cull += (long long)ma * mb * __popc(live & (SYM ? 0xf : 1));
-                ledger += lcell;
+            live &= ~closed;
+            if (!live) {
 #ifdef HXF_PROF_SCREEN
                 ++cyc[4];
 #endif

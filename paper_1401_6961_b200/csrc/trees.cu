@@ -158,7 +158,19 @@ __device__ double diag_q(const PrimPair* pp, int64_t b0, int64_t b1, double3 A, 
     return q;
 }
 
-// Q for canonical pairs i <= j, mirrored to (j, i) (quadtree.py:307-313)
+// Q for canonical pairs i <= j, mirrored to (j, i) (quadtree.py:307-313).  With a
+// caller-supplied, non-symmetric |S| (the overlap_matrix override) a node can be
+// live while its mirror is pruned: the mirror write is skipped when the (j, i)
+// node is pruned, and a pair (i > j) whose canonical node is pruned evaluates
+// its own Q from its primitive pairs transposed into the canonical (j, i) order,
+// so the value is bitwise the one the canonical node would have cached.
+__device__ double diag_q_any(int li, int lj, const PrimPair* pp, int n, double3 A, double3 C) {
+    if (li == 0 && lj == 0) return diag_q<0, 0>(pp, 0, n, A, C);
+    if (li == 0) return diag_q<0, 1>(pp, 0, n, A, C);
+    if (lj == 0) return diag_q<1, 0>(pp, 0, n, A, C);
+    return diag_q<1, 1>(pp, 0, n, A, C);
+}
+
 __global__ void k_diag_q(DevBasis B, int64_t n_pairs, const int* pi, const int* pj,
                          const int64_t* ppoff, const PrimPair* pp, const int* leaf_of_shell,
                          const int* lslo, const int* lshi, int nleaf, const int64_t* leaf_base,
@@ -166,23 +178,24 @@ __global__ void k_diag_q(DevBasis B, int64_t n_pairs, const int* pi, const int* 
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= n_pairs) return;
     const int i = pi[t], j = pj[t];
-    if (i > j) return;
+    const int Li = leaf_of_shell[i], Lj = leaf_of_shell[j];
+    const int64_t mb = i == j ? -1 : leaf_base[(int64_t)Lj * nleaf + Li];   // the mirror pair's node
     const int64_t b0 = ppoff[t], b1 = ppoff[t + 1];
-    const double3 A = B.ctr[i], C = B.ctr[j];
-    const PrimPair* base = pp + b0;
-    double v;
-    const int li = B.l[i], lj = B.l[j];
-    if (li == 0 && lj == 0) v = diag_q<0, 0>(base, 0, b1 - b0, A, C);
-    else if (li == 0) v = diag_q<0, 1>(base, 0, b1 - b0, A, C);
-    else if (lj == 0) v = diag_q<1, 0>(base, 0, b1 - b0, A, C);
-    else v = diag_q<1, 1>(base, 0, b1 - b0, A, C);
-    q[t] = v;
-    if (i != j) {
-        // pair (j, i) lives in node (leaf(j), leaf(i)) at row j, column i
-        const int Li = leaf_of_shell[i], Lj = leaf_of_shell[j];
-        const int64_t mb = leaf_base[(int64_t)Lj * nleaf + Li];
-        q[mb + (int64_t)(j - lslo[Lj]) * (lshi[Li] - lslo[Li]) + (i - lslo[Li])] = v;
+    const int n = (int)(b1 - b0);
+    if (i > j) {
+        if (mb >= 0) return;   // the canonical pair (j, i) exists and writes both
+        const int ni = B.poff[i + 1] - B.poff[i], nj = B.poff[j + 1] - B.poff[j];
+        // n <= 9: shells hold 1..3 primitives (hxf_system_create checks)
+        PrimPair tr[16];       // (b over j outer, a over i inner): the (j, i) pair's order
+        for (int a = 0; a < ni; ++a)
+            for (int b = 0; b < nj; ++b) tr[b * ni + a] = pp[b0 + a * nj + b];
+        q[t] = diag_q_any(B.l[j], B.l[i], tr, n, B.ctr[j], B.ctr[i]);
+        return;
     }
+    const double v = diag_q_any(B.l[i], B.l[j], pp + b0, n, B.ctr[i], B.ctr[j]);
+    q[t] = v;
+    // pair (j, i) lives in node (leaf(j), leaf(i)) at row j, column i
+    if (mb >= 0) q[mb + (int64_t)(j - lslo[Lj]) * (lshi[Li] - lslo[Li]) + (i - lslo[Li])] = v;
 }
 
 // primitive Schwarz factors S = sqrt(max_comp (ab|ab)) of every primitive pair,
@@ -434,6 +447,10 @@ __global__ void k_node_vectors(const int* lslo, const int* lshi, int nl, const i
                 v[NV_SR + x] += s;
                 v[NV_SC + y] += s;
             }
+        for (int k = 0; k < NV_MAXS; ++k) {
+            v[NV_GR + k] = sqrt(v[NV_FR + k]);
+            v[NV_GC + k] = sqrt(v[NV_FC + k]);
+        }
     }
 }
 
