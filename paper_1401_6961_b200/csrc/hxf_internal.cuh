@@ -32,8 +32,10 @@ struct HxfError {
 // c = w_a w_b exp(-ab/p |AB|^2) / p * sqrt(2 pi^{5/2}), so the primitive
 // (ss|ss) is c_bra c_ket F0(T) / sqrt(p+q).  64-byte aligned record.
 // cs = c / sqrt(p): the far-field (ss|ss) closed form c'_b c'_k sqrt(pi)/2 / |P-Q|
-struct __align__(16) PrimPair {
-    double p, ip, c, x, y, z, cs, pad1;
+// One primitive pair, 64 bytes in two 32-byte halves: {centre, cs} is all the far-field
+// (ss|ss) path reads (one 256-bit load), {p, 1/p, c} completes the record (a second one).
+struct __align__(32) PrimPair {
+    double x, y, z, cs, p, ip, c, pad1;
 };
 
 // Partition levels on device (quadtree.py:55-84): spans of every level,
@@ -162,22 +164,29 @@ __host__ __device__ __forceinline__ int64_t node_index(const int64_t* node_off, 
     return node_off[level] + (int64_t)r * nspan + c;
 }
 
-__device__ __forceinline__ PrimPair load_pp(const PrimPair* p) {
-    const double2* q = reinterpret_cast<const double2*>(p);
-    double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
-    PrimPair r;
-    r.p = a.x; r.ip = a.y; r.c = b.x; r.x = b.y; r.y = c.x; r.z = c.y;
-    r.cs = 0.0; r.pad1 = 0.0;
+// 256-bit read-only global load (sm_100a LDG.E.256): one instruction, and for the
+// scattered per-lane gathers of the ERI kernels one L1 wavefront per lane, per 32 bytes
+struct __align__(32) Double4 { double a, b, c, d; };
+__device__ __forceinline__ Double4 ldg256(const void* p) {
+    Double4 r;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.a), "=d"(r.b), "=d"(r.c), "=d"(r.d) : "l"(p));
     return r;
 }
 
-// the fields the far-field (ss|ss) path reads: c, centre, cs
-__device__ __forceinline__ PrimPair load_pp_far(const PrimPair* p) {
-    const double2* q = reinterpret_cast<const double2*>(p);
-    double2 b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
+__device__ __forceinline__ PrimPair load_pp(const PrimPair* p) {
+    const Double4 u = ldg256(p), v = ldg256(reinterpret_cast<const char*>(p) + 32);
     PrimPair r;
-    r.p = 0.0; r.ip = 0.0; r.c = b.x; r.x = b.y; r.y = c.x; r.z = c.y;
-    r.cs = d.x; r.pad1 = 0.0;
+    r.x = u.a; r.y = u.b; r.z = u.c; r.cs = u.d;
+    r.p = v.a; r.ip = v.b; r.c = v.c; r.pad1 = 0.0;
+    return r;
+}
+
+// the fields the far-field (ss|ss) path reads: centre and cs
+__device__ __forceinline__ PrimPair load_pp_far(const PrimPair* p) {
+    const Double4 u = ldg256(p);
+    PrimPair r;
+    r.x = u.a; r.y = u.b; r.z = u.c; r.cs = u.d;
+    r.p = 0.0; r.ip = 0.0; r.c = 0.0; r.pad1 = 0.0;
     return r;
 }
 

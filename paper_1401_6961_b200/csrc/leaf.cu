@@ -752,6 +752,33 @@ __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double
     k_fixed_add(e.K + ((int64_t)row * e.nfn + col), v, e.S);
 }
 
+// Warp-combined K flush (HXF_KCOMBINE, north star item 4): the lanes of a warp whose
+// contribution goes to the same K element (the records of one (bra pair, ket row)
+// run share K[mu,lam] and K[nu,lam]) are summed first -- in fixed point, each value
+// already rounded as the direct path rounds it, so K stays bitwise the same -- and
+// one lane issues a single reduction per distinct element.  Called by all 32 lanes.
+__device__ __forceinline__ void k_add_warp(const EriArgs& e, bool on, int row, int col, double v) {
+    const int lane = threadIdx.x & 31;
+    long long fv = 0, key = -1 - lane;
+    if (on) {
+        fv = __double2ll_rn(ldexp(v, e.S));
+        key = (long long)row * e.nfn + col;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const bool leader = (__ffs(peers) - 1) == lane;
+    int rel = __popc(peers & ((1u << lane) - 1u));   // my position among my peers
+    unsigned rest = peers & (0xfffffffeu << lane);    // the peers above me
+    while (__any_sync(0xffffffffu, rest != 0)) {      // log2(largest group) steps
+        const int next = __ffs(rest);
+        const long long t = __shfl_sync(0xffffffffu, fv, next ? next - 1 : lane);
+        if (next) fv += t;
+        const bool done = rel & 1;
+        rest &= __ballot_sync(0xffffffffu, !done);
+        rel >>= 1;
+    }
+    if (leader && on && fv) atomicAdd(e.K + key, (unsigned long long)fv);
+}
+
 #ifndef HXF_ERI_MINB0
 #define HXF_ERI_MINB0 3
 #endif
@@ -796,6 +823,81 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
     extern __shared__ __align__(16) double s_tab[];
     if (!FAR) boys_eri_table_to_smem<E::L>(s_tab);
     long long nprim = 0, nq = 0;
+#ifdef HXF_KCOMBINE
+    // warp-uniform trip count: every lane reaches the combined flush
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - (threadIdx.x & 31) < e.n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = t < e.n ? e.rec[t] : 0ull;
+        const int mask = (int)((r >> 56) & 0xf);
+        int fi = 0, fj = 0, fk = 0, fl = 0;
+        double out[NI * NJ * NK * NL];
+        double half = -0.5;
+        if (mask) {
+            const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
+            const int4 ib = __ldg(e.binfo + pb), ik = __ldg(e.kinfo + pk);
+            const int nb = ib.w, nk = ik.w;
+            nprim += (long long)nb * nk;
+            nq += 1;
+            double3 A{0, 0, 0}, B{0, 0, 0}, C{0, 0, 0}, D{0, 0, 0};
+            if (LA | LB) { A = e.ctr[e.bpi[pb]]; B = e.ctr[e.bpj[pb]]; }
+            if (LC | LD) { C = e.ctr[e.kpi[pk]]; D = e.ctr[e.kpj[pk]]; }
+            E::template eval<FAR>(e.bpp + ib.z, nb, e.kpp + ik.z, nk, A, B, C, D, s_tab, out);
+            fi = ib.x; fj = ib.y; fk = ik.x; fl = ik.y;
+            if constexpr (LA == LC && LB == LD) half = ((r >> 60) & 1) ? -0.25 : -0.5;
+        }
+        const int64_t n = e.nfn;
+        const double* P = e.P;
+#define OUT(x, y, z, w) out[(((x) * NJ + (y)) * NK + (z)) * NL + (w)]
+        if (__any_sync(0xffffffffu, mask & 1)) {  // K[mu,sig] <- P[nu,lam]
+            const bool on = mask & 1;
+            for (int x = 0; x < NI; ++x)
+                for (int w = 0; w < NL; ++w) {
+                    double s = 0.0;
+                    if (on)
+                        for (int y = 0; y < NJ; ++y)
+                            for (int z = 0; z < NK; ++z) s += __ldg(P + (fj + y) * n + fk + z) * OUT(x, y, z, w);
+                    k_add_warp(e, on, fi + x, fl + w, half * s);
+                }
+        }
+        if (__any_sync(0xffffffffu, mask & 2)) {  // K[nu,sig] <- P[mu,lam]
+            const bool on = mask & 2;
+            for (int y = 0; y < NJ; ++y)
+                for (int w = 0; w < NL; ++w) {
+                    double s = 0.0;
+                    if (on)
+                        for (int x = 0; x < NI; ++x)
+                            for (int z = 0; z < NK; ++z) s += __ldg(P + (fi + x) * n + fk + z) * OUT(x, y, z, w);
+                    k_add_warp(e, on, fj + y, fl + w, half * s);
+                }
+        }
+        if (__any_sync(0xffffffffu, mask & 4)) {  // K[mu,lam] <- P[nu,sig]
+            const bool on = mask & 4;
+            for (int x = 0; x < NI; ++x)
+                for (int z = 0; z < NK; ++z) {
+                    double s = 0.0;
+                    if (on)
+                        for (int y = 0; y < NJ; ++y)
+                            for (int w = 0; w < NL; ++w) s += __ldg(P + (fj + y) * n + fl + w) * OUT(x, y, z, w);
+                    k_add_warp(e, on, fi + x, fk + z, half * s);
+                }
+        }
+        if (__any_sync(0xffffffffu, mask & 8)) {  // K[nu,lam] <- P[mu,sig]
+            const bool on = mask & 8;
+            for (int y = 0; y < NJ; ++y)
+                for (int z = 0; z < NK; ++z) {
+                    double s = 0.0;
+                    if (on)
+                        for (int x = 0; x < NI; ++x)
+                            for (int w = 0; w < NL; ++w) s += __ldg(P + (fi + x) * n + fl + w) * OUT(x, y, z, w);
+                    k_add_warp(e, on, fj + y, fk + z, half * s);
+                }
+        }
+#undef OUT
+    }
+#else
+    // (Measured and not kept, profiles/r02_ab_eri_memory.log: a software pipeline over the
+    // thread's records, L1 prefetch of the bra primitives, bra primitives two iterations
+    // ahead, more resident far-field blocks -- all +0.4 .. +3.4 % on the ERI stage.)
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < e.n;
          t += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t r = e.rec[t];
@@ -811,19 +913,34 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
             double3 A{0, 0, 0}, B{0, 0, 0}, C{0, 0, 0}, D{0, 0, 0};
             if (LA | LB) { A = e.ctr[e.bpi[pb]]; B = e.ctr[e.bpj[pb]]; }
             if (LC | LD) { C = e.ctr[e.kpi[pk]]; D = e.ctr[e.kpj[pk]]; }
+            const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
+            const int64_t n = e.nfn;
+            const double* P = e.P;
+            // (ss|ss): the four density elements are requested before the primitive loops
+            double pv[4] = {0.0, 0.0, 0.0, 0.0};
+            if constexpr (NI * NJ * NK * NL == 1) {
+                if (mask & 1) pv[0] = __ldg(P + fj * n + fk);
+                if (mask & 2) pv[1] = __ldg(P + fi * n + fk);
+                if (mask & 4) pv[2] = __ldg(P + fj * n + fl);
+                if (mask & 8) pv[3] = __ldg(P + fi * n + fl);
+            }
 #ifdef HXF_EXP_NOPRIM  // timing experiment: skip the primitive loops (results wrong)
             for (int q = 0; q < NI * NJ * NK * NL; ++q) out[q] = e.bpp[ib.z].c * e.kpp[ik.z].c;
 #else
             E::template eval<FAR>(e.bpp + ib.z, nb, e.kpp + ik.z, nk, A, B, C, D, s_tab, out);
 #endif
-            const int fi = ib.x, fj = ib.y, fk = ik.x, fl = ik.y;
-            const int64_t n = e.nfn;
-            const double* P = e.P;
             // -1/2 exchange factor; eightfold: the self-mirror quartet (bra pair ==
             // ket pair, record bit 60, only in classes with bra class == ket class)
             // enters A once and K = A + A^T, so it carries 1/2
             double half = -0.5;
             if constexpr (LA == LC && LB == LD) half = ((r >> 60) & 1) ? -0.25 : -0.5;
+            if constexpr (NI * NJ * NK * NL == 1) {
+                const double v = half * out[0];
+                if (mask & 1) k_add(e, fi, fl, pv[0] * v);
+                if (mask & 2) k_add(e, fj, fl, pv[1] * v);
+                if (mask & 4) k_add(e, fi, fk, pv[2] * v);
+                if (mask & 8) k_add(e, fj, fk, pv[3] * v);
+            } else {
 #define OUT(x, y, z, w) out[(((x) * NJ + (y)) * NK + (z)) * NL + (w)]
             if (mask & 1) {  // K[mu,sig] <- P[nu,lam]
                 for (int x = 0; x < NI; ++x)
@@ -862,8 +979,10 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
                     }
             }
 #undef OUT
+            }
         }
     }
+#endif
     nq = warp_sum_ll(nq);
     nprim = warp_sum_ll(nprim);
     if ((threadIdx.x & 31) == 0 && nprim) {
