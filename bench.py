@@ -415,13 +415,19 @@ def native_arm(args):
     _native.check(_native.lib().hxf_fp64_peak(ctypes.byref(peak), _native.current_stream()))
 
     shards = None
+    plan_ms = None
     if world > 1:
         P_tree0 = hx.build_matrix_tree(P_dev, part)
         # once per geometry + density (an SCF reuses it across iterations): hashed task
         # groups, costs from counters-only builds (each rank measures 1/world of
         # them), longest-first onto ranks
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
         shards = distributed.plan(pairs, pairs, P_tree0, cfg.tau_2e, "schwarz", sym, world,
                                   strategy="balanced", K_scratch=K_dev)
+        torch.cuda.synchronize()
+        plan_ms = 1e3 * (time.perf_counter() - t0)
         del P_tree0
 
     def step(P_src):
@@ -481,7 +487,7 @@ def native_arm(args):
         lv, rng = shards
         shard = (lv,) + tuple(rng[rank])
     _, craw, _ = exchange.run_exchange(pairs, pairs, P_tree, cfg.tau_2e, "schwarz", sym, True, None,
-                                       K_out=K_dev, shard=shard, symmetrize=not (world > 1))
+                                       K_out=K_dev, shard=shard, symmetrize=not (world > 1), screen_bytes=True)
     tm = exchange.last_timings()
     flops = eri_flops(craw)
     flops_exec = eri_flops_executed(craw)
@@ -509,7 +515,8 @@ def native_arm(args):
             e2e_times.append(1e3 * (time.perf_counter() - t0))
             del Pt
             assert c_e2e.eri_shell_quartets == quartets
-        del P_np, K_np
+        del P_np
+        K_np = None
         e2e_api = "drop-in: build_matrix_tree(numpy P) + build_exchange_" + \
             {"naive": "naive", "fourfold": "symmetric", "eightfold": "eightfold"}[args.mode] + \
             " -> numpy K (pageable host buffers)"
@@ -569,7 +576,7 @@ def native_arm(args):
             cpu, port = port, None
 
     if rank == 0:
-        stage_med = [statistics.median([s[k] for s in stage]) for k in range(6)] if stage else tm
+        stage_med = [statistics.median([s[k] for s in stage]) for k in range(7)] if stage else tm
         nt = ncu_traffic(args.config, args.mode) if world == 1 else None
         hbm = hbm_peak()
         # traversal: SURVEY 8(d) algorithmic bytes per visited task (naive 48 B, symmetric 104 B)
@@ -582,6 +589,30 @@ def native_arm(args):
                      "bytes_basis": f"algorithmic: {bpt} B per visited task (SURVEY 8(d)) x tasks_visited",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy test)",
                      "traffic_source": nt["file"] if nt else None}
+        # leaf screen: SURVEY 8(d) algorithmic bytes (Q of both pair lists + the |P| block of
+        # every live slot per leaf task, counted by the kernel) + the 8-byte record and 2-byte
+        # key written per surviving quartet, over the screen's device time
+        screen_bytes = int(craw.screen_bytes) + 10 * int(craw.eri_shell_quartets)
+        screen_gbs = screen_bytes / (stage_med[1] * 1e-3) / 1e9 if stage_med[1] > 0 else None
+        scr_traffic = (nt.get("k_screen2") or nt.get("k_screen") or {}).get("dram_bytes_per_build") if nt else None
+        roof_screen = {"bound": "hbm", "achieved": screen_gbs, "peak": hbm, "unit": "GB/s",
+                       "frac": screen_gbs / hbm if (screen_gbs and hbm) else None,
+                       "traffic": scr_traffic,
+                       "kernel": "k_screen2 (hierarchical leaf screen), all chunks",
+                       "bytes_basis": "algorithmic: 8 (m_bra + m_ket) B of Q + 8 n_row n_col B of |P| per live slot "
+                                      "per leaf task (SURVEY 8(d), counted on the device: screen_bytes) "
+                                      "+ 10 B per surviving quartet (record + sort key)",
+                       "bytes_per_step_rank0": screen_bytes,
+                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy test)",
+                       "traffic_source": nt["file"] if nt else None,
+                       "note": "the node vectors and |P| blocks the screen gathers are L2-resident and the "
+                               "kernel is instruction-issue bound (ncu: issue active 66 %, DRAM ~130 GB/s), "
+                               "so the HBM fraction is low by construction; see DESIGN.md"}
+        roof_trav["dram_gbs_ncu"] = (roof_trav["traffic"] / (stage_med[0] * 1e-3) / 1e9
+                                     if (roof_trav["traffic"] and stage_med[0] > 0) else None)
+        roof_trav["note"] = ("achieved = algorithmic bytes / stage time; the node arrays are L2-resident, so the "
+                             "DRAM rate ncu measures (dram_gbs_ncu) is ~20x lower and the kernel is issue-bound: "
+                             "not an HBM utilisation")
         line = {
             "metric": METRIC, "value": value, "unit": "quartets/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -595,7 +626,8 @@ def native_arm(args):
             "prim_quartets_per_step": last.prim_quartets,
             "stage_ms": {"traversal": stage_med[0], "leaf_screen": stage_med[1],
                          "eri_stage": stage_med[2], "epilogue": stage_med[3],
-                         "exchange_total": stage_med[4], "eri_kernels": stage_med[5]},
+                         "exchange_total": stage_med[4], "eri_kernels": stage_med[5],
+                         "far_classify_and_sort": stage_med[6]},
             "pair_tree_ms": pair_ms, "input_gen_s": gen_s,
             "counters": last.to_dict() | {"ties_task": last.ties_task, "ties_leaf": last.ties_leaf},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
@@ -616,6 +648,8 @@ def native_arm(args):
                                   "flops_basis": "executed FP64 (dadd + dmul + 2 dfma) per primitive quartet "
                                                  "per class from ncu, profiles/r01_eri_fp64_executed.json"},
             "roofline_traversal": roof_trav,
+            "roofline_screen": roof_screen,
+            "plan_ms": plan_ms,
             "e2e": {"value": e2e_value, "unit": "quartets/s",
                     "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8,
                     "ms_per_step": float(et.item()) / max(args.e2e_steps, 1), "api": e2e_api},

@@ -71,7 +71,31 @@ typedef struct hxf_counters {
     int64_t class_quartets[16];      /* evaluated shell quartets per (li,lj,lk,ll) class */
     int64_t class_prim_quartets[16]; /* primitive quartets per class                    */
     double culled_bound_ledger;
+    /* leaf screen, algorithmic bytes: per leaf task 8 (m_bra + m_ket)
+       of Q plus 8 n_row n_col of the |P| block per live slot; filled only when
+       hxf_exchange_opts.count_screen_bytes is set */
+    int64_t screen_bytes;
 } hxf_counters;
+
+/* One culling comparison whose bound lies within 1e-12 (relative) of its threshold
+ * (BASELINE north star: "such ties must be logged").  The
+ * device takes the decision the reference's rule gives for its own bound; a tie is
+ * where a bound computed a few ulps differently could decide the other way. */
+#define HXF_TIE_TASK 0      /* traversal: (lo*mid)*hi <= tau (exchange_naive.py:68-88)   */
+#define HXF_TIE_LEAF 1      /* leaf quartet: (f(Q_ij)|P|)f(Q_kl) > tau (:156-182)        */
+#define HXF_TIE_OVERLAP 2   /* pair-tree pruning: block max |S| < tau_ovlp (quadtree.py:296-299) */
+typedef struct hxf_tie_record {
+    int32_t stage;         /* HXF_TIE_*                                               */
+    int32_t level;         /* task / overlap: partition level of the node(s); leaf: -1 */
+    int32_t slot;          /* fourfold slot g (0: naive, overlap)                      */
+    int32_t decision;      /* 1: kept / expanded / live, 0: culled / pruned            */
+    int32_t id[4];         /* task: level-local span indices mu,nu,lam,sig; leaf: shell
+                              ids i,j,k,l; overlap: level-local span indices r,c,-1,-1 */
+    double bound;
+    double threshold;
+    double contribution;   /* task / leaf: upper bound on the K change a flipped decision
+                              could cause (= bound); overlap: the block max |S|        */
+} hxf_tie_record;
 
 /* Exchange options.  The shard fields select a subset of the product-tree
  * tasks at level `shard_level` (tasks [shard_begin, shard_end) of that
@@ -122,6 +146,17 @@ typedef struct hxf_exchange_opts {
        indices fn - fn_lo).  K_fixed requires the tree root. */
     int root_level;
     int root_index;
+    /* Tie records of this build (task and leaf stages): NULL, or a host array of
+       tie_capacity records; *tie_count (may be NULL) receives the number of ties
+       found, which may exceed the capacity.  The counters' ties_task / ties_leaf
+       are filled either way.  Overlap-stage ties belong to the pair tree:
+       hxf_pairs_ties. */
+    hxf_tie_record* tie_log;
+    int64_t tie_capacity;
+    int64_t* tie_count;
+    /* != 0: also fill counters.screen_bytes (one extra pass over the leaf task list;
+       a measurement aid for the leaf-screen roofline, off in normal builds) */
+    int count_screen_bytes;
 } hxf_exchange_opts;
 
 const char* hxf_last_error(void);
@@ -244,6 +279,11 @@ int hxf_block_pack(const int64_t* K, int n, int bs, const uint8_t* mask, const i
 int hxf_block_unpack(int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, const int64_t* buf,
                      void* stream);
 
+/* Overlap-pruning ties of a pair tree: nodes whose block max |S| lies within 1e-12
+ * (relative) of tau_ovlp, found when the tree was built.  Copies up to `capacity`
+ * records (out may be NULL) and sets *count to the number found. */
+int hxf_pairs_ties(const hxf_pairs* p, hxf_tie_record* out, int64_t capacity, int64_t* count);
+
 /* Number of kernels libhxf has launched in this process (work evidence). */
 int hxf_launch_count(int64_t* n);
 
@@ -254,8 +294,9 @@ int hxf_launch_count(int64_t* n);
 int hxf_scratch_release(int64_t* bytes);
 
 /* Device timing of the last hxf_exchange on this thread (ms per stage):
- * [0] traversal, [1] leaf screen, [2] ERI stage (sort + ERI kernels), [3] epilogue,
- * [4] total, [5] ERI + contraction kernels only. */
+ * [0] traversal, [1] leaf screen, [2] ERI stage (far-field classification + sort +
+ * ERI kernels), [3] epilogue, [4] total, [5] ERI + contraction kernels only,
+ * [6] far-field classification + survivor sort + key bounds. */
 int hxf_last_timings(double* ms, int n);
 
 #ifdef __cplusplus

@@ -20,7 +20,7 @@ HXF_OK, HXF_EINVAL, HXF_ELOGIC, HXF_ECUDA, HXF_ENOMEM = 0, 1, 2, 3, 4
 NCASES = 9
 
 EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_destroy",
-            "hxf_system_info", "hxf_pairs_build", "hxf_pairs_build_ovlp", "hxf_pairs_destroy", "hxf_pairs_download",
+            "hxf_system_info", "hxf_pairs_build", "hxf_pairs_build_ovlp", "hxf_pairs_destroy", "hxf_pairs_ties", "hxf_pairs_download",
             "hxf_pairs_download_q", "hxf_pairs_overlap", "hxf_density_build",
             "hxf_density_destroy", "hxf_density_download", "hxf_density_download_pmax", "hxf_exchange", "hxf_exchange_direct", "hxf_frontier",
             "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count",
@@ -51,7 +51,29 @@ class Counters(ctypes.Structure):
                 ("prim_quartets", ctypes.c_int64),
                 ("class_quartets", ctypes.c_int64 * 16),
                 ("class_prim_quartets", ctypes.c_int64 * 16),
-                ("culled_bound_ledger", ctypes.c_double)]
+                ("culled_bound_ledger", ctypes.c_double),
+                ("screen_bytes", ctypes.c_int64)]
+
+
+TIE_STAGES = ("task", "leaf", "overlap")
+
+
+class TieRecord(ctypes.Structure):
+    """hxf_tie_record: one culling comparison within 1e-12 relative of its threshold."""
+    _fields_ = [("stage", ctypes.c_int32),
+                ("level", ctypes.c_int32),
+                ("slot", ctypes.c_int32),
+                ("decision", ctypes.c_int32),
+                ("id", ctypes.c_int32 * 4),
+                ("bound", ctypes.c_double),
+                ("threshold", ctypes.c_double),
+                ("contribution", ctypes.c_double)]
+
+    def to_dict(self):
+        return {"stage": TIE_STAGES[self.stage], "level": int(self.level), "slot": int(self.slot),
+                "decision": "kept" if self.decision else "culled", "ids": tuple(int(v) for v in self.id),
+                "bound": float(self.bound), "threshold": float(self.threshold),
+                "contribution": float(self.contribution)}
 
 
 class ExchangeOpts(ctypes.Structure):
@@ -75,7 +97,11 @@ class ExchangeOpts(ctypes.Structure):
                 ("shard_stride", ctypes.c_int64),
                 ("shard_mask", ctypes.POINTER(ctypes.c_uint8)),
                 ("root_level", ctypes.c_int),
-                ("root_index", ctypes.c_int)]
+                ("root_index", ctypes.c_int),
+                ("tie_log", ctypes.POINTER(TieRecord)),
+                ("tie_capacity", ctypes.c_int64),
+                ("tie_count", ctypes.POINTER(ctypes.c_int64)),
+                ("count_screen_bytes", ctypes.c_int)]
 
 
 _lib = None
@@ -102,6 +128,7 @@ def lib():
     L.hxf_pairs_build_ovlp.argtypes = [vp, dbl, vp, i32, vp, P(vp)]
     L.hxf_pairs_destroy.argtypes = [vp]
     L.hxf_pairs_destroy.restype = None
+    L.hxf_pairs_ties.argtypes = [vp, P(TieRecord), i64, P(i64)]
     L.hxf_pairs_download.argtypes = [vp, i32, vp, vp, vp, vp]
     L.hxf_pairs_download_q.argtypes = [vp, vp]
     L.hxf_pairs_overlap.argtypes = [vp, vp]

@@ -320,6 +320,15 @@ void hxf_pairs_destroy(hxf_pairs* p) {
     delete p;
 }
 
+int hxf_pairs_ties(const hxf_pairs* p, hxf_tie_record* out, int64_t capacity, int64_t* count) {
+    HXF_TRY({
+        if (!p) throw HxfError{HXF_EINVAL, "NULL pair tree"};
+        if (count) *count = p->n_ovlp_ties;
+        if (out)
+            for (int64_t k = 0; k < capacity && k < (int64_t)p->ovlp_ties.size(); ++k) out[k] = p->ovlp_ties[k];
+    })
+}
+
 int hxf_pairs_download(const hxf_pairs* p, int level, double* norm, double* rowsum, double* colsum,
                        uint8_t* pruned) {
     HXF_TRY({

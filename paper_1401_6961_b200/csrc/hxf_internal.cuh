@@ -1,6 +1,7 @@
 // Internal types and device helpers shared by the hxf translation units.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -109,6 +110,8 @@ struct hxf_pairs {
     float* gip;        // per pair: max 1/p over its primitives (rounded up)
     double* eS;        // per entry of epp: primitive Schwarz factor sqrt(max_comp (ab|ab))
     double smax_prim;  // max eS
+    std::vector<hxf_tie_record> ovlp_ties;   // overlap-pruning ties found at build (first 4096)
+    int64_t n_ovlp_ties = 0;
     int* ncid;         // per leaf pair node (nleaf^2): compact live-node id, -1 if pruned
     double* nvec;      // per live node: NVEC doubles, row/col max Q and row/col sums of sqrt(Q)
     double* nvec_tri;  // per leaf span (diagonal node, canonical x <= y pairs): the same vectors
@@ -365,13 +368,58 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
     return v;
 }
 
+// ---------------------------------------------------------------- NVTX
+// Stage ranges for timeline tools (header-only nvtx3: no library, no cost unless a
+// tool is attached): pair tree, density tree, traversal, leaf screen, ERI stage, epilogue.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// ---------------------------------------------------------------- tie records
+// Bounded device log of culling comparisons within 1e-12 (relative) of their
+// threshold (hxf_tie_record, include/hxf.h).  Ties are rare: the append is one
+// atomic on the cold path of the comparison; count == NULL disables it.
+struct TieLog {
+    hxf_tie_record* rec;
+    unsigned long long* count;
+    long long cap;
+};
+
+// (never inlined: the hot kernels keep their register budgets; ties are rare)
+static __device__ __noinline__ void tie_emit(TieLog tl, int stage, int level, int slot, bool kept, int a,
+                                      int b, int c, int d, double bound, double thr) {
+    if (!tl.count) return;
+    const unsigned long long pos = atomicAdd(tl.count, 1ull);
+    if ((long long)pos < tl.cap) {
+        hxf_tie_record r;
+        r.stage = stage; r.level = level; r.slot = slot; r.decision = kept ? 1 : 0;
+        r.id[0] = a; r.id[1] = b; r.id[2] = c; r.id[3] = d;
+        r.bound = bound; r.threshold = thr; r.contribution = bound;
+        tl.rec[pos] = r;
+    }
+}
+
 // counter slots in the device counter array
 enum {
     C_VISITED = 0, C_CULL_SCREEN, C_CULL_ABSENT, C_LEAF, C_ERIQ, C_CULL_LEAF, C_EXPANDED,
     C_SPAWNED, C_LINK_SCREEN, C_LINK_ABSENT, C_CASE0, C_CASELEAF0 = C_CASE0 + HXF_NCASES,
     C_TIE_TASK = C_CASELEAF0 + HXF_NCASES, C_TIE_LEAF, C_PRIMQ, C_OVERFLOW, C_CLSQ0,
-    C_CLSPQ0 = C_CLSQ0 + 16, C_DBG0 = C_CLSPQ0 + 16, C_NCOUNTERS = C_DBG0 + 8
+    C_CLSPQ0 = C_CLSQ0 + 16, C_DBG0 = C_CLSPQ0 + 16, C_SCREEN_BYTES = C_DBG0 + 8,
+    C_NCOUNTERS = C_SCREEN_BYTES + 1
 };
+
+// Device-side bounds checks (build with -DHXF_DEBUG_BOUNDS; compute-sanitizer is not
+// available on the GPU pool): a failed check counts in counters[C_OVERFLOW] and the
+// access is skipped; the build then fails with HXF_ELOGIC.  Off: no code.
+#ifdef HXF_DEBUG_BOUNDS
+#define HXF_BCHECK(cond, counters) \
+    ((cond) ? true : (atomicAdd(reinterpret_cast<unsigned long long*>(&(counters)[C_OVERFLOW]), 1ull), false))
+#else
+#define HXF_BCHECK(cond, counters) true
+#endif
 
 // kernels launched by the library (evidence that the device path ran)
 void note_launch(int n = 1);

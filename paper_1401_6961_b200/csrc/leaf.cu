@@ -76,6 +76,12 @@ struct ScreenArgs {
     const int* ncidk;
     const double* nveck;
     const double* nveck_tri;
+    const int* bpi;           // shells of the bra / ket pair ids (tie records)
+    const int* bpj;
+    const int* kpi;
+    const int* kpj;
+    TieLog ties;
+    int64_t n_bpairs, n_kpairs;   // pair table sizes (HXF_DEBUG_BOUNDS checks)
 };
 
 // Far field (ERI key bit 12): every primitive quartet of a shell quartet has
@@ -99,6 +105,12 @@ struct Slab {
     unsigned long long base;
     int used;
 };
+
+// a leaf-stage tie: shell ids from the pair ids (cold path, not inlined)
+static __device__ __noinline__ void tie_emit_leaf(TieLog tl, const int* bpi, const int* bpj, const int* kpi, const int* kpj,
+                                           int64_t pa, int64_t pk, int slot, double bound, double tau) {
+    tie_emit(tl, HXF_TIE_LEAF, -1, slot, bound > tau, bpi[pa], bpj[pa], kpi[pk], kpj[pk], bound, tau);
+}
 
 template <typename Args>
 __device__ __forceinline__ void slab_pad(const Slab& s, const Args& a, int lane) {
@@ -124,6 +136,8 @@ __device__ __forceinline__ void slab_emit(Slab& s, const Args& a, unsigned bal, 
     }
     if (keep) {
         const unsigned long long pos = s.base + s.used + __popc(bal & ((1u << lane) - 1u));
+        HXF_BCHECK((int64_t)(rec & 0xfffffff) < a.n_bpairs && (int64_t)((rec >> 28) & 0xfffffff) < a.n_kpairs,
+                   a.counters);
         if ((int64_t)pos < a.cap) {
             a.rec[pos] = rec;
             a.keys[pos] = key;
@@ -149,7 +163,9 @@ __device__ __forceinline__ void tri_decode(int a, int n, int* x, int* y) {
 // The path for partitions whose leaf spans exceed the staged screen's 10
 // shells, and the A/B reference of k_screen2 (HXF_SCREEN=flat); same
 // decisions, counters and ledger.
-template <bool SYM, bool EMIT, bool EIGHT = false>
+// TIES: the diagnostic instantiation that also appends tie records (second pass, run
+// only when a build counted leaf ties and the caller asked for the log).
+template <bool SYM, bool EMIT, bool EIGHT = false, bool TIES = false>
 __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = blockIdx.x * (int64_t)SCREEN_WARPS + (threadIdx.x >> 5);
@@ -202,7 +218,10 @@ __global__ void __launch_bounds__(SCREEN_WARPS * 32) k_screen(ScreenArgs a) {
                         if (!((live >> g) & 1)) continue;
                         const double pm = __ldg(a.pmax + (int64_t)(rs[g] + rowv[g]) * a.ns + cs[g] + colv[g]);
                         const double bound = __dmul_rn(__dmul_rn(fa, pm), fb);
-                        n_tie += bound >= tie_lo && bound <= tie_hi && a.tau > 0.0;
+                        if (bound >= tie_lo && bound <= tie_hi && a.tau > 0.0) {
+                            ++n_tie;
+                            if (TIES) tie_emit_leaf(a.ties, a.bpi, a.bpj, a.kpi, a.kpj, pa, pb, g, bound, a.tau);
+                        }
                         if (bound > a.tau) {
                             keep_any = true;
                             mask |= 1 << g;
@@ -720,6 +739,28 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
     }
 }
 
+// Leaf-screen algorithmic bytes: per leaf task 8 (m_bra + m_ket) B of Q
+// plus 8 n_row n_col B of the |P| block per live slot.  A measurement pass over the leaf
+// task list (hxf_exchange_opts.count_screen_bytes), not part of a normal build.
+__global__ void k_screen_bytes(const uint64_t* tasks, int64_t n, const int* lslo, const int* lshi, int sym,
+                               long long* counters) {
+    long long b = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t task = tasks[t];
+        const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
+                  sig = (task >> 45) & 0x7fff;
+        const int live = sym ? (int)(task >> 60) : 1;
+        const int nmu = lshi[mu] - lslo[mu], nnu = lshi[nu] - lslo[nu], nlam = lshi[lam] - lslo[lam],
+                  nsig = lshi[sig] - lslo[sig];
+        const long long ma = (sym && mu == nu) ? nmu * (nmu + 1) / 2 : nmu * nnu;
+        const long long mb = (sym && lam == sig) ? nlam * (nlam + 1) / 2 : nlam * nsig;
+        b += 8 * (ma + mb) + 8 * (((live & 1) ? nnu * nlam : 0) + ((live & 2) ? nmu * nlam : 0) +
+                                  ((live & 4) ? nnu * nsig : 0) + ((live & 8) ? nmu * nsig : 0));
+    }
+    b = warp_sum_ll(b);
+    if ((threadIdx.x & 31) == 0 && b) atomic_add_ll(&counters[C_SCREEN_BYTES], b);
+}
+
 struct EriArgs {
     const uint64_t* rec;
     int64_t n;
@@ -741,6 +782,7 @@ struct EriArgs {
     unsigned long long* K;
     long long* counters;
     const int64_t* dbounds;  // non-NULL: this class's record range is read on the device
+    int64_t n_bpairs, n_kpairs, n_bprim, n_kprim;   // table sizes (HXF_DEBUG_BOUNDS checks)
 };
 
 __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double v) {
@@ -749,6 +791,7 @@ __device__ __forceinline__ void k_add(const EriArgs& e, int row, int col, double
     if (v == 1.2345) e.K[0] = 1;
     return;
 #endif
+    if (!HXF_BCHECK(row >= 0 && row < e.nfn && col >= 0 && col < e.nfn, e.counters)) return;
     k_fixed_add(e.K + ((int64_t)row * e.nfn + col), v, e.S);
 }
 
@@ -904,9 +947,14 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
         const int mask = (int)((r >> 56) & 0xf);
         if (mask) {
             const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
+            if (!HXF_BCHECK(pb < e.n_bpairs && pk < e.n_kpairs, e.counters)) continue;
             // one 16-byte record per pair: function offsets, primitive-pair range
             const int4 ib = __ldg(e.binfo + pb), ik = __ldg(e.kinfo + pk);
             const int nb = ib.w, nk = ik.w;
+            if (!HXF_BCHECK(nb >= 1 && nk >= 1 && ib.z >= 0 && ik.z >= 0 && (int64_t)ib.z + nb <= e.n_bprim &&
+                                (int64_t)ik.z + nk <= e.n_kprim,
+                            e.counters))
+                continue;
             nprim += (long long)nb * nk;
             nq += 1;
             double out[NI * NJ * NK * NL];
@@ -1229,7 +1277,8 @@ struct Timer {
 // kernels over the sorted copy, without a host synchronisation: every class
 // kernel reads its record range from the device-side key bounds (empty classes
 // exit at once)
-void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cudaStream_t st) {
+void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cudaStream_t st,
+                            cudaEvent_t after_sort = nullptr) {
     if (b.bgeo && !HXF_ERI_NOFAR) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -1241,6 +1290,7 @@ void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cuda
     size_t tb = b.sort_tb;
     HXF_CUDA(cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, KEY_BITS, st));
     { k_key_bounds<<<KEY_RANGES / 256 + 1, 256, 0, st>>>(b.keys2, nrec, b.dbounds); note_launch(); }
+    if (after_sort) cudaEventRecord(after_sort, st);
     e.rec = b.rec2;
     e.n = 0;
     e.dbounds = b.dbounds;
@@ -1338,6 +1388,7 @@ int hxf_last_timings_impl(double* ms, int n) {
 
 int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_exchange_opts* o,
                  double* K_out, hxf_counters* out, cudaStream_t st) {
+    NvtxRange nvtx_build("hxf: exchange build");
     hxf_system* s = bra->sys;
     if (ket->sys != s || dens->sys != s)
         throw HxfError{HXF_EINVAL, "bra, ket and P must be built over the same partition"};
@@ -1356,6 +1407,15 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     unsigned long long* dledger = lalloc<unsigned long long>(LEDGER_LIMBS, st);
     HXF_CUDA(cudaMemsetAsync(dcount, 0, C_NCOUNTERS * sizeof(long long), st));
     HXF_CUDA(cudaMemsetAsync(dledger, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
+
+    // tie records (task and leaf stages): bounded device log, copied out at the end
+    TieLog tl{nullptr, nullptr, 0};
+    if (o->tie_log || o->tie_count) {
+        tl.cap = o->tie_log ? std::max<int64_t>(o->tie_capacity, 0) : 0;
+        tl.rec = lalloc<hxf_tie_record>(std::max<long long>(tl.cap, 1), st);
+        tl.count = lalloc<unsigned long long>(1, st);
+        HXF_CUDA(cudaMemsetAsync(tl.count, 0, sizeof(unsigned long long), st));
+    }
 
     // ---- traversal
     Timer ttrav(st);
@@ -1384,6 +1444,22 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     HXF_CUDA(cudaMemcpyAsync(hc, dcount, sizeof(hc), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaMemcpyAsync(hl, dledger, sizeof(hl), cudaMemcpyDeviceToHost, st));
     HXF_CUDA(cudaStreamSynchronize(st));
+    if (tl.count && hc[C_TIE_TASK] > 0) {
+        // task-stage tie records: the traversal once more with the logging kernels
+        // (counters and ledger into scratch); off the timed path of a tie-free build
+        NvtxRange nvtx_ties("hxf: tie records (task stage)");
+        long long* c2 = lalloc<long long>(C_NCOUNTERS, st);
+        unsigned long long* l2 = lalloc<unsigned long long>(LEDGER_LIMBS, st);
+        HXF_CUDA(cudaMemsetAsync(c2, 0, C_NCOUNTERS * sizeof(long long), st));
+        HXF_CUDA(cudaMemsetAsync(l2, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
+        TravInput t2 = ti;
+        t2.counters = c2;
+        t2.ledger = l2;
+        t2.ties = tl;
+        TraversalResult r2 = traverse(t2, st);
+        for (void* p : {(void*)c2, (void*)l2, (void*)r2.leaf, (void*)r2.frontier})
+            if (p) hxf_cache_free(p, st);
+    }
 
     ScreenArgs sa;
     sa.tasks = tr.leaf;
@@ -1430,6 +1506,13 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     sa.nfn = s->nfn;
     sa.tau = o->tau_2e;
     sa.mode = o->mode;
+    sa.bpi = bra->pi;
+    sa.bpj = bra->pj;
+    sa.kpi = ket->pi;
+    sa.kpj = ket->pj;
+    sa.ties = tl;
+    sa.n_bpairs = bra->n_pairs;
+    sa.n_kpairs = ket->n_pairs;
 
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, s->device);
@@ -1575,6 +1658,10 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         e.S = S;
         e.K = Kfx;
         e.counters = ecount;
+        e.n_bpairs = bra->n_pairs;
+        e.n_kpairs = ket->n_pairs;
+        e.n_bprim = bra->n_prim_pairs;
+        e.n_kprim = ket->n_prim_pairs;
         cudaStream_t se = st;
         cudaEvent_t ev_in = nullptr, ev_scr[2] = {nullptr, nullptr}, ev_eri[2] = {nullptr, nullptr};
         if (pipe) {
@@ -1592,6 +1679,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             HXF_CUDA(cudaStreamWaitEvent(se, ev_in, 0));
         }
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> eri_ev;
+        std::vector<cudaEvent_t> sort_ev;   // after classification + sort + key bounds, per chunk
         bool used[2] = {false, false};
         int cur = 0;
         int64_t chunk = std::max<int64_t>(1, cap / 1024);
@@ -1612,7 +1700,9 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sa.fill = bfill[cur];
             sa.counters = bcount[cur];
             sa.ledger = bledger[cur];
+            nvtxRangePushA("hxf: leaf screen");
             launch_screen(true);
+            nvtxRangePop();
             HXF_CUDA(cudaGetLastError());
             unsigned long long fill = 0;
             long long c2[C_NCOUNTERS];
@@ -1638,10 +1728,15 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                     HXF_CUDA(cudaEventRecord(ev_scr[cur], st));
                     HXF_CUDA(cudaStreamWaitEvent(se, ev_scr[cur], 0));
                 }
+                cudaEvent_t es;
+                cudaEventCreate(&es);
                 HXF_CUDA(cudaEventRecord(ea, se));
-                eri_sorted_stage_async(e, sb[cur], nrec, se);
+                nvtxRangePushA("hxf: ERI stage");
+                eri_sorted_stage_async(e, sb[cur], nrec, se, es);
+                nvtxRangePop();
                 HXF_CUDA(cudaEventRecord(eb, se));
                 eri_ev.push_back({ea, eb});
+                sort_ev.push_back(es);
                 if (want_log)
                     { k_log<<<(unsigned)((nrec + 255) / 256), 256, 0, se>>>(sb[cur].rec2, nrec, bra->pi, bra->pj, ket->pi,
                                                                         ket->pj, dlog, o->log_capacity, dlogfill); note_launch(); }
@@ -1665,13 +1760,16 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             HXF_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
         }
         HXF_CUDA(cudaStreamSynchronize(se));
-        for (auto& pr : eri_ev) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, pr.first, pr.second);
-            g_timings[2] += ms;
-            g_timings[5] += ms;
-            cudaEventDestroy(pr.first);
-            cudaEventDestroy(pr.second);
+        for (size_t k = 0; k < eri_ev.size(); ++k) {
+            float ms = 0.f, ms_sort = 0.f;
+            cudaEventElapsedTime(&ms, eri_ev[k].first, eri_ev[k].second);
+            cudaEventElapsedTime(&ms_sort, eri_ev[k].first, sort_ev[k]);
+            g_timings[2] += ms;             // the whole ERI stage
+            g_timings[5] += ms - ms_sort;   // ERI + contraction kernels only
+            g_timings[6] += ms_sort;        // far-field classification + sort + key bounds
+            cudaEventDestroy(eri_ev[k].first);
+            cudaEventDestroy(eri_ev[k].second);
+            cudaEventDestroy(sort_ev[k]);
         }
         long long ce[C_NCOUNTERS];
         HXF_CUDA(cudaMemcpyAsync(ce, ecount, sizeof(ce), cudaMemcpyDeviceToHost, st));
@@ -1698,7 +1796,41 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         hxf_cache_free(ecount, st);
     }
 
+    if (o->count_screen_bytes && tr.n_leaf) {
+        HXF_CUDA(cudaMemsetAsync(scount, 0, C_NCOUNTERS * sizeof(long long), st));
+        k_screen_bytes<<<(unsigned)std::min<int64_t>((tr.n_leaf + 255) / 256, (int64_t)dev_sms * 16), 256, 0, st>>>(
+            tr.leaf, tr.n_leaf, d_lslo, d_lshi, sym, scount);
+        note_launch();
+        long long c2[C_NCOUNTERS];
+        HXF_CUDA(cudaMemcpyAsync(c2, scount, sizeof(c2), cudaMemcpyDeviceToHost, st));
+        HXF_CUDA(cudaStreamSynchronize(st));
+        acc_c[C_SCREEN_BYTES] = c2[C_SCREEN_BYTES];
+    }
+    if (tl.count && acc_c[C_TIE_LEAF] > 0 && tr.n_leaf) {
+        // leaf-stage tie records: the per-quartet screen once more over every leaf task
+        // with the logging instantiation (no emission, counters and ledger into scratch)
+        NvtxRange nvtx_ties("hxf: tie records (leaf stage)");
+        HXF_CUDA(cudaMemsetAsync(scount, 0, C_NCOUNTERS * sizeof(long long), st));
+        HXF_CUDA(cudaMemsetAsync(sledger, 0, LEDGER_LIMBS * sizeof(unsigned long long), st));
+        sa.t0 = 0;
+        sa.t1 = tr.n_leaf;
+        sa.rec = nullptr;
+        sa.keys = nullptr;
+        sa.cap = 0;
+        sa.fill = dfill;
+        sa.counters = scount;
+        sa.ledger = sledger;
+        const unsigned g = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>((tr.n_leaf + SCREEN_WARPS - 1) / SCREEN_WARPS, (int64_t)dev_sms * 8));
+        if (eight) k_screen<true, false, true, true><<<g, SCREEN_WARPS * 32, 0, st>>>(sa);
+        else if (sym) k_screen<true, false, false, true><<<g, SCREEN_WARPS * 32, 0, st>>>(sa);
+        else k_screen<false, false, false, true><<<g, SCREEN_WARPS * 32, 0, st>>>(sa);
+        note_launch();
+        HXF_CUDA(cudaGetLastError());
+    }
+
     // ---- epilogue
+    NvtxRange nvtx_epilogue("hxf: epilogue");
     Timer tep(st);
     if (eight && Kfx) {  // K = A + A^T, exact in fixed point (each |entry| < 2^61)
         k_fold_fx<<<1024, 256, 0, st>>>(Kfx, s->nfn);
@@ -1754,6 +1886,17 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         hxf_cache_free(dlogfill, st);
     }
     if (o->log_count) *o->log_count = logged;
+    if (tl.count) {
+        unsigned long long nt = 0;
+        HXF_CUDA(cudaMemcpyAsync(&nt, tl.count, sizeof(nt), cudaMemcpyDeviceToHost, st));
+        HXF_CUDA(cudaStreamSynchronize(st));
+        const int64_t ncopy = std::min<int64_t>((int64_t)nt, tl.cap);
+        if (ncopy) HXF_CUDA(cudaMemcpyAsync(o->tie_log, tl.rec, ncopy * sizeof(hxf_tie_record), cudaMemcpyDeviceToHost, st));
+        if (o->tie_count) *o->tie_count = (int64_t)nt;
+        HXF_CUDA(cudaStreamSynchronize(st));
+        hxf_cache_free(tl.rec, st);
+        hxf_cache_free(tl.count, st);
+    }
     if (o->digest) {
         unsigned long long hd[3] = {0, 0, 0};
         if (want_digest) {
@@ -1791,12 +1934,14 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     }
     c.ties_task = acc_c[C_TIE_TASK];
     c.ties_leaf = acc_c[C_TIE_LEAF];
+    c.screen_bytes = acc_c[C_SCREEN_BYTES];
     c.prim_quartets = acc_c[C_PRIMQ];
     for (int k = 0; k < 16; ++k) {
         c.class_quartets[k] = acc_c[C_CLSQ0 + k];
         c.class_prim_quartets[k] = acc_c[C_CLSPQ0 + k];
     }
     c.culled_bound_ledger = fx_to_double<LEDGER_LIMBS>(acc_l, LEDGER_SCALE);
+    if (acc_c[C_OVERFLOW]) throw HxfError{HXF_ELOGIC, "device bounds check failed (HXF_DEBUG_BOUNDS build)"};
     static const bool eri_stats = getenv("HXF_ERI_STATS") != nullptr;
     if (eri_stats)
         fprintf(stderr, "eri: quartets %lld far %lld (%.1f%%), primitive quartets %lld far %lld (%.1f%%)\n",
@@ -1945,6 +2090,7 @@ __global__ void __launch_bounds__(256) k_direct(DirectArgs a, int64_t p0, int64_
 
 int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, double* K_out,
                hxf_counters* out, cudaStream_t st) {
+    NvtxRange nvtx_build("hxf: direct twin");
     hxf_system* s = pairs->sys;
     if (dens->sys != s) throw HxfError{HXF_EINVAL, "pairs and P must be built over the same partition"};
     if (!(o->tau_2e >= 0.0)) throw HxfError{HXF_EINVAL, "tau_2e must be non-negative"};
@@ -2068,6 +2214,8 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         e.S = S;
         e.K = Kfx;
         e.counters = scount;
+        e.n_bpairs = e.n_kpairs = pairs->n_pairs;
+        e.n_bprim = e.n_kprim = pairs->n_prim_pairs;
         da.off = off;
         da.rec = sb.rec;
         da.keys = sb.keys;

@@ -42,6 +42,7 @@ struct LevelView {
     int64_t node_off;      // offset of this level's dense node arrays
     const int* leaf_id;    // per span (level-local pointer)
     const int* flo;
+    int level;             // partition level (tie records)
 };
 
 // bf / kf: the task factors f(norm) (sqrt(norm) for Schwarz, norm for literal),
@@ -56,6 +57,7 @@ struct TreeView {
     const double* pnorm;
     double tau;
     int mode;
+    TieLog ties;
 };
 
 struct Visit {
@@ -79,6 +81,9 @@ __device__ __forceinline__ double ledger_term(double pn, double sbs, double sks)
     return __dmul_rn(__dmul_rn(__dmul_rn(0.5, pn), sbs), sks);
 }
 
+// TIES: the diagnostic instantiation that also appends tie records (run a second time,
+// only when a build counted ties and the caller asked for the log: the timed path has none)
+template <bool TIES>
 __device__ Visit visit_naive(const TreeView& tv, const LevelView& lv, int mu, int nu, int lam,
                              int sig) {
     Visit v{O_NONE, 0, 0, 0, 0, 0, 0.0};
@@ -93,6 +98,7 @@ __device__ Visit visit_naive(const TreeView& tv, const LevelView& lv, int mu, in
     }
     const double bound = sorted_product3(fb, np, fk);
     v.tie = is_tie(bound, tv.tau);
+    if (TIES && v.tie) tie_emit(tv.ties, HXF_TIE_TASK, lv.level, 0, bound > tv.tau, mu, nu, lam, sig, bound, tv.tau);
     if (bound <= tv.tau) {
         v.outcome = O_SCREEN;
         v.ledger = ledger_term(np, tv.brow[ib], tv.kcol[ik]);
@@ -120,6 +126,7 @@ __device__ __forceinline__ int case_label(const LevelView& lv, int mu, int nu, i
     return CASE_D;
 }
 
+template <bool TIES>
 __device__ Visit visit_sym(const TreeView& tv, const LevelView& lv, int mu, int nu, int lam, int sig,
                            int alive) {
     Visit v{O_NONE, 0, 0, 0, 0, 0, 0.0};
@@ -144,7 +151,10 @@ __device__ Visit visit_sym(const TreeView& tv, const LevelView& lv, int mu, int 
             continue;
         }
         const double bound = sorted_product3(fb, pn, fk);
-        v.tie += is_tie(bound, tv.tau);
+        if (is_tie(bound, tv.tau)) {
+            ++v.tie;
+            if (TIES) tie_emit(tv.ties, HXF_TIE_TASK, lv.level, g, bound > tv.tau, mu, nu, lam, sig, bound, tv.tau);
+        }
         if (bound <= tv.tau) {
             v.links_screen++;
             screened = true;
@@ -269,7 +279,7 @@ __device__ __forceinline__ void flush_packed(long long* counters, unsigned word,
     }
 }
 
-template <bool SYM, bool WRITE>
+template <bool SYM, bool WRITE, bool TIES = false>
 __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
     typedef cub::BlockScan<int, 256> Scan;
     typedef cub::BlockReduce<double, 256> Red;
@@ -302,8 +312,8 @@ __global__ void __launch_bounds__(256) k_expand(ExpandArgs a) {
         const uint64_t task = a.in[parent];
         int cm = 0, cn = 0, cl = 0, cs = 0;
         if (child_spans<SYM>(a, task, c, &cm, &cn, &cl, &cs))
-            v = SYM ? visit_sym(a.tv, a.child, cm, cn, cl, cs, (int)(task >> 60))
-                    : visit_naive(a.tv, a.child, cm, cn, cl, cs);
+            v = SYM ? visit_sym<TIES>(a.tv, a.child, cm, cn, cl, cs, (int)(task >> 60))
+                    : visit_naive<TIES>(a.tv, a.child, cm, cn, cl, cs);
         const int is_leaf = v.outcome == O_LEAF, is_exp = v.outcome == O_EXPAND;
         a.outc[t] = (uint8_t)(is_leaf | (is_exp << 1) | ((is_leaf | is_exp) ? (v.live << 2) : 0));
     }
@@ -379,10 +389,10 @@ __global__ void k_fold_stripes(const long long* sc, const unsigned long long* sl
 
 // the start task: the diagonal node (r, r) of the start level visited against
 // itself (the root, or a diagonal subtree the caller passed as bra = ket = P)
-template <bool SYM>
+template <bool SYM, bool TIES = false>
 __global__ void k_root(TreeView tv, LevelView lv, int r, uint64_t* out_expand, uint64_t* out_leaf,
                        int* outcome, long long* counters, unsigned long long* ledger) {
-    Visit v = SYM ? visit_sym(tv, lv, r, r, r, r, 0xf) : visit_naive(tv, lv, r, r, r, r);
+    Visit v = SYM ? visit_sym<TIES>(tv, lv, r, r, r, r, 0xf) : visit_naive<TIES>(tv, lv, r, r, r, r);
     counters[C_VISITED] += 1;
     counters[C_CULL_SCREEN] += v.outcome == O_SCREEN;
     counters[C_CULL_ABSENT] += v.outcome == O_ABSENT;
@@ -427,10 +437,12 @@ __global__ void k_unpack_counts(const int* packed, int64_t n, int64_t* leaf, int
 // [shard_begin, shard_end) (every shard_stride-th task) and, unless shard_begin == 0, counters and leaf
 // tasks produced above the cut are discarded (they belong to rank 0).
 TraversalResult traverse(const TravInput& in, cudaStream_t st) {
+    NvtxRange nvtx_range("hxf: traversal");
     hxf_system* s = in.sys;
     const bool schwarz = in.mode == HXF_MODE_SCHWARZ;
     TreeView tv{schwarz ? in.bra->snorm : in.bra->norm, in.bra->srow, in.bra->scol,
-                schwarz ? in.ket->snorm : in.ket->norm, in.ket->srow, in.ket->scol, in.dens->norm, in.tau, in.mode};
+                schwarz ? in.ket->snorm : in.ket->norm, in.ket->srow, in.ket->scol, in.dens->norm, in.tau, in.mode,
+                in.ties};
     TraversalResult res;
     res.leaf = nullptr;
     res.n_leaf = 0;
@@ -473,9 +485,13 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
     uint64_t* leaf0 = talloc<uint64_t>(1, st);
     int* d_outcome = talloc<int>(1, st);
     LevelView lv0{s->h_off[L0 + 1] - s->h_off[L0], s->node_off[L0], s->lv.leaf_id + s->h_off[L0],
-                  s->lv.flo + s->h_off[L0]};
+                  s->lv.flo + s->h_off[L0], L0};
     const int r0 = in.root_index;
-    if (in.sym) { k_root<true><<<1, 1, 0, st>>>(tv, lv0, r0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
+    const bool log_ties = in.ties.count != nullptr;   // the diagnostic pass (tie records)
+    if (log_ties) {
+        if (in.sym) { k_root<true, true><<<1, 1, 0, st>>>(tv, lv0, r0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
+        else { k_root<false, true><<<1, 1, 0, st>>>(tv, lv0, r0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
+    } else if (in.sym) { k_root<true><<<1, 1, 0, st>>>(tv, lv0, r0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
     else { k_root<false><<<1, 1, 0, st>>>(tv, lv0, r0, cur, leaf0, d_outcome, counters, ledger); note_launch(); }
     int outcome = 0;
     HXF_CUDA(cudaMemcpyAsync(&outcome, d_outcome, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -540,7 +556,7 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         (void)n_par;
         const int base_ch = s->h_off[L + 1];
         LevelView ch{s->h_off[L + 2] - s->h_off[L + 1], s->node_off[L + 1], s->lv.leaf_id + base_ch,
-                     s->lv.flo + base_ch};
+                     s->lv.flo + base_ch, L + 1};
         static const bool trace = getenv("HXF_TRAV_TRACE") != nullptr;
         const double tr0 = trace ? trav_now_ms() : 0.0;
         const int64_t nthreads = n_cur * 16;
@@ -567,7 +583,10 @@ TraversalResult traverse(const TravInput& in, cudaStream_t st) {
         a.blk_off_expand = oe;
         a.blk_off_leaf = ol;
         a.eight = in.sym == 2;
-        if (in.sym) { k_expand<true, false><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
+        if (log_ties) {
+            if (in.sym) { k_expand<true, false, true><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
+            else { k_expand<false, false, true><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
+        } else if (in.sym) { k_expand<true, false><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         else { k_expand<false, false><<<(unsigned)nb, 256, 0, st>>>(a); note_launch(); }
         { k_unpack_counts<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(blk, nb, cl, ce); note_launch(); }
         HXF_CUDA(cudaMemsetAsync(cl + nb, 0, sizeof(int64_t), st));

@@ -24,6 +24,7 @@ struct TravInput {
     unsigned long long* ledger;  // device LEDGER_LIMBS
     int root_level = 0;    // the traversal starts at the diagonal node (root_index, root_index)
     int root_index = 0;    // of this level (a diagonal subtree; 0, 0 = the tree root)
+    TieLog ties{nullptr, nullptr, 0};   // device tie log (task stage), or disabled
 };
 
 struct TraversalResult {

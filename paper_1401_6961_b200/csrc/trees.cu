@@ -317,6 +317,16 @@ __global__ void k_leaf_norms(const int* lslo, const int* lshi, int nleaf, const 
     lcol[t] = cm;
 }
 
+// overlap-pruning comparisons (block max |S| < tau_ovlp) within 1e-12 relative of tau_ovlp
+__global__ void k_overlap_ties(const double* smax, int n, int level, double tau, TieLog tl) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * n) return;
+    const double m = smax[t];
+    if (fabs(m - tau) <= 1e-12 * tau) {
+        tie_emit(tl, HXF_TIE_OVERLAP, level, 0, !(m < tau), (int)(t / n), (int)(t % n), -1, -1, m, tau);
+    }
+}
+
 // fill one level of the pair tree (bottom-up); leaves copy leaf-pair data
 __global__ void k_pair_level(int level, int n, int nnext, const int* span_base_L,
                              const int* leaf_id, const int* kid0, const int* kid1, int nleaf,
@@ -549,6 +559,7 @@ static LeafTables make_leaf_tables(hxf_system* s, cudaStream_t st, std::vector<v
 }
 
 void trees_build_pairs(hxf_pairs* pr, cudaStream_t st, const double* s_user) {
+    NvtxRange nvtx_range("hxf: pair tree");
     hxf_system* s = pr->sys;
     std::vector<void*> tmp;
     const int nl = s->n_leaves;
@@ -664,6 +675,30 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st, const double* s_user) {
             L, n, nnext, d_off + L, s->lv.leaf_id, s->lv.kid0, s->lv.kid1, nl, lnorm, lrow, lcol,
             lsmax, pr->tau_ovlp, d_node_off, pr->norm, pr->rowsum, pr->colsum, pr->smax); note_launch(); }
     }
+    // overlap-stage ties: nodes whose block max |S| lies within 1e-12 (relative) of
+    // tau_ovlp, the comparison that decides pruning at every level
+    if (pr->tau_ovlp > 0.0) {
+        const long long cap = 4096;
+        TieLog tl{dalloc<hxf_tie_record>(cap, st), dalloc<unsigned long long>(1, st), cap};
+        tmp.push_back(tl.rec);
+        tmp.push_back(tl.count);
+        HXF_CUDA(cudaMemsetAsync(tl.count, 0, sizeof(unsigned long long), st));
+        for (int L = 0; L < s->n_levels; ++L) {
+            const int n = s->h_off[L + 1] - s->h_off[L];
+            k_overlap_ties<<<nblk((int64_t)n * n), 256, 0, st>>>(pr->smax + s->node_off[L], n, L, pr->tau_ovlp, tl);
+            note_launch();
+        }
+        unsigned long long nt = 0;
+        HXF_CUDA(cudaMemcpyAsync(&nt, tl.count, sizeof(nt), cudaMemcpyDeviceToHost, st));
+        HXF_CUDA(cudaStreamSynchronize(st));
+        pr->n_ovlp_ties = (int64_t)nt;
+        pr->ovlp_ties.resize((size_t)std::min<long long>((long long)nt, cap));
+        if (!pr->ovlp_ties.empty()) {
+            HXF_CUDA(cudaMemcpyAsync(pr->ovlp_ties.data(), tl.rec, pr->ovlp_ties.size() * sizeof(hxf_tie_record),
+                                     cudaMemcpyDeviceToHost, st));
+            HXF_CUDA(cudaStreamSynchronize(st));
+        }
+    }
     // the traversal's per-node square roots, once per pair tree (correctly rounded:
     // bitwise what a per-visit sqrt would give)
     pr->snorm = dalloc<double>(nn, st);
@@ -703,6 +738,7 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st, const double* s_user) {
 }
 
 void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStream_t st) {
+    NvtxRange nvtx_range("hxf: density tree");
     hxf_system* s = d->sys;
     std::vector<void*> tmp;
     const int nl = s->n_leaves;

@@ -55,6 +55,7 @@ class TraversalCounters:
     # device extras (not part of the reference's to_dict)
     ties_task: int = 0
     ties_leaf: int = 0
+    screen_bytes: int = 0   # leaf screen: SURVEY 8(d) algorithmic bytes (bench roofline)
     prim_quartets: int = 0
 
     _KEYS = ("tasks_visited", "tasks_culled_screening", "tasks_culled_absent",
@@ -89,6 +90,7 @@ class SymmetryCounters:
     case_leaf_tasks: dict = field(default_factory=lambda: {c: 0 for c in CASE_LABELS})
     ties_task: int = 0
     ties_leaf: int = 0
+    screen_bytes: int = 0   # leaf screen: SURVEY 8(d) algorithmic bytes (bench roofline)
     prim_quartets: int = 0
 
     _KEYS = ("tasks_visited", "tasks_culled_screening", "tasks_culled_absent",
@@ -255,7 +257,7 @@ def _start_node(bra, ket, P):
 
 def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log=None,
                  K_out=None, shard=None, symmetrize=True, digest=None, digest_sample=(1, 0),
-                 K_fixed=False):
+                 K_fixed=False, tie_log=None, screen_bytes=False):
     """Low-level call of hxf_exchange.
 
     K_out: None (return a new host array), or a CUDA tensor (n x n float64)
@@ -269,6 +271,10 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
     digest: None, or a caller-owned numpy uint64[3] filled with the
     order-independent digest (count, sum h, sum h(h)) of the evaluated quartet
     tuples with i % digest_sample[0] == digest_sample[1] (include/hxf.h).
+    tie_log: None, or a list extended with one dict per culling comparison of the
+    task and leaf stages whose bound lies within 1e-12 relative of tau_2e (stage,
+    level, slot, decision, ids, bound, threshold, contribution: include/hxf.h
+    hxf_tie_record; at most TIE_CAPACITY records, the counters hold the totals).
     Returns (K or None, hxf counters struct, list of logged quartets or None).
     """
     if not (tau_2e >= 0.0):
@@ -307,6 +313,13 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
         opts.digest_mod, opts.digest_rem = int(digest_sample[0]), int(digest_sample[1])
     if K_out is not None:
         check_device_matrix(K_out, n, "int64" if K_fixed else "float64", bra._t.ds.device_index)
+    opts.count_screen_bytes = 1 if screen_bytes else 0   # measurement aid (bench roofline_screen)
+    tie_buf, tie_count = None, ctypes.c_int64(0)
+    if tie_log is not None:
+        tie_buf = (_native.TieRecord * TIE_CAPACITY)()
+        opts.tie_log = ctypes.cast(tie_buf, ctypes.POINTER(_native.TieRecord))
+        opts.tie_capacity = TIE_CAPACITY
+        opts.tie_count = ctypes.pointer(tie_count)
     log_count = ctypes.c_int64(0)
     cap = 0
     if quartet_log is not None and evaluate:
@@ -342,6 +355,8 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
             cap = int(log_count.value)
             continue
         break
+    if tie_log is not None:
+        tie_log.extend(tie_buf[k].to_dict() for k in range(min(int(tie_count.value), TIE_CAPACITY)))
     log = None
     if cap:
         arr = logbuf[:log_count.value]
@@ -350,18 +365,22 @@ def run_exchange(bra, ket, P, tau_2e, mode, symmetry, evaluate=True, quartet_log
     return K, c, log
 
 
+TIE_CAPACITY = 4096   # tie records returned per build (ties are rare; the counters hold the totals)
+
+
 def last_timings():
-    """Device stage times (ms) of the last build on this thread:
-    [traversal, screen, eri stage, epilogue, total, eri kernels only]."""
-    out = (ctypes.c_double * 6)()
-    _native.lib().hxf_last_timings(out, 6)
+    """Device stage times (ms) of the last build on this thread: [traversal, screen,
+    eri stage, epilogue, total, eri kernels only, far-field classification + survivor sort]."""
+    out = (ctypes.c_double * 7)()
+    _native.lib().hxf_last_timings(out, 7)
     return list(out)
 
 
 def _fill_common(dst, c):
     for k in ("tasks_visited", "tasks_culled_screening", "tasks_culled_absent",
               "leaf_contractions", "eri_shell_quartets", "quartets_culled_leaf",
-              "tasks_expanded", "children_spawned", "ties_task", "ties_leaf", "prim_quartets"):
+              "tasks_expanded", "children_spawned", "ties_task", "ties_leaf", "prim_quartets",
+              "screen_bytes"):
         setattr(dst, k, int(getattr(c, k)))
     dst.culled_bound_ledger = float(c.culled_bound_ledger)
 
@@ -369,12 +388,13 @@ def _fill_common(dst, c):
 def build_exchange_naive(bra: ShellPairNode, ket: ShellPairNode, P: MatrixQuadtree,
                          tau_2e: float = 0.0, mode: str = "schwarz",
                          quartet_log: list | None = None, evaluate: bool = True,
-                         threads: int = 1):
+                         threads: int = 1, tie_log: list | None = None):
     """K = -1/2 sum P_nl (mn|ls) by hextree traversal on the GPU.
 
     Returns (K, TraversalCounters).  Reference: exchange_naive.py:200-240.
+    tie_log (extension): a list that receives the build's tie records (run_exchange).
     """
-    K, c, log = run_exchange(bra, ket, P, tau_2e, mode, False, evaluate, quartet_log)
+    K, c, log = run_exchange(bra, ket, P, tau_2e, mode, False, evaluate, quartet_log, tie_log=tie_log)
     out = TraversalCounters()
     _fill_common(out, c)
     if quartet_log is not None and log is not None:
@@ -384,13 +404,14 @@ def build_exchange_naive(bra: ShellPairNode, ket: ShellPairNode, P: MatrixQuadtr
 
 def build_exchange_symmetric(pairs: ShellPairNode, P: MatrixQuadtree, tau_2e: float = 0.0,
                              mode: str = "schwarz", quartet_log: list | None = None,
-                             evaluate: bool = True, threads: int = 1):
+                             evaluate: bool = True, threads: int = 1, tie_log: list | None = None):
     """Canonical-pair (4-fold) exchange build on the GPU; K passes symmetrize_final.
 
     Returns (K, SymmetryCounters).  Reference: exchange_symmetry.py:364-409.
+    tie_log (extension): a list that receives the build's tie records (run_exchange).
     """
     K, c, log = run_exchange(pairs, pairs, P, tau_2e, mode, True, evaluate, quartet_log,
-                             symmetrize=evaluate)
+                             symmetrize=evaluate, tie_log=tie_log)
     out = SymmetryCounters()
     _fill_common(out, c)
     out.links_culled_screening = int(c.links_culled_screening)

@@ -397,6 +397,20 @@ class _PairTree:
             self._lvl[L] = v
         return v
 
+    def overlap_ties(self):
+        """Overlap-pruning comparisons (block max |S| < tau_ovlp, quadtree.py:296-299)
+        within 1e-12 relative of tau_ovlp, found when the tree was built: a list of
+        tie-record dicts (stage "overlap", level, level-local span ids, |S|, tau_ovlp)."""
+        n = ctypes.c_int64(0)
+        _native.check(_native.lib().hxf_pairs_ties(self.handle, None, 0, ctypes.byref(n)))
+        k = min(int(n.value), 4096)
+        if not k:
+            return []
+        buf = (_native.TieRecord * k)()
+        _native.check(_native.lib().hxf_pairs_ties(self.handle, ctypes.cast(buf, ctypes.POINTER(_native.TieRecord)),
+                                                   k, ctypes.byref(n)))
+        return [buf[i].to_dict() for i in range(k)]
+
     def qmatrix(self):
         if self._q is None:
             ns = self.ds.n_shells
@@ -443,6 +457,11 @@ class ShellPairNode:
     @property
     def colsum_max(self) -> float:
         return float(self._get(2))
+
+    @property
+    def overlap_ties(self):
+        """(extension) tie records of the tree's overlap pruning."""
+        return self._t.overlap_ties()
 
     @property
     def is_leaf(self) -> bool:

@@ -36,7 +36,9 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     src = tmp_path / "layout.c"
     lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "hxf.h"', "int main(void) {"]
-    for cname, py in (("hxf_counters", _native.Counters), ("hxf_exchange_opts", _native.ExchangeOpts)):
+    structs = (("hxf_counters", _native.Counters), ("hxf_exchange_opts", _native.ExchangeOpts),
+               ("hxf_tie_record", _native.TieRecord))
+    for cname, py in structs:
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
         for f, _ in py._fields_:
             lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
@@ -46,7 +48,7 @@ def test_struct_layouts_match_header(tmp_path):
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
     got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
                                                  check=True).stdout.splitlines())
-    for cname, py in (("hxf_counters", _native.Counters), ("hxf_exchange_opts", _native.ExchangeOpts)):
+    for cname, py in structs:
         assert int(got[cname]) == ctypes.sizeof(py), cname
         for f, _ in py._fields_:
             assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, (cname, f)

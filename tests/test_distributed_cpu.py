@@ -169,6 +169,26 @@ def _sharded_run(st, tau, level, world, rank, strategy):
     if strategy == "hashed":
         _, _, m = distributed.split_hashed(len(frontier), world)[rank]
         picked = [t for t, keep in zip(frontier, m) if keep]
+    elif strategy == "balanced":
+        # distributed.plan(strategy="balanced") on the CPU: hashed task groups costed by
+        # counters-only runs (every rank costs every world-th group, one all-reduce),
+        # then longest-first onto ranks (group_costs + split_lpt)
+        groups = 4 * world
+        owner = distributed._owner(len(frontier), groups)
+        cost = np.zeros(groups)
+        for g in range(rank, groups, world):
+            probe = ho._Naive(st.shells, st.P, st.P.shape[0], tau, "schwarz", False, False)
+            for (b, p, k), o in zip(frontier, owner):
+                if o == g:
+                    _expand_children(probe, b, p, k)
+            cost[g] = (distributed.COST_PER_QUARTET * probe.c.eri_shell_quartets
+                       + distributed.COST_PER_LEAF_TASK * probe.c.leaf_contractions
+                       + distributed.COST_PER_VISIT * probe.c.tasks_visited)
+        t = torch.from_numpy(cost)
+        if dist.is_initialized():
+            dist.all_reduce(t)
+        _, _, m = distributed.split_lpt(len(frontier), world, groups, t.numpy())[rank]
+        picked = [t_ for t_, keep in zip(frontier, m) if keep]
     elif strategy == "cyclic":
         b0, e0, s0 = distributed.split_cyclic(len(frontier), world)[rank]
         picked = frontier[b0:e0:s0]
@@ -211,7 +231,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,strategy", [(2, "hashed"), (2, "cyclic"), (2, "contiguous")])
+@pytest.mark.parametrize("world,strategy", [(2, "hashed"), (2, "balanced"), (2, "cyclic"), (2, "contiguous")])
 def test_gloo_sharded_build_equals_single_process(tmp_path, world, strategy):
     path = str(tmp_path / "res.npz")
     mp.spawn(_worker, args=(world, _free_port(), path, strategy), nprocs=world, join=True)
