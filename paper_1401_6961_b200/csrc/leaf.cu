@@ -90,7 +90,17 @@ struct ScreenArgs {
 // Such quartets sort into their own ERI range whose kernels evaluate only the
 // asymptotic Boys branch (the branch the table path selects there).
 #define KEY_FAR 0x1000
+#ifdef HXF_KEY8
+// A/B: one radix pass.  The screen's 12-bit key is rewritten by k_classify_far to
+// far << 7 | class << 3 | (min(nk, 8) - 1): no ordering by the bra primitive count.
+#define KEY_BITS 8
+#define KEY_CLASS_SPAN 8
+#define KEY_OF(far, cls) (((far) ? 0x80 : 0) | ((cls) << 3))
+#else
 #define KEY_BITS 13
+#define KEY_CLASS_SPAN 256
+#define KEY_OF(far, cls) (((far) ? KEY_FAR : 0) | ((cls) << 8))
+#endif
 #define KEY_RANGES (1 << KEY_BITS)
 
 // Survivor emission through per-warp slabs: one global atomic reserves SLAB
@@ -98,7 +108,11 @@ struct ScreenArgs {
 // sentinel records (key 0xFFFF sorts after every real 12-bit key and is
 // excluded by the key bounds), so no emitting iteration waits for an atomic.
 #define SLAB 1024
+#ifdef HXF_KEY8
+#define SENTINEL_REC (1ull << 63)   // slot mask 0: a sentinel that sorts into a class range is skipped
+#else
 #define SENTINEL_REC (~0ull)
+#endif
 #define SENTINEL_KEY ((uint16_t)0xFFFF)
 
 struct Slab {
@@ -856,10 +870,10 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
     typedef Eri<LA, LB, LC, LD> E;
     constexpr int NI = E::NI, NJ = E::NJ, NK = E::NK, NL = E::NL;
     constexpr int CLS = (LA << 3) | (LB << 2) | (LC << 1) | LD;
-    constexpr int K0 = (FAR ? KEY_FAR : 0) | (CLS << 8);
+    constexpr int K0 = KEY_OF(FAR, CLS);
     if (e.dbounds) {  // asynchronous launch: range from the sorted keys' bounds
         const int64_t b0 = e.dbounds[K0];
-        e.n = e.dbounds[K0 + 256] - b0;
+        e.n = e.dbounds[K0 + KEY_CLASS_SPAN] - b0;
         e.rec += b0;
         if (e.n <= 0) return;
     }
@@ -1056,7 +1070,11 @@ __global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __res
                                const float4* __restrict__ kgeo, const float* __restrict__ kgip) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const uint16_t key = keys[t];
+#ifdef HXF_KEY8
+        if (key == SENTINEL_KEY) { keys[t] = 0; continue; }
+#else
         if (key == SENTINEL_KEY) continue;
+#endif
         const uint64_t r = rec[t];
         const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
         const int L = __popc((key >> 8) & 15);
@@ -1064,7 +1082,12 @@ __global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __res
         const float ip = __ldg(bgip + pb) + __ldg(kgip + pk);
         const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
         const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
-        if (d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip) keys[t] = key | KEY_FAR;
+        const bool far = d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip;
+#ifdef HXF_KEY8
+        keys[t] = (uint16_t)(KEY_OF(far, (key >> 8) & 15) | min((int)(key & 15), 7));
+#else
+        if (far) keys[t] = key | KEY_FAR;
+#endif
     }
 }
 
