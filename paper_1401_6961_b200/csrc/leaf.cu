@@ -89,18 +89,13 @@ struct ScreenArgs {
 // quartet from the two pairs' enclosing spheres (k_pair_geo, k_classify_far).
 // Such quartets sort into their own ERI range whose kernels evaluate only the
 // asymptotic Boys branch (the branch the table path selects there).
+// (An 8-bit key -- far, class, min(nk, 8), one radix pass instead of two -- saves
+// ~170 ms of sort per c5 build and costs 880 ms in the ERI kernels, whose warps then mix
+// bra primitive counts: profiles/r02_ab_eri_memory.log.  13 bits stay.)
 #define KEY_FAR 0x1000
-#ifdef HXF_KEY8
-// A/B: one radix pass.  The screen's 12-bit key is rewritten by k_classify_far to
-// far << 7 | class << 3 | (min(nk, 8) - 1): no ordering by the bra primitive count.
-#define KEY_BITS 8
-#define KEY_CLASS_SPAN 8
-#define KEY_OF(far, cls) (((far) ? 0x80 : 0) | ((cls) << 3))
-#else
 #define KEY_BITS 13
 #define KEY_CLASS_SPAN 256
 #define KEY_OF(far, cls) (((far) ? KEY_FAR : 0) | ((cls) << 8))
-#endif
 #define KEY_RANGES (1 << KEY_BITS)
 
 // Survivor emission through per-warp slabs: one global atomic reserves SLAB
@@ -108,11 +103,7 @@ struct ScreenArgs {
 // sentinel records (key 0xFFFF sorts after every real 12-bit key and is
 // excluded by the key bounds), so no emitting iteration waits for an atomic.
 #define SLAB 1024
-#ifdef HXF_KEY8
-#define SENTINEL_REC (1ull << 63)   // slot mask 0: a sentinel that sorts into a class range is skipped
-#else
 #define SENTINEL_REC (~0ull)
-#endif
 #define SENTINEL_KEY ((uint16_t)0xFFFF)
 
 struct Slab {
@@ -1070,11 +1061,7 @@ __global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __res
                                const float4* __restrict__ kgeo, const float* __restrict__ kgip) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const uint16_t key = keys[t];
-#ifdef HXF_KEY8
-        if (key == SENTINEL_KEY) { keys[t] = 0; continue; }
-#else
         if (key == SENTINEL_KEY) continue;
-#endif
         const uint64_t r = rec[t];
         const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
         const int L = __popc((key >> 8) & 15);
@@ -1082,12 +1069,7 @@ __global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __res
         const float ip = __ldg(bgip + pb) + __ldg(kgip + pk);
         const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
         const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
-        const bool far = d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip;
-#ifdef HXF_KEY8
-        keys[t] = (uint16_t)(KEY_OF(far, (key >> 8) & 15) | min((int)(key & 15), 7));
-#else
-        if (far) keys[t] = key | KEY_FAR;
-#endif
+        if (d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip) keys[t] = key | KEY_FAR;
     }
 }
 
