@@ -1073,6 +1073,15 @@ __global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __res
     }
 }
 
+// experiment (HXF_EXP_SORTPB): 41-bit key = sort key << 28 | bra (1) or ket (2) pair id
+__global__ void k_exp_key64(const uint16_t* keys, const uint64_t* rec, int64_t n, int which, uint64_t* out) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = rec[t];
+        const uint64_t id = which == 1 ? (r & 0xfffffff) : ((r >> 28) & 0xfffffff);
+        out[t] = ((uint64_t)keys[t] << 28) | id;
+    }
+}
+
 // lower bounds of every 12-bit key value in the sorted key array
 __global__ void k_key_bounds(const uint16_t* keys, int64_t n, int64_t* bounds) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1295,13 +1304,34 @@ void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cuda
     size_t tb = b.sort_tb;
     HXF_CUDA(cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, KEY_BITS, st));
     { k_key_bounds<<<KEY_RANGES / 256 + 1, 256, 0, st>>>(b.keys2, nrec, b.dbounds); note_launch(); }
+    // HXF_EXP_SORTPB=1|2 (experiment, costs a 41-bit radix sort): inside every key range
+    // order the records by bra pair id (1) or by ket pair id (2), to measure what a warp
+    // that shares its bra / ket pair would gain in the ERI kernels
+    static const int exp_sortpb = getenv("HXF_EXP_SORTPB") ? atoi(getenv("HXF_EXP_SORTPB")) : 0;
+    uint64_t* rec_sorted = b.rec2;
+    uint64_t *k64a = nullptr, *k64b = nullptr, *rec3 = nullptr;
+    void* tmp64 = nullptr;
+    if (exp_sortpb) {
+        k64a = lalloc<uint64_t>(nrec, st);
+        k64b = lalloc<uint64_t>(nrec, st);
+        rec3 = lalloc<uint64_t>(nrec, st);
+        k_exp_key64<<<(unsigned)std::min<int64_t>((nrec + 255) / 256, 1 << 20), 256, 0, st>>>(b.keys2, b.rec2, nrec,
+                                                                                      exp_sortpb, k64a);
+        size_t tb64 = 0;
+        HXF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb64, k64a, k64b, b.rec2, rec3, nrec, 0, 28 + KEY_BITS, st));
+        tmp64 = lalloc<char>(tb64, st);
+        HXF_CUDA(cub::DeviceRadixSort::SortPairs(tmp64, tb64, k64a, k64b, b.rec2, rec3, nrec, 0, 28 + KEY_BITS, st));
+        rec_sorted = rec3;
+    }
     if (after_sort) cudaEventRecord(after_sort, st);
-    e.rec = b.rec2;
+    e.rec = rec_sorted;
     e.n = 0;
     e.dbounds = b.dbounds;
     for (int c = 0; c < 16; ++c) launch_eri_class(c, false, e, st);
     for (int c = 0; c < 16; ++c) launch_eri_class(c, true, e, st);
     HXF_CUDA(cudaGetLastError());
+    for (void* p : {(void*)k64a, (void*)k64b, (void*)rec3, tmp64})
+        if (p) hxf_cache_free(p, st);
 }
 
 void host_ledger_add(unsigned long long* acc, const unsigned long long* v) {

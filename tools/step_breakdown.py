@@ -38,5 +38,6 @@ for r in range(reps):
     t3 = time.perf_counter()
     st = exchange.last_timings()
     print(f"rep {r}: density {1e3*(t1-t0):.1f} ms  exchange {1e3*(t2-t1):.1f} ms (device total {st[4]:.1f}: "
-          f"trav {st[0]:.1f} screen {st[1]:.1f} eri {st[2]:.1f} epi {st[3]:.1f})  teardown {1e3*(t3-t2):.1f} ms",
+          f"trav {st[0]:.1f} screen {st[1]:.1f} eri {st[2]:.1f} [kernels {st[5]:.1f} sort {st[6]:.1f}] epi {st[3]:.1f})  "
+          f"teardown {1e3*(t3-t2):.1f} ms",
           flush=True)
