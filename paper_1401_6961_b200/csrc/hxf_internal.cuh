@@ -427,6 +427,10 @@ void note_launch(int n = 1);
 // ---------------------------------------------------------------- launchers
 // (defined in the .cu files)
 
+// pageable host <-> device transfers of the boundary's n^2 arrays (xfer.cu): return when done
+void xfer_to_device(void* dst_dev, const void* src_host, size_t bytes, cudaStream_t st);
+void xfer_to_host(void* dst_host, const void* src_dev, size_t bytes, cudaStream_t st);
+
 void launch_boys_init();
 void trees_build_pairs(hxf_pairs* pr, cudaStream_t st, const double* s_user = nullptr);
 void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStream_t st);

@@ -1906,7 +1906,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                                        o->K_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
             hxf_cache_free(Kd, st);
         } else if (!o->K_on_device) {
-            HXF_CUDA(cudaMemcpyAsync(K_out, Kd, n2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            xfer_to_host(K_out, Kd, n2 * sizeof(double), st);
             hxf_cache_free(Kd, st);
         }
     }
@@ -2285,7 +2285,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         if (Kfx) { k_fx_to_double<<<1024, 256, 0, st>>>(Kfx, nfn2, S, Kd); note_launch(); }
         else HXF_CUDA(cudaMemsetAsync(Kd, 0, nfn2 * sizeof(double), st));
         if (!o->K_on_device) {
-            HXF_CUDA(cudaMemcpyAsync(K_out, Kd, nfn2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+            xfer_to_host(K_out, Kd, nfn2 * sizeof(double), st);
             hxf_cache_free(Kd, st);
         }
     }

@@ -745,8 +745,8 @@ void trees_build_density(hxf_density* d, const double* P, int on_device, cudaStr
     const int64_t nl2 = (int64_t)nl * nl;
     const int64_t n2 = (int64_t)s->nfn * s->nfn;
     d->P = dalloc<double>(n2, st);
-    HXF_CUDA(cudaMemcpyAsync(d->P, P, n2 * sizeof(double),
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (on_device) HXF_CUDA(cudaMemcpyAsync(d->P, P, n2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    else xfer_to_device(d->P, P, n2 * sizeof(double), st);
     LeafTables lt = make_leaf_tables(s, st, tmp);
     double* lnorm = dalloc<double>(nl2, st);
     tmp.push_back(lnorm);
