@@ -314,7 +314,7 @@ void hxf_pairs_destroy(hxf_pairs* p) {
     void* ptrs[] = {p->norm, p->rowsum, p->colsum, p->smax, p->leaf_base, p->pi,
                     p->pj,   p->ppoff,  p->q,      p->pp,       p->info, p->sq, p->meta,
                     p->ncid, p->nvec,   p->nvec_tri, p->epp, p->eS, p->snorm, p->srow, p->scol,
-                    p->geo, p->gip};
+                    p->geo, p->gip, p->fcol};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     delete p;

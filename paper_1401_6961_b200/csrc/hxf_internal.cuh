@@ -109,6 +109,8 @@ struct hxf_pairs {
     float4* geo;       // per pair: centroid of the primitive centres, radius (conservative, far-field test)
     float* gip;        // per pair: max 1/p over its primitives (rounded up)
     double* eS;        // per entry of epp: primitive Schwarz factor sqrt(max_comp (ab|ab))
+    uint8_t* fcol;     // per pair: 1 = same-centre (ss| pair whose far-field primitive list collapses to the
+                       // single point charge stored at epp[n_prim_pairs + pair id] (k_prim_schwarz_sort)
     double smax_prim;  // max eS
     std::vector<hxf_tie_record> ovlp_ties;   // overlap-pruning ties found at build (first 4096)
     int64_t n_ovlp_ties = 0;

@@ -779,6 +779,8 @@ struct EriArgs {
     const PrimPair* kpp;
     const int4* binfo;
     const int4* kinfo;
+    const int4* bfinfo;   // far-field kernels: collapsed same-centre (ss| pairs (k_prune_pairs)
+    const int4* kfinfo;
     const double3* ctr;
     const int* fn;
     const double* P;
@@ -882,7 +884,7 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
         double half = -0.5;
         if (mask) {
             const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
-            const int4 ib = __ldg(e.binfo + pb), ik = __ldg(e.kinfo + pk);
+            const int4 ib = __ldg((FAR ? e.bfinfo : e.binfo) + pb), ik = __ldg((FAR ? e.kfinfo : e.kinfo) + pk);
             const int nb = ib.w, nk = ik.w;
             nprim += (long long)nb * nk;
             nq += 1;
@@ -954,7 +956,7 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
             const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
             if (!HXF_BCHECK(pb < e.n_bpairs && pk < e.n_kpairs, e.counters)) continue;
             // one 16-byte record per pair: function offsets, primitive-pair range
-            const int4 ib = __ldg(e.binfo + pb), ik = __ldg(e.kinfo + pk);
+            const int4 ib = __ldg((FAR ? e.bfinfo : e.binfo) + pb), ik = __ldg((FAR ? e.kfinfo : e.kinfo) + pk);
             const int nb = ib.w, nk = ik.w;
             if (!HXF_BCHECK(nb >= 1 && nk >= 1 && ib.z >= 0 && ik.z >= 0 && (int64_t)ib.z + nb <= e.n_bprim &&
                                 (int64_t)ik.z + nk <= e.n_kprim,
@@ -1058,7 +1060,8 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
 // record; the spheres are gathered with the locality of the screen's order).
 __global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __restrict__ keys, int64_t n,
                                const float4* __restrict__ bgeo, const float* __restrict__ bgip,
-                               const float4* __restrict__ kgeo, const float* __restrict__ kgip) {
+                               const float4* __restrict__ kgeo, const float* __restrict__ kgip,
+                               const uint8_t* __restrict__ bfcnt, const uint8_t* __restrict__ kfcnt) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const uint16_t key = keys[t];
         if (key == SENTINEL_KEY) continue;
@@ -1069,7 +1072,9 @@ __global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __res
         const float ip = __ldg(bgip + pb) + __ldg(kgip + pk);
         const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
         const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
-        if (d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip) keys[t] = key | KEY_FAR;
+        // a far quartet sorts by its far-field primitive counts (1 for a collapsed pair)
+        if (d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip)
+            keys[t] = (uint16_t)(KEY_FAR | (key & 0xf00) | (__ldg(bfcnt + pb) << 4) | __ldg(kfcnt + pk));
     }
 }
 
@@ -1266,6 +1271,8 @@ struct SurvivorBufs {
     const float4* kgeo = nullptr;
     const float* bgip = nullptr;
     const float* kgip = nullptr;
+    const uint8_t* bfcnt = nullptr;   // far-field primitive count - 1 per pair (EriTables::fcnt)
+    const uint8_t* kfcnt = nullptr;
 };
 
 struct Timer {
@@ -1298,7 +1305,7 @@ void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cuda
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrec + 255) / 256, (int64_t)sms * 8));
-        k_classify_far<<<g, 256, 0, st>>>(b.rec, b.keys, nrec, b.bgeo, b.bgip, b.kgeo, b.kgip);
+        k_classify_far<<<g, 256, 0, st>>>(b.rec, b.keys, nrec, b.bgeo, b.bgip, b.kgeo, b.kgip, b.bfcnt, b.kfcnt);
         note_launch();
     }
     size_t tb = b.sort_tb;
@@ -1351,8 +1358,12 @@ void host_ledger_add(unsigned long long* acc, const unsigned long long* v) {
 // Per-build ERI pair tables: the pair records and sort-key bytes with each
 // pair's primitive count cut to the primitives with S > thr (epp holds them
 // first, sorted by S); at least one primitive is kept.
+// finfo / fcnt: the same for the far-field kernels -- a collapsible pair (hxf_pairs::fcol)
+// is the one point charge at epp[n_prim + pair id]; fcnt = far-field primitive count - 1,
+// the sort-key nibble k_classify_far writes for a far quartet.
 __global__ void k_prune_pairs(int64_t n, const int4* __restrict__ info, const uint8_t* __restrict__ meta,
-                              const double* __restrict__ eS, double thr, int4* einfo, uint8_t* emeta) {
+                              const double* __restrict__ eS, double thr, int4* einfo, uint8_t* emeta,
+                              const uint8_t* __restrict__ fcol, int64_t n_prim, int4* finfo, uint8_t* fcnt) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= n) return;
     const int4 v = info[t];
@@ -1361,11 +1372,16 @@ __global__ void k_prune_pairs(int64_t n, const int4* __restrict__ info, const ui
     keep = max(keep, 1);
     einfo[t] = make_int4(v.x, v.y, v.z, keep);
     emeta[t] = (uint8_t)((meta[t] & 3) | ((keep - 1) << 2));
+    const bool col = fcol[t] != 0;
+    finfo[t] = col ? make_int4(v.x, v.y, (int)(n_prim + t), 1) : make_int4(v.x, v.y, v.z, keep);
+    fcnt[t] = (uint8_t)(col ? 0 : keep - 1);
 }
 
 struct EriTables {
     int4* info = nullptr;
     uint8_t* meta = nullptr;
+    int4* finfo = nullptr;
+    uint8_t* fcnt = nullptr;
 };
 
 // thr = HXF_PRIM_EPS / (max S of the other side * max|P|)
@@ -1373,6 +1389,8 @@ EriTables prune_tables(const hxf_pairs* pr, double other_smax, double pmax, cuda
     EriTables t;
     t.info = lalloc<int4>(pr->n_pairs, st);
     t.meta = lalloc<uint8_t>(pr->n_pairs, st);
+    t.finfo = lalloc<int4>(pr->n_pairs, st);
+    t.fcnt = lalloc<uint8_t>(pr->n_pairs, st);
     // HXF_PRIM_EPS in the environment overrides the neglect threshold (0: keep every primitive);
     // a diagnostic hook for the tests, read per build
     const char* pe = getenv("HXF_PRIM_EPS");
@@ -1380,7 +1398,8 @@ EriTables prune_tables(const hxf_pairs* pr, double other_smax, double pmax, cuda
     const double thr = eps / (std::max(other_smax, 1e-300) * std::max(pmax, 1e-300));
     if (pr->n_pairs) {
         k_prune_pairs<<<(unsigned)((pr->n_pairs + 255) / 256), 256, 0, st>>>(pr->n_pairs, pr->info, pr->meta, pr->eS,
-                                                                           thr, t.info, t.meta);
+                                                                           thr, t.info, t.meta, pr->fcol,
+                                                                           pr->n_prim_pairs, t.finfo, t.fcnt);
         note_launch();
     }
     return t;
@@ -1389,6 +1408,8 @@ EriTables prune_tables(const hxf_pairs* pr, double other_smax, double pmax, cuda
 void free_tables(EriTables& t, cudaStream_t st) {
     if (t.info) hxf_cache_free(t.info, st);
     if (t.meta) hxf_cache_free(t.meta, st);
+    if (t.finfo) hxf_cache_free(t.finfo, st);
+    if (t.fcnt) hxf_cache_free(t.fcnt, st);
     t = EriTables();
 }
 
@@ -1667,6 +1688,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             sb[b].kgeo = ket->geo;
             sb[b].bgip = bra->gip;
             sb[b].kgip = ket->gip;
+            sb[b].bfcnt = etb.fcnt;
+            sb[b].kfcnt = etk_use.fcnt;
             bfill[b] = b == 0 ? dfill : lalloc<unsigned long long>(1, st);
             bcount[b] = b == 0 ? scount : lalloc<long long>(C_NCOUNTERS, st);
             bledger[b] = b == 0 ? sledger : lalloc<unsigned long long>(LEDGER_LIMBS, st);
@@ -1686,6 +1709,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         e.kpp = ket->epp;
         e.binfo = etb.info;
         e.kinfo = etk_use.info;
+        e.bfinfo = etb.finfo;
+        e.kfinfo = etk_use.finfo;
         e.ctr = s->basis.ctr;
         e.fn = s->basis.fn;
         e.P = dens->P;
@@ -1695,8 +1720,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         e.counters = ecount;
         e.n_bpairs = bra->n_pairs;
         e.n_kpairs = ket->n_pairs;
-        e.n_bprim = bra->n_prim_pairs;
-        e.n_kprim = ket->n_prim_pairs;
+        e.n_bprim = bra->n_prim_pairs + bra->n_pairs;
+        e.n_kprim = ket->n_prim_pairs + ket->n_pairs;
         cudaStream_t se = st;
         cudaEvent_t ev_in = nullptr, ev_scr[2] = {nullptr, nullptr}, ev_eri[2] = {nullptr, nullptr};
         if (pipe) {
@@ -2235,6 +2260,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         sb.dbounds = lalloc<int64_t>(KEY_RANGES + 1, st);
         sb.bgeo = sb.kgeo = pairs->geo;   // the same far-field decisions as the hierarchical drivers
         sb.bgip = sb.kgip = pairs->gip;
+        sb.bfcnt = sb.kfcnt = et.fcnt;
         EriArgs e;
         e.dbounds = nullptr;
         e.bpi = e.kpi = pairs->pi;
@@ -2242,6 +2268,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         e.bppoff = e.kppoff = pairs->ppoff;
         e.bpp = e.kpp = pairs->epp;
         e.binfo = e.kinfo = et.info;
+        e.bfinfo = e.kfinfo = et.finfo;
         e.ctr = s->basis.ctr;
         e.fn = s->basis.fn;
         e.P = dens->P;
@@ -2250,7 +2277,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
         e.K = Kfx;
         e.counters = scount;
         e.n_bpairs = e.n_kpairs = pairs->n_pairs;
-        e.n_bprim = e.n_kprim = pairs->n_prim_pairs;
+        e.n_bprim = e.n_kprim = pairs->n_prim_pairs + pairs->n_pairs;
         da.off = off;
         da.rec = sb.rec;
         da.keys = sb.keys;

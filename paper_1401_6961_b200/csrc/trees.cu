@@ -201,8 +201,19 @@ __global__ void k_diag_q(DevBasis B, int64_t n_pairs, const int* pi, const int* 
 // primitive Schwarz factors S = sqrt(max_comp (ab|ab)) of every primitive pair,
 // and the ERI copy of each pair's primitives sorted by S, descending (ties by
 // index), so a build can drop a negligible tail by shortening the count
+//
+// Far-field collapse: a pair of two s shells on one centre is a sum of concentric
+// spherical Gaussian charges; outside their extent (where every Boys argument is past
+// the table range, i.e. exactly the quartets the far-field kernels take) its potential
+// is that of one point charge sum_u c_u / sqrt(p_u) at the centre, independent of the
+// exponents.  Such a pair gets one extra primitive at epp[n_prim + pair id] {centre,
+// p = min_u p_u (keeps T above the far-field bound the classification proved), cs = the
+// summed charge, c = cs sqrt(p)}: the far-field kernels read it instead of the list
+// (the asymptotic recurrences cancel p term by term, so any p gives the same value to
+// rounding).  Summed in epp order so mirrored pairs (i,j), (j,i) agree.
 __global__ void k_prim_schwarz_sort(DevBasis B, int64_t n_pairs, const int* pi, const int* pj,
-                                    const int64_t* ppoff, const PrimPair* pp, PrimPair* epp, double* eS) {
+                                    const int64_t* ppoff, const PrimPair* pp, PrimPair* epp, double* eS,
+                                    int64_t n_prim, int collapse, uint8_t* fcol) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= n_pairs) return;
     const int i = pi[t], j = pj[t];
@@ -233,6 +244,24 @@ __global__ void k_prim_schwarz_sort(DevBasis B, int64_t n_pairs, const int* pi, 
         epp[b0 + u] = pp[b0 + idx[u]];
         eS[b0 + u] = sv[u];
     }
+    const bool same = A.x == C.x && A.y == C.y && A.z == C.z;
+    const bool col = collapse && li == 0 && lj == 0 && same && n > 1;
+    fcol[t] = col ? 1 : 0;
+    PrimPair f = pp[b0 + idx[0]];
+    if (col) {
+        double cs = 0.0, pmin = f.p;
+        for (int u = 0; u < n; ++u) {
+            const PrimPair& q = pp[b0 + idx[u]];
+            cs += q.cs;
+            pmin = fmin(pmin, q.p);
+        }
+        f.x = A.x; f.y = A.y; f.z = A.z;
+        f.p = pmin;
+        f.ip = 1.0 / pmin;
+        f.cs = cs;
+        f.c = cs * sqrt(pmin);
+    }
+    epp[n_prim + t] = f;
 }
 
 // Far-field geometry per pair (the ERI stage's per-quartet asymptotic test,
@@ -609,10 +638,19 @@ void trees_build_pairs(hxf_pairs* pr, cudaStream_t st, const double* s_user) {
     { k_diag_q<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
                                                      pr->pp, lt.leaf_of_shell, lt.lslo, lt.lshi, nl,
                                                      pr->leaf_base, pr->q); note_launch(); }
-    pr->epp = dalloc<PrimPair>(pr->n_prim_pairs, st);
+    if (pr->n_prim_pairs + pr->n_pairs >= (1ll << 31))
+        throw HxfError{HXF_EINVAL, "too many primitive pairs for 32-bit offsets"};
+    pr->epp = dalloc<PrimPair>(pr->n_prim_pairs + pr->n_pairs, st);   // + one far-field slot per pair
     pr->eS = dalloc<double>(pr->n_prim_pairs, st);
-    { k_prim_schwarz_sort<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
-                                                                 pr->pp, pr->epp, pr->eS); note_launch(); }
+    pr->fcol = dalloc<uint8_t>(std::max<int64_t>(pr->n_pairs, 1), st);
+    {   // HXF_FAR_COLLAPSE=0: every far-field quartet keeps its full primitive lists (A/B hook)
+        const char* fc = getenv("HXF_FAR_COLLAPSE");
+        const int collapse = fc ? atoi(fc) : 1;
+        k_prim_schwarz_sort<<<nblk(pr->n_pairs, 128), 128, 0, st>>>(s->basis, pr->n_pairs, pr->pi, pr->pj, pr->ppoff,
+                                                                   pr->pp, pr->epp, pr->eS, pr->n_prim_pairs,
+                                                                   collapse, pr->fcol);
+        note_launch();
+    }
     pr->geo = dalloc<float4>(std::max<int64_t>(pr->n_pairs, 1), st);
     pr->gip = dalloc<float>(std::max<int64_t>(pr->n_pairs, 1), st);
     if (pr->n_pairs) {
