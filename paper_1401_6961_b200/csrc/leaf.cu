@@ -43,6 +43,7 @@ namespace {
 struct ScreenArgs {
     const uint64_t* tasks;
     int64_t t0, t1;
+    int tblock;               // k_screen2: a warp takes runs of tblock consecutive tasks (block-cyclic)
     const int* lslo;
     const int* lshi;
     int nleaf;
@@ -346,7 +347,12 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
 #else
 #define PROF_MARK(v)
 #endif
-    for (int64_t t = a.t0 + gw; t < a.t1; t += Wt) {
+    // block-cyclic: runs of tblock consecutive leaf tasks per warp, so a warp's survivor slab
+    // (and after the stable key sort every ERI warp) holds neighbouring tasks of one bra node
+    const int TB = a.tblock;
+    const int64_t tskip = (Wt - 1) * (int64_t)TB + 1;
+    int trun = 0;
+    for (int64_t t = a.t0 + gw * TB; t < a.t1; t += (++trun == TB ? (trun = 0, tskip) : 1)) {
         PROF_MARK(c_start);
         const uint64_t task = a.tasks[t];
         const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
@@ -1517,8 +1523,34 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             if (p) hxf_cache_free(p, st);
     }
 
+    // Leaf tasks in bra-node-major order (stable radix sort on the bra leaf ids, bits 0-29 of
+    // the task word; the traversal leaves them in the product tree's interleaved order): with
+    // the screen's block-cyclic task runs, neighbouring survivor records share the bra node's
+    // pair records, primitives, P rows and K rows.  Any order gives the same counters and,
+    // through the integer accumulators, bitwise the same K and ledger words.
+    {
+        const char* ls = getenv("HXF_LEAF_SORT");
+        const bool leaf_sort = ls ? atoi(ls) != 0 : true;
+        if (leaf_sort && tr.n_leaf > 4096) {
+            NvtxRange nvtx_ls("hxf: leaf task order");
+            Timer tls(st);
+            uint64_t* sorted = lalloc<uint64_t>(tr.n_leaf, st);
+            size_t tb = 0;
+            HXF_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, tr.leaf, sorted, tr.n_leaf, 0, 30, st));
+            void* tmp = lalloc<char>(tb, st);
+            HXF_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, tr.leaf, sorted, tr.n_leaf, 0, 30, st));
+            note_launch();
+            hxf_cache_free(tmp, st);
+            hxf_cache_free(tr.leaf, st);
+            tr.leaf = sorted;
+            g_timings[0] += tls.stop();   // counted with the traversal
+        }
+    }
     ScreenArgs sa;
     sa.tasks = tr.leaf;
+    const char* tb_env = getenv("HXF_TASK_BLOCK");
+    const int tblock_max = std::max(1, tb_env ? atoi(tb_env) : 32);
+    sa.tblock = 1;
     std::vector<int> lslo(s->n_leaves), lshi(s->n_leaves);
     {
         const int D = s->n_levels - 1;
@@ -1584,6 +1616,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     const unsigned screen_grid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * (sym ? 12 : 8)));
     auto launch_screen = [&](bool emit) {
+        // task runs per warp: up to tblock_max, shorter when the range would leave warps idle
+        sa.tblock = (int)std::max<int64_t>(1, std::min<int64_t>(tblock_max, (sa.t1 - sa.t0) / ((int64_t)screen_grid * sw)));
         if (flat) {
             if (eight) { if (emit) k_screen<true, true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false, true><<<screen_grid, sw * 32, 0, st>>>(sa); }
             else if (sym) { if (emit) k_screen<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
