@@ -137,6 +137,33 @@ void* hxf_cache_alloc(size_t bytes, cudaStream_t st) {
     return p;
 }
 
+// Free device memory for sizing a build's survivor buffers: when less than `want` bytes are
+// free, the cached scratch blocks of earlier builds (other sizes, other drivers) are handed
+// back first -- a cache that starves the next build's chunk capacity defeats its purpose.
+size_t hxf_free_memory(size_t want) {
+    size_t freeb = 0, totb = 0;
+    cudaMemGetInfo(&freeb, &totb);
+    if (freeb >= want) return freeb;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceSynchronize();
+    ScratchCache& c = scratch_cache();
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        for (auto& kv : c.free_lists) {
+            if (std::get<0>(kv.first) != dev) continue;
+            for (void* q : kv.second) {
+                cudaFree(q);
+                c.dev_of.erase(q);
+            }
+            kv.second.clear();
+        }
+    }
+    cudaMemGetInfo(&freeb, &totb);
+    return freeb;
+}
+
+
 void hxf_cache_free(void* p, cudaStream_t st) {
     if (!p) return;
     ScratchCache& c = scratch_cache();

@@ -150,6 +150,8 @@ struct hxf_pairs {
 // to cudaFreeAsync.
 void* hxf_cache_alloc(size_t bytes, cudaStream_t st);
 void hxf_cache_free(void* p, cudaStream_t st);
+// free device bytes; hands the cached scratch back first when fewer than `want` are free
+size_t hxf_free_memory(size_t want);
 
 struct hxf_density {
     hxf_system* sys;

@@ -93,11 +93,16 @@ struct ScreenArgs {
 // (An 8-bit key -- far, class, min(nk, 8), one radix pass instead of two -- saves
 // ~170 ms of sort per c5 build and costs 880 ms in the ERI kernels, whose warps then mix
 // bra primitive counts: profiles/r02_ab_eri_memory.log.  13 bits stay.)
-#define KEY_FAR 0x1000
-#define KEY_BITS 13
-#define KEY_CLASS_SPAN 256
-#define KEY_OF(far, cls) (((far) ? KEY_FAR : 0) | ((cls) << 8))
-#define KEY_RANGES (1 << KEY_BITS)
+// ERI bin of a survivor (written over the screen's 12-bit class / count key by
+// k_bin_classify): ((far * 16 + class) * 9 + nb-1) * 9 + nk-1, 2592 bins (a pair has at most
+// 3 x 3 primitives); slab padding goes to bin ERI_NBINS.  One ERI kernel per (far, class)
+// reads the 81 bins of its primitive-count combinations as one record range.
+// (Measured and dropped: bra pair id bits appended to the key -- with the leaf tasks in
+// bra-node-major order 2 / 3 extra bits cost 80 / 106 ms of ERI kernels at c5: they scatter a
+// leaf task's run over sub-ranges and lose more ket-side locality than the bra side gains.)
+#define ERI_NBINS 2592
+#define KEY_CLASS_SPAN 81
+#define KEY_OF(far, cls) ((((far) ? 16 : 0) + (cls)) * KEY_CLASS_SPAN)
 
 // Survivor emission through per-warp slabs: one global atomic reserves SLAB
 // record slots; a slab that cannot take the next ballot is padded with
@@ -1057,66 +1062,173 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
     }
 }
 
-// Per-quartet far-field test over one chunk of survivor records, before the
-// sort: sets key bit 12 for the quartets whose every primitive quartet has a
-// Boys argument past the table range (per-pair enclosing spheres, k_pair_geo).
-// The decision is a function of the quartet alone, so every driver (naive,
-// fourfold, eightfold, the direct twin) evaluates a given quartet with the same
-// arithmetic and their K agree bit for bit.  A streaming pass (8 + 2 bytes per
-// record; the spheres are gathered with the locality of the screen's order).
-__global__ void k_classify_far(const uint64_t* __restrict__ rec, uint16_t* __restrict__ keys, int64_t n,
-                               const float4* __restrict__ bgeo, const float* __restrict__ bgip,
-                               const float4* __restrict__ kgeo, const float* __restrict__ kgip,
-                               const uint8_t* __restrict__ bfcnt, const uint8_t* __restrict__ kfcnt) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const uint16_t key = keys[t];
-        if (key == SENTINEL_KEY) continue;
-        const uint64_t r = rec[t];
-        const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
-        const int L = __popc((key >> 8) & 15);
-        const float4 gb = __ldg(bgeo + pb), gk = __ldg(kgeo + pk);
-        const float ip = __ldg(bgip + pb) + __ldg(kgip + pk);
+// Survivor binning: a stable counting sort by ERI bin in four kernels (no library sort).
+//
+// Every warp owns one contiguous run of the chunk's records (a "column") and walks it in
+// order with private shared-memory counters, so no atomics are needed and the sort is
+// stable: inside a bin the records keep the screen's order, which is the locality the ERI
+// kernels live on (neighbouring records = neighbouring leaf tasks of one bra node).
+//
+// k_bin_classify  per-quartet far-field test + final bin id, written over the screen's key,
+//                 and the column's histogram.  The far-field decision is a function of the
+//                 quartet alone (the two pairs' enclosing spheres, k_pair_geo), so every
+//                 driver (naive, fourfold, eightfold, the direct twin) evaluates a given
+//                 quartet with the same arithmetic.
+// k_bin_rowscan   per bin: exclusive scan over the columns, in place, and the bin total.
+// k_bin_scan      bin starts from the totals: the ERI kernels' record ranges.
+// k_bin_scatter   every warp re-reads its run and moves the records: slot = bin start +
+//                 column offset + the warp's running count (+ rank among the lanes of the
+//                 same bin, by __match_any_sync).
+// Traffic: 10 B read + 2 B written, then 10 B read + 8 B written per record.
+#define BIN_WARPS 4
+#ifndef BIN_UNROLL
+#define BIN_UNROLL 8
+#endif
+
+struct BinGeo {
+    const float4* bgeo;
+    const float* bgip;
+    const float4* kgeo;
+    const float* kgip;
+    const uint8_t* bfcnt;
+    const uint8_t* kfcnt;
+    int do_far;
+};
+
+__device__ __forceinline__ int eri_bin_of(uint16_t key, uint64_t r, const BinGeo& g) {
+    if (key == SENTINEL_KEY) return ERI_NBINS;
+    const int64_t pb = (int64_t)(r & 0xfffffff), pk = (int64_t)((r >> 28) & 0xfffffff);
+    const int cls = (key >> 8) & 15;   // the screen's key: class << 8 | nb-1 << 4 | nk-1
+    int nb1 = (key >> 4) & 15, nk1 = key & 15, far = 0;
+    if (g.do_far) {
+        const int L = __popc(cls);
+        const float4 gb = __ldg(g.bgeo + pb), gk = __ldg(g.kgeo + pk);
+        const float ip = __ldg(g.bgip + pb) + __ldg(g.kgip + pk);
         const float dx = gb.x - gk.x, dy = gb.y - gk.y, dz = gb.z - gk.z;
         const float d = sqrtf(dx * dx + dy * dy + dz * dz) * (1.0f - 1e-5f) - gb.w - gk.w;
         // a far quartet sorts by its far-field primitive counts (1 for a collapsed pair)
-        if (d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip)
-            keys[t] = (uint16_t)(KEY_FAR | (key & 0xf00) | (__ldg(bfcnt + pb) << 4) | __ldg(kfcnt + pk));
+        if (d > 0.0f && d * d >= (float)(boys_far_t(L) * 1.0001) * ip) {
+            far = 1;
+            nb1 = __ldg(g.bfcnt + pb);
+            nk1 = __ldg(g.kfcnt + pk);
+        }
     }
+    return ((far * 16 + cls) * 9 + nb1) * 9 + nk1;
 }
 
-// experiment (HXF_EXP_SORTPB): 41-bit key = sort key << 28 | bra (1) or ket (2) pair id
-__global__ void k_exp_key64(const uint16_t* keys, const uint64_t* rec, int64_t n, int which, uint64_t* out) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = rec[t];
-        const uint64_t id = which == 1 ? (r & 0xfffffff) : ((r >> 28) & 0xfffffff);
-        out[t] = ((uint64_t)keys[t] << 28) | id;
+// wseg: records per column, a multiple of 32 * BIN_UNROLL
+__global__ void __launch_bounds__(BIN_WARPS * 32) k_bin_classify(
+    const uint64_t* __restrict__ rec, uint16_t* __restrict__ keys, int64_t n, int64_t wseg, BinGeo g,
+    unsigned* __restrict__ hist) {
+    __shared__ unsigned h_all[BIN_WARPS][ERI_NBINS + 1];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned* h = h_all[wid];
+    for (int i = lane; i <= ERI_NBINS; i += 32) h[i] = 0;
+    __syncwarp();
+    const int64_t col = (int64_t)blockIdx.x * BIN_WARPS + wid, ncol = (int64_t)gridDim.x * BIN_WARPS;
+    const int64_t lo = col * wseg, hi = min(n, lo + wseg);
+    for (int64_t t0 = lo; t0 < hi; t0 += 32 * BIN_UNROLL) {
+        uint16_t key[BIN_UNROLL];
+        uint64_t r[BIN_UNROLL];
+#pragma unroll
+        for (int u = 0; u < BIN_UNROLL; ++u) {
+            const int64_t t = t0 + 32 * u + lane;
+            key[u] = t < hi ? keys[t] : SENTINEL_KEY;
+            r[u] = t < hi ? rec[t] : 0ull;
+        }
+        int bin[BIN_UNROLL];
+#pragma unroll
+        for (int u = 0; u < BIN_UNROLL; ++u) bin[u] = eri_bin_of(key[u], r[u], g);
+#pragma unroll
+        for (int u = 0; u < BIN_UNROLL; ++u) {
+            const int64_t t = t0 + 32 * u + lane;
+            const bool on = t < hi;
+            if (on) keys[t] = (uint16_t)bin[u];
+            const int b = on ? bin[u] : -1 - lane;   // out of range: a group of its own, not counted
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            if (on && (__ffs(peers) - 1) == lane) h[b] += (unsigned)__popc(peers);
+            __syncwarp();
+        }
     }
+    __syncwarp();
+    for (int i = lane; i <= ERI_NBINS; i += 32) hist[(int64_t)i * ncol + col] = h[i];
 }
 
-// lower bounds of every 12-bit key value in the sorted key array
-__global__ void k_key_bounds(const uint16_t* keys, int64_t n, int64_t* bounds) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > KEY_RANGES) return;
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if ((int)keys[mid] < c) lo = mid + 1;
-        else hi = mid;
+// per bin (one warp each): exclusive scan of the row of column counts, in place; the row total
+__global__ void __launch_bounds__(256) k_bin_rowscan(unsigned* __restrict__ hist, int ncol, long long* __restrict__ total) {
+    const int b = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (b > ERI_NBINS) return;
+    unsigned* row = hist + (int64_t)b * ncol;
+    unsigned run = 0;
+    for (int k0 = 0; k0 < ncol; k0 += 32) {
+        const int k = k0 + lane;
+        const unsigned v = k < ncol ? row[k] : 0u;
+        unsigned inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (k < ncol) row[k] = run + inc - v;
+        run += __shfl_sync(0xffffffffu, inc, 31);
     }
-    bounds[c] = lo;
+    if (lane == 0) total[b] = run;
 }
 
-__global__ void k_class_bounds(const uint16_t* keys, int64_t n, int64_t* bounds) {
-    const int c = threadIdx.x;
-    if (c > 16) return;
-    // first index with class >= c (keys sorted by class, then primitive counts)
-    int64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if ((int)(keys[mid] >> 8) < c) lo = mid + 1;
-        else hi = mid;
+// bin starts from the bin totals (one block; ERI_NBINS + 1 totals, the scan is serial in
+// shared memory: ~10 us)
+__global__ void __launch_bounds__(1024) k_bin_scan(const long long* __restrict__ total, int64_t* __restrict__ bounds) {
+    __shared__ long long tot[ERI_NBINS + 2];
+    for (int b = threadIdx.x; b <= ERI_NBINS; b += 1024) tot[b] = total[b];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long run = 0;
+        for (int b = 0; b <= ERI_NBINS; ++b) {
+            const long long c = tot[b];
+            tot[b] = run;
+            run += c;
+        }
+        tot[ERI_NBINS + 1] = run;
     }
-    bounds[c] = lo;
+    __syncthreads();
+    for (int b = threadIdx.x; b <= ERI_NBINS + 1; b += 1024) bounds[b] = tot[b];
+}
+
+__global__ void __launch_bounds__(BIN_WARPS * 32) k_bin_scatter(
+    const uint64_t* __restrict__ rec, const uint16_t* __restrict__ keys, int64_t n, int64_t wseg,
+    const unsigned* __restrict__ hist, const int64_t* __restrict__ bounds, uint64_t* __restrict__ out) {
+    // next free slot of this column's run in each bin, relative to the bin start (< 2^29 per chunk)
+    __shared__ unsigned pos_all[BIN_WARPS][ERI_NBINS + 1];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned* pos = pos_all[wid];
+    const int64_t col = (int64_t)blockIdx.x * BIN_WARPS + wid, ncol = (int64_t)gridDim.x * BIN_WARPS;
+    for (int i = lane; i <= ERI_NBINS; i += 32) pos[i] = hist[(int64_t)i * ncol + col];
+    __syncwarp();
+    const int64_t lo = col * wseg, hi = min(n, lo + wseg);
+    for (int64_t t0 = lo; t0 < hi; t0 += 32 * BIN_UNROLL) {
+        int bin[BIN_UNROLL];
+        uint64_t r[BIN_UNROLL];
+#pragma unroll
+        for (int u = 0; u < BIN_UNROLL; ++u) {
+            const int64_t t = t0 + 32 * u + lane;
+            bin[u] = t < hi ? (int)keys[t] : -1 - lane;
+            r[u] = t < hi ? rec[t] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < BIN_UNROLL; ++u) {
+            const int b = bin[u];
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            const int leader = __ffs(peers) - 1;
+            unsigned base = 0;
+            if (b >= 0 && leader == lane) {
+                base = pos[b];
+                pos[b] = base + (unsigned)__popc(peers);
+            }
+            __syncwarp();
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (b >= 0) out[bounds[b] + base + __popc(peers & ((1u << lane) - 1u))] = r[u];
+        }
+    }
 }
 
 __global__ void k_log(const uint64_t* rec, int64_t n, const int* bpi, const int* bpj, const int* kpi,
@@ -1267,11 +1379,11 @@ void launch_eri_class(int cls, bool far, const EriArgs& e, cudaStream_t st) {
 thread_local double g_timings[8];
 
 struct SurvivorBufs {
-    uint64_t *rec, *rec2;
-    uint16_t *keys, *keys2;
-    void* sort_tmp;
-    size_t sort_tb;
-    int64_t* dbounds;
+    uint64_t *rec, *rec2;   // screen order; binned
+    uint16_t* keys;
+    unsigned* hist;         // (ERI_NBINS + 1) x (bin_blocks * BIN_WARPS columns) counts, then first slots
+    int bin_blocks;
+    int64_t* dbounds;       // ERI_NBINS + 2 bin starts (slab padding last)
     // per-pair spheres for the per-quartet far-field pass (NULL: skip it)
     const float4* bgeo = nullptr;
     const float4* kgeo = nullptr;
@@ -1300,51 +1412,52 @@ struct Timer {
     }
 };
 
-// sort one chunk of survivors by (class, nb, nk) and run the per-class ERI
-// kernels over the sorted copy, without a host synchronisation: every class
-// kernel reads its record range from the device-side key bounds (empty classes
+// bin one chunk of survivors by (far, class, nb, nk) and run the per-class ERI
+// kernels over the binned copy, without a host synchronisation: every class
+// kernel reads its record range from the device-side bin starts (empty classes
 // exit at once)
 void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cudaStream_t st,
                             cudaEvent_t after_sort = nullptr) {
-    if (b.bgeo && !HXF_ERI_NOFAR) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrec + 255) / 256, (int64_t)sms * 8));
-        k_classify_far<<<g, 256, 0, st>>>(b.rec, b.keys, nrec, b.bgeo, b.bgip, b.kgeo, b.kgip, b.bfcnt, b.kfcnt);
-        note_launch();
-    }
-    size_t tb = b.sort_tb;
-    HXF_CUDA(cub::DeviceRadixSort::SortPairs(b.sort_tmp, tb, b.keys, b.keys2, b.rec, b.rec2, nrec, 0, KEY_BITS, st));
-    { k_key_bounds<<<KEY_RANGES / 256 + 1, 256, 0, st>>>(b.keys2, nrec, b.dbounds); note_launch(); }
-    // HXF_EXP_SORTPB=1|2 (experiment, costs a 41-bit radix sort): inside every key range
-    // order the records by bra pair id (1) or by ket pair id (2), to measure what a warp
-    // that shares its bra / ket pair would gain in the ERI kernels
-    static const int exp_sortpb = getenv("HXF_EXP_SORTPB") ? atoi(getenv("HXF_EXP_SORTPB")) : 0;
-    uint64_t* rec_sorted = b.rec2;
-    uint64_t *k64a = nullptr, *k64b = nullptr, *rec3 = nullptr;
-    void* tmp64 = nullptr;
-    if (exp_sortpb) {
-        k64a = lalloc<uint64_t>(nrec, st);
-        k64b = lalloc<uint64_t>(nrec, st);
-        rec3 = lalloc<uint64_t>(nrec, st);
-        k_exp_key64<<<(unsigned)std::min<int64_t>((nrec + 255) / 256, 1 << 20), 256, 0, st>>>(b.keys2, b.rec2, nrec,
-                                                                                      exp_sortpb, k64a);
-        size_t tb64 = 0;
-        HXF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb64, k64a, k64b, b.rec2, rec3, nrec, 0, 28 + KEY_BITS, st));
-        tmp64 = lalloc<char>(tb64, st);
-        HXF_CUDA(cub::DeviceRadixSort::SortPairs(tmp64, tb64, k64a, k64b, b.rec2, rec3, nrec, 0, 28 + KEY_BITS, st));
-        rec_sorted = rec3;
-    }
+    const int G = b.bin_blocks;
+    const int64_t ncol = (int64_t)G * BIN_WARPS;
+    // contiguous run per column (warp), a multiple of the warp's stride
+    constexpr int64_t WSTEP = 32 * BIN_UNROLL;
+    const int64_t wseg = ((nrec + ncol - 1) / ncol + WSTEP - 1) / WSTEP * WSTEP;
+    long long* total = reinterpret_cast<long long*>(b.dbounds + ERI_NBINS + 2);
+    const BinGeo geo{b.bgeo, b.bgip, b.kgeo, b.kgip, b.bfcnt, b.kfcnt, (b.bgeo && !HXF_ERI_NOFAR) ? 1 : 0};
+    k_bin_classify<<<G, BIN_WARPS * 32, 0, st>>>(b.rec, b.keys, nrec, wseg, geo, b.hist);
+    k_bin_rowscan<<<(ERI_NBINS + 1 + 7) / 8, 256, 0, st>>>(b.hist, (int)ncol, total);
+    k_bin_scan<<<1, 1024, 0, st>>>(total, b.dbounds);
+    k_bin_scatter<<<G, BIN_WARPS * 32, 0, st>>>(b.rec, b.keys, nrec, wseg, b.hist, b.dbounds, b.rec2);
+    for (int k = 0; k < 4; ++k) note_launch();
     if (after_sort) cudaEventRecord(after_sort, st);
-    e.rec = rec_sorted;
+    e.rec = b.rec2;
     e.n = 0;
     e.dbounds = b.dbounds;
     for (int c = 0; c < 16; ++c) launch_eri_class(c, false, e, st);
     for (int c = 0; c < 16; ++c) launch_eri_class(c, true, e, st);
     HXF_CUDA(cudaGetLastError());
-    for (void* p : {(void*)k64a, (void*)k64b, (void*)rec3, tmp64})
-        if (p) hxf_cache_free(p, st);
+}
+
+// the survivor buffers of one chunk set (cap records)
+void survivor_bufs_alloc(SurvivorBufs& sb, int64_t cap, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    sb.rec = lalloc<uint64_t>(cap, st);
+    sb.rec2 = lalloc<uint64_t>(cap, st);
+    sb.keys = lalloc<uint16_t>(cap, st);
+    // up to 5 blocks of BIN_WARPS warps x 41.5 KB of counters per SM; fewer columns = fewer
+    // concurrent (column, bin) write cursors for L2 to merge into full sectors
+    const char* bb = getenv("HXF_BIN_BLOCKS");
+    sb.bin_blocks = sms * std::max(1, std::min(5, bb ? atoi(bb) : 5));
+    sb.hist = lalloc<unsigned>((size_t)(ERI_NBINS + 1) * sb.bin_blocks * BIN_WARPS, st);
+    sb.dbounds = lalloc<int64_t>(2 * (ERI_NBINS + 2), st);   // bin starts, then the bin totals
+}
+
+void survivor_bufs_free(SurvivorBufs& sb, cudaStream_t st) {
+    for (void* p : {(void*)sb.rec, (void*)sb.rec2, (void*)sb.keys, (void*)sb.hist, (void*)sb.dbounds})
+        hxf_cache_free(p, st);
 }
 
 void host_ledger_add(unsigned long long* acc, const unsigned long long* v) {
@@ -1530,7 +1643,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     // through the integer accumulators, bitwise the same K and ledger words.
     {
         const char* ls = getenv("HXF_LEAF_SORT");
-        const bool leaf_sort = ls ? atoi(ls) != 0 : true;
+        const int leaf_sort = ls ? atoi(ls) : 1;
         if (leaf_sort && tr.n_leaf > 4096) {
             NvtxRange nvtx_ls("hxf: leaf task order");
             Timer tls(st);
@@ -1549,7 +1662,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     ScreenArgs sa;
     sa.tasks = tr.leaf;
     const char* tb_env = getenv("HXF_TASK_BLOCK");
-    const int tblock_max = std::max(1, tb_env ? atoi(tb_env) : 32);
+    const int tblock_max = std::max(1, tb_env ? atoi(tb_env) : 16);
     sa.tblock = 1;
     std::vector<int> lslo(s->n_leaves), lshi(s->n_leaves);
     {
@@ -1699,8 +1812,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         const char* pv = getenv("HXF_PIPE");
         const bool pipe = pv && pv[0] == '1';
         const int NB = pipe ? 2 : 1;
-        size_t freeb = 0, totb = 0;
-        cudaMemGetInfo(&freeb, &totb);
+        // (a full-size chunk set is 2^29 records x 160 B; cached scratch of other builds yields to it)
+        const size_t freeb = hxf_free_memory((size_t)160 * NB << 29);
         // survivor chunk capacity: ~40 B of device memory per record and buffer
         // set (two record buffers, two key buffers, radix-sort scratch)
         const int64_t cap = std::min<int64_t>(1ll << 29, std::max<int64_t>(1 << 16, (int64_t)(freeb / (160 * NB))));
@@ -1709,15 +1822,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         long long* bcount[2];
         unsigned long long* bledger[2];
         for (int b = 0; b < NB; ++b) {
-            sb[b].rec = lalloc<uint64_t>(cap, st);
-            sb[b].rec2 = lalloc<uint64_t>(cap, st);
-            sb[b].keys = lalloc<uint16_t>(cap, st);
-            sb[b].keys2 = lalloc<uint16_t>(cap, st);
-            sb[b].sort_tb = 0;
-            HXF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb[b].sort_tb, sb[b].keys, sb[b].keys2, sb[b].rec,
-                                            sb[b].rec2, cap, 0, KEY_BITS, st));
-            sb[b].sort_tmp = lalloc<char>(sb[b].sort_tb, st);
-            sb[b].dbounds = lalloc<int64_t>(KEY_RANGES + 1, st);
+            survivor_bufs_alloc(sb[b], cap, st);
             sb[b].bgeo = bra->geo;
             sb[b].kgeo = ket->geo;
             sb[b].bgip = bra->gip;
@@ -1878,9 +1983,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
             cudaStreamDestroy(se);
         }
         for (int b = 0; b < NB; ++b) {
-            for (void* p : {(void*)sb[b].rec, (void*)sb[b].rec2, (void*)sb[b].keys, (void*)sb[b].keys2,
-                            sb[b].sort_tmp, (void*)sb[b].dbounds})
-                hxf_cache_free(p, st);
+            survivor_bufs_free(sb[b], st);
             if (b) {
                 hxf_cache_free(bfill[b], st);
                 hxf_cache_free(bcount[b], st);
@@ -2280,18 +2383,10 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     if (o->evaluate && total) {
         Kfx = lalloc<unsigned long long>(nfn2, st);
         HXF_CUDA(cudaMemsetAsync(Kfx, 0, nfn2 * sizeof(unsigned long long), st));
-        size_t freeb = 0, totb = 0;
-        cudaMemGetInfo(&freeb, &totb);
+        const size_t freeb = hxf_free_memory((size_t)160 << 29);
         const int64_t cap = std::min<int64_t>(1ll << 29, std::max<int64_t>(1 << 16, (int64_t)(freeb / 160)));
         SurvivorBufs sb;
-        sb.rec = lalloc<uint64_t>(cap, st);
-        sb.rec2 = lalloc<uint64_t>(cap, st);
-        sb.keys = lalloc<uint16_t>(cap, st);
-        sb.keys2 = lalloc<uint16_t>(cap, st);
-        sb.sort_tb = 0;
-        HXF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sb.sort_tb, sb.keys, sb.keys2, sb.rec, sb.rec2, cap, 0, KEY_BITS, st));
-        sb.sort_tmp = lalloc<char>(sb.sort_tb, st);
-        sb.dbounds = lalloc<int64_t>(KEY_RANGES + 1, st);
+        survivor_bufs_alloc(sb, cap, st);
         sb.bgeo = sb.kgeo = pairs->geo;   // the same far-field decisions as the hierarchical drivers
         sb.bgip = sb.kgip = pairs->gip;
         sb.bfcnt = sb.kfcnt = et.fcnt;
@@ -2336,8 +2431,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
             }
             p0 = p1;
         }
-        for (void* p : {(void*)sb.rec, (void*)sb.rec2, (void*)sb.keys, (void*)sb.keys2, sb.sort_tmp, (void*)sb.dbounds})
-            hxf_cache_free(p, st);
+        survivor_bufs_free(sb, st);
     }
     // ---- epilogue
     Timer tep(st);
