@@ -279,6 +279,27 @@ int hxf_block_pack(const int64_t* K, int n, int bs, const uint8_t* mask, const i
 int hxf_block_unpack(int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, const int64_t* buf,
                      void* stream);
 
+/* K quadtree leaves and the row-owning reduce-scatter (second part; the
+ * reference treats K as a quadtree over the same index bisection as P, PAPER.md:174-198;
+ * csrc/reduce.cu).  Leaf tile (r, c) = rows [flo[r], fhi[r]) x cols [flo[c], fhi[c]) of the
+ * partition's leaf spans (device int32 arrays of nleaf entries, the function ranges of
+ * quadtree.py:28-60's leaf Spans in order).
+ * hxf_span_mask: mask[r * nleaf + c] = 1 if leaf tile (r, c) of the n x n int64 K holds a nonzero.
+ * hxf_span_pack / hxf_span_unpack: move the flagged tiles of row spans [r0, r1) between K and
+ *   buf; tile (r, c) lives at buf + off[r * nleaf + c] - off_base, row-major inside (off: the
+ *   caller's exclusive scan of mask * tile size, in elements).  K addresses matrix row i at
+ *   K + (i - row_base) * n, so K may be a row block of the matrix.
+ * hxf_fixed_fold: K <- K + K^T in place (exact integer adds). */
+int hxf_span_mask(const int64_t* K, int n, const int32_t* flo, const int32_t* fhi, int nleaf, uint8_t* mask,
+                  void* stream);
+int hxf_span_pack(const int64_t* K, int n, int row_base, const int32_t* flo, const int32_t* fhi, int nleaf,
+                  int r0, int r1, const uint8_t* mask, const int64_t* off, int64_t off_base, int64_t* buf,
+                  void* stream);
+int hxf_span_unpack(int64_t* K, int n, int row_base, const int32_t* flo, const int32_t* fhi, int nleaf,
+                    int r0, int r1, const uint8_t* mask, const int64_t* off, int64_t off_base, const int64_t* buf,
+                    void* stream);
+int hxf_fixed_fold(int64_t* K, int n, void* stream);
+
 /* Overlap-pruning ties of a pair tree: nodes whose block max |S| lies within 1e-12
  * (relative) of tau_ovlp, found when the tree was built.  Copies up to `capacity`
  * records (out may be NULL) and sets *count to the number found. */

@@ -26,7 +26,7 @@ EXPORTED = ("hxf_last_error", "hxf_version", "hxf_system_create", "hxf_system_de
             "hxf_last_timings", "hxf_symmetrize", "hxf_fp64_peak", "hxf_launch_count",
             "hxf_fixed_to_double", "hxf_scratch_release", "hxf_hilbert_order",
             "hxf_partition_build", "hxf_block_mask", "hxf_block_slots", "hxf_block_pack",
-            "hxf_block_unpack")
+            "hxf_block_unpack", "hxf_span_mask", "hxf_span_pack", "hxf_span_unpack", "hxf_fixed_fold")
 
 
 class LogicError(RuntimeError):
@@ -151,6 +151,10 @@ def lib():
     L.hxf_block_slots.argtypes = [vp, i64, vp, P(i64), vp]
     L.hxf_block_pack.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     L.hxf_block_unpack.argtypes = [vp, i32, i32, vp, vp, vp, vp]
+    L.hxf_span_mask.argtypes = [vp, i32, vp, vp, i32, vp, vp]
+    L.hxf_span_pack.argtypes = [vp, i32, i32, vp, vp, i32, i32, i32, vp, vp, i64, vp, vp]
+    L.hxf_span_unpack.argtypes = [vp, i32, i32, vp, vp, i32, i32, i32, vp, vp, i64, vp, vp]
+    L.hxf_fixed_fold.argtypes = [vp, i32, vp]
     L.hxf_partition_build.argtypes = [vp, i64, i32, vp, vp, i64, vp, i32, P(i64), P(i32), vp]
     _lib = L
     return L

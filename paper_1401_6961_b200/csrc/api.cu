@@ -23,6 +23,12 @@ void note_launch(int n) { g_launches += n; }
 int hxf_last_timings_impl(double* ms, int n);
 int fixed_to_double_impl(const int64_t* Kfx, int64_t n2, int S, double* K, cudaStream_t st);
 void block_mask_device(const int64_t* K, int n, int bs, uint8_t* mask, cudaStream_t st);
+void span_mask_device(const int64_t* K, int n, const int* flo, const int* fhi, int nleaf, uint8_t* mask,
+                      cudaStream_t st);
+void span_move_device(int64_t* K, int n, int row_base, const int* flo, const int* fhi, int nleaf, int r0, int r1,
+                      const uint8_t* mask, const int64_t* off, int64_t off_base, int64_t* buf, bool pack,
+                      cudaStream_t st);
+void fold_fixed_device(int64_t* K, int n, cudaStream_t st);
 int64_t block_slots_device(const uint8_t* mask, int64_t nt, int64_t* slot, cudaStream_t st);
 void block_move_device(int64_t* K, int n, int bs, const uint8_t* mask, const int64_t* slot, int64_t* buf,
                        bool pack, cudaStream_t st);
@@ -619,6 +625,56 @@ int hxf_block_unpack(int64_t* K, int n, int bs, const uint8_t* mask, const int64
         if (n > 0 && (!K || !mask || !slot || !buf)) throw HxfError{HXF_EINVAL, "NULL argument"};
         need_device();
         block_move_device(K, n, bs, mask, slot, const_cast<int64_t*>(buf), false, (cudaStream_t)stream);
+    })
+}
+
+static void check_spans(int n, int nleaf, const void* flo, const void* fhi) {
+    if (n < 0 || nleaf < 0 || nleaf > 32767) throw HxfError{HXF_EINVAL, "bad size"};
+    if (nleaf > 0 && (!flo || !fhi)) throw HxfError{HXF_EINVAL, "NULL argument"};
+}
+
+int hxf_span_mask(const int64_t* K, int n, const int32_t* flo, const int32_t* fhi, int nleaf, uint8_t* mask,
+                  void* stream) {
+    HXF_TRY({
+        check_spans(n, nleaf, flo, fhi);
+        if (n > 0 && nleaf > 0 && (!K || !mask)) throw HxfError{HXF_EINVAL, "NULL argument"};
+        need_device();
+        span_mask_device(K, n, flo, fhi, nleaf, mask, (cudaStream_t)stream);
+    })
+}
+
+int hxf_span_pack(const int64_t* K, int n, int row_base, const int32_t* flo, const int32_t* fhi, int nleaf,
+                  int r0, int r1, const uint8_t* mask, const int64_t* off, int64_t off_base, int64_t* buf,
+                  void* stream) {
+    HXF_TRY({
+        check_spans(n, nleaf, flo, fhi);
+        if (r0 < 0 || r1 > nleaf || r0 > r1) throw HxfError{HXF_EINVAL, "bad row span range"};
+        if (r1 > r0 && n > 0 && (!K || !mask || !off || !buf)) throw HxfError{HXF_EINVAL, "NULL argument"};
+        need_device();
+        span_move_device(const_cast<int64_t*>(K), n, row_base, flo, fhi, nleaf, r0, r1, mask, off, off_base, buf,
+                         true, (cudaStream_t)stream);
+    })
+}
+
+int hxf_span_unpack(int64_t* K, int n, int row_base, const int32_t* flo, const int32_t* fhi, int nleaf,
+                    int r0, int r1, const uint8_t* mask, const int64_t* off, int64_t off_base, const int64_t* buf,
+                    void* stream) {
+    HXF_TRY({
+        check_spans(n, nleaf, flo, fhi);
+        if (r0 < 0 || r1 > nleaf || r0 > r1) throw HxfError{HXF_EINVAL, "bad row span range"};
+        if (r1 > r0 && n > 0 && (!K || !mask || !off || !buf)) throw HxfError{HXF_EINVAL, "NULL argument"};
+        need_device();
+        span_move_device(K, n, row_base, flo, fhi, nleaf, r0, r1, mask, off, off_base, const_cast<int64_t*>(buf),
+                         false, (cudaStream_t)stream);
+    })
+}
+
+int hxf_fixed_fold(int64_t* K, int n, void* stream) {
+    HXF_TRY({
+        if (n < 0) throw HxfError{HXF_EINVAL, "bad size"};
+        if (n > 0 && !K) throw HxfError{HXF_EINVAL, "NULL argument"};
+        need_device();
+        fold_fixed_device(K, n, (cudaStream_t)stream);
     })
 }
 

@@ -1554,6 +1554,15 @@ int fixed_to_double_impl(const int64_t* Kfx, int64_t n2, int S, double* K, cudaS
     return HXF_OK;
 }
 
+// A + A^T in place on a fixed-point accumulator (exact integer adds): the eightfold epilogue,
+// and the symmetric form a shard's partial takes before a row-owning reduce-scatter
+void fold_fixed_device(int64_t* K, int n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_fold_fx<<<1024, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(K), n);
+    note_launch();
+    HXF_CUDA(cudaGetLastError());
+}
+
 int hxf_last_timings_impl(double* ms, int n) {
     for (int k = 0; k < n && k < 8; ++k) ms[k] = g_timings[k];
     return HXF_OK;

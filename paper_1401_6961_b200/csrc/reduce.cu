@@ -165,3 +165,100 @@ void block_move_device(int64_t* K, int n, int bs, const uint8_t* mask, const int
     note_launch();
     HXF_CUDA(cudaGetLastError());
 }
+
+// ---------------------------------------------------------------------------
+// K quadtree leaves (second part; PAPER.md:174-198 treats K as a
+// quadtree over the same index bisection as P).  A leaf tile (r, c) is the block
+// rows [flo[r], fhi[r]) x cols [flo[c], fhi[c]) of the partition's leaf spans r, c
+// (ragged: spans hold different function counts).  Occupancy of the leaf tiles is
+// the quadtree's bottom level; the host ORs it up the span tree.  Pack / unpack move
+// the flagged tiles between K (or a row block of K) and one dense buffer in tile
+// row-major order, each tile row-major inside, at the element offsets the caller
+// scanned from the occupancy: a rank's rows are one contiguous slice of the buffer,
+// which is what the reduce-scatter of distributed.reduce_scatter_quadtree sends.
+// One CTA per leaf row span: whole K rows are read / written coalesced.
+
+namespace {
+
+__global__ void k_span_index(const int* __restrict__ flo, const int* __restrict__ fhi, int nleaf,
+                             int* __restrict__ leaf_of_fn) {
+    const int r = blockIdx.x;
+    if (r >= nleaf) return;
+    for (int f = flo[r] + threadIdx.x; f < fhi[r]; f += blockDim.x) leaf_of_fn[f] = r;
+}
+
+__global__ void __launch_bounds__(256) k_span_mask(const int64_t* __restrict__ K, int n, const int* __restrict__ flo,
+                                                   const int* __restrict__ fhi, int nleaf,
+                                                   const int* __restrict__ leaf_of_fn, uint8_t* __restrict__ mask) {
+    extern __shared__ unsigned s_flag[];   // one bit per column span
+    const int r = blockIdx.x, words = (nleaf + 31) / 32;
+    for (int i = threadIdx.x; i < words; i += blockDim.x) s_flag[i] = 0u;
+    __syncthreads();
+    for (int row = flo[r]; row < fhi[r]; ++row) {
+        const int64_t* kr = K + (int64_t)row * n;
+        for (int c = threadIdx.x; c < n; c += blockDim.x)
+            if (__ldcs(kr + c) != 0) {
+                const int lc = leaf_of_fn[c];
+                atomicOr(&s_flag[lc >> 5], 1u << (lc & 31));
+            }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nleaf; c += blockDim.x)
+        mask[(int64_t)r * nleaf + c] = (uint8_t)((s_flag[c >> 5] >> (c & 31)) & 1u);
+}
+
+// K addresses rows relative to row_base (K may be a row block of the matrix)
+template <bool PACK>
+__global__ void __launch_bounds__(256) k_span_move(int64_t* __restrict__ K, int n, int row_base,
+                                                   const int* __restrict__ flo, const int* __restrict__ fhi, int nleaf,
+                                                   int r0, const int* __restrict__ leaf_of_fn,
+                                                   const uint8_t* __restrict__ mask, const int64_t* __restrict__ off,
+                                                   int64_t off_base, int64_t* __restrict__ buf) {
+    const int r = r0 + blockIdx.x;
+    const uint8_t* mr = mask + (int64_t)r * nleaf;
+    const int64_t* orow = off + (int64_t)r * nleaf;
+    for (int row = flo[r]; row < fhi[r]; ++row) {
+        int64_t* kr = K + (int64_t)(row - row_base) * n;
+        const int dr = row - flo[r];
+        for (int c = threadIdx.x; c < n; c += blockDim.x) {
+            const int lc = leaf_of_fn[c];
+            if (!mr[lc]) continue;
+            const int w = fhi[lc] - flo[lc];
+            int64_t* b = buf + (orow[lc] - off_base) + (int64_t)dr * w + (c - flo[lc]);
+            if (PACK) *b = kr[c];
+            else kr[c] = *b;
+        }
+    }
+}
+
+}  // namespace
+
+void span_index_device(const int* flo, const int* fhi, int nleaf, int* leaf_of_fn, cudaStream_t st) {
+    if (nleaf <= 0) return;
+    { k_span_index<<<nleaf, 32, 0, st>>>(flo, fhi, nleaf, leaf_of_fn); note_launch(); }
+    HXF_CUDA(cudaGetLastError());
+}
+
+void span_mask_device(const int64_t* K, int n, const int* flo, const int* fhi, int nleaf, uint8_t* mask,
+                      cudaStream_t st) {
+    if (nleaf <= 0 || n <= 0) return;
+    int* lof = (int*)hxf_cache_alloc((size_t)n * sizeof(int), st);
+    span_index_device(flo, fhi, nleaf, lof, st);
+    const size_t smem = (size_t)((nleaf + 31) / 32) * sizeof(unsigned);
+    { k_span_mask<<<nleaf, 256, smem, st>>>(K, n, flo, fhi, nleaf, lof, mask); note_launch(); }
+    HXF_CUDA(cudaGetLastError());
+    hxf_cache_free(lof, st);
+}
+
+void span_move_device(int64_t* K, int n, int row_base, const int* flo, const int* fhi, int nleaf, int r0, int r1,
+                      const uint8_t* mask, const int64_t* off, int64_t off_base, int64_t* buf, bool pack,
+                      cudaStream_t st) {
+    if (r1 <= r0 || n <= 0) return;
+    int* lof = (int*)hxf_cache_alloc((size_t)n * sizeof(int), st);
+    span_index_device(flo, fhi, nleaf, lof, st);
+    if (pack) k_span_move<true><<<r1 - r0, 256, 0, st>>>(K, n, row_base, flo, fhi, nleaf, r0, lof, mask, off, off_base, buf);
+    else k_span_move<false><<<r1 - r0, 256, 0, st>>>(K, n, row_base, flo, fhi, nleaf, r0, lof, mask, off, off_base, buf);
+    note_launch();
+    HXF_CUDA(cudaGetLastError());
+    hxf_cache_free(lof, st);
+}

@@ -282,6 +282,195 @@ def allreduce_fixed_sparse(Kfx, counters_vec, group=None, block=64, ops=None):
     return Kfx, counters_vec, stats
 
 
+# ---------------------------------------------------------------------------
+# K as a block-sparse quadtree over the partition + a row-owning reduce-scatter
+# (second part; PAPER.md:174-198 writes the K update block by block over
+# the same index bisection as P).
+
+def leaf_function_ranges(part):
+    """(flo, fhi): int32 function ranges of the partition's leaf spans, in order."""
+    leaves = part.leaves
+    return (np.asarray([s.fn_lo for s in leaves], dtype=np.int32),
+            np.asarray([s.fn_hi for s in leaves], dtype=np.int32))
+
+
+class KQuadtree:
+    """Occupancy quadtree of a block-sparse K: level L holds one flag per (row span,
+    column span) pair of the partition's level-L spans (Partition.levels: ragged leaves
+    repeat at deeper levels), set when any leaf tile below it holds a nonzero.  The
+    bottom level is the leaf-tile mask the device computed (hxf_span_mask)."""
+
+    def __init__(self, part, leaf_mask):
+        leaves = part.leaves
+        nl = len(leaves)
+        m = np.asarray(leaf_mask, dtype=np.uint8).reshape(nl, nl)
+        self.partition = part
+        self.leaf_mask = m
+        self.flo, self.fhi = leaf_function_ranges(part)
+        first = {id(s): k for k, s in enumerate(leaves)}
+        # leaf-index range [a, b) under every span of every level
+        def rng(s):
+            t = s
+            while not t.is_leaf:
+                t = t.left
+            a = first[id(t)]
+            t = s
+            while not t.is_leaf:
+                t = t.right
+            return a, first[id(t)] + 1
+        integ = np.zeros((nl + 1, nl + 1), dtype=np.int64)
+        integ[1:, 1:] = m.astype(np.int64).cumsum(0).cumsum(1)
+        self.levels = []
+        for spans in part.levels:
+            r = np.asarray([rng(s) for s in spans], dtype=np.int64)
+            a, b = r[:, 0], r[:, 1]
+            cnt = integ[b][:, b] - integ[a][:, b] - integ[b][:, a] + integ[a][:, a]
+            self.levels.append(cnt > 0)
+
+    @property
+    def n_levels(self):
+        return len(self.levels)
+
+    def occupied(self, level, i, j):
+        return bool(self.levels[level][i, j])
+
+    @property
+    def nnz_tiles(self):
+        return int(self.leaf_mask.sum())
+
+    @property
+    def stored_elements(self):
+        nf = (self.fhi - self.flo).astype(np.int64)
+        return int((self.leaf_mask.astype(np.int64) * np.outer(nf, nf)).sum())
+
+    def fill(self, level=None):
+        """Occupied fraction of a level's nodes (default: the leaf level)."""
+        lv = self.levels[-1 if level is None else level]
+        return float(lv.mean()) if lv.size else 0.0
+
+
+class _NativeSpanOps:
+    """Leaf-span tile ops of libhxf (csrc/reduce.cu) on CUDA int64 tensors."""
+
+    @staticmethod
+    def mask(K, flo_d, fhi_d):
+        import torch
+        nl = flo_d.numel()
+        m = torch.empty(nl * nl, dtype=torch.uint8, device=K.device)
+        _native.check(_native.lib().hxf_span_mask(ctypes.c_void_p(K.data_ptr()), K.shape[1],
+                                                  ctypes.c_void_p(flo_d.data_ptr()), ctypes.c_void_p(fhi_d.data_ptr()),
+                                                  nl, ctypes.c_void_p(m.data_ptr()), _native.current_stream()))
+        return m
+
+    @staticmethod
+    def move(K, row_base, flo_d, fhi_d, r0, r1, m, off, off_base, buf, pack):
+        fn = _native.lib().hxf_span_pack if pack else _native.lib().hxf_span_unpack
+        _native.check(fn(ctypes.c_void_p(K.data_ptr()), K.shape[1], int(row_base),
+                         ctypes.c_void_p(flo_d.data_ptr()), ctypes.c_void_p(fhi_d.data_ptr()), flo_d.numel(),
+                         int(r0), int(r1), ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(off.data_ptr()),
+                         int(off_base), ctypes.c_void_p(buf.data_ptr()), _native.current_stream()))
+
+    @staticmethod
+    def fold(K):
+        _native.check(_native.lib().hxf_fixed_fold(ctypes.c_void_p(K.data_ptr()), K.shape[0],
+                                                   _native.current_stream()))
+
+
+class KRowBlock:
+    """What one rank holds after reduce_scatter_quadtree: the reduced leaf tiles of its
+    row spans [r0, r1) (functions [f0, f1)), packed, in fixed point."""
+
+    def __init__(self, r0, r1, f0, f1, n, flo_d, fhi_d, mask, off, off_base, buf, scale, folded, ops):
+        self.r0, self.r1, self.f0, self.f1, self.n = r0, r1, f0, f1, n
+        self._flo, self._fhi, self.mask, self.off, self.off_base = flo_d, fhi_d, mask, off, off_base
+        self.tiles = buf
+        self.scale, self.folded, self._ops = scale, folded, ops
+
+    def dense_fixed(self):
+        """(f1 - f0) x n int64 row block (zero outside the stored tiles)."""
+        import torch
+        out = torch.zeros((max(self.f1 - self.f0, 0), self.n), dtype=torch.int64, device=self.tiles.device)
+        if self.r1 > self.r0 and out.numel():
+            self._ops.move(out, self.f0, self._flo, self._fhi, self.r0, self.r1, self.mask, self.off,
+                           self.off_base, self.tiles, False)
+        return out
+
+    def dense(self):
+        """The rank's rows of K in FP64: fixed / 2^scale, halved when the partials were folded
+        (K = (A + A^T) / 2, the fourfold epilogue of exchange_symmetry.py:197-209)."""
+        import torch
+        k = torch.ldexp(self.dense_fixed().to(torch.float64),
+                        torch.tensor(-self.scale - (1 if self.folded else 0), device=self.tiles.device))
+        return k
+
+
+def reduce_scatter_quadtree(Kfx, part, scale, group=None, fold=False, ops=None):
+    """Row-owning block-sparse reduction of the shard accumulators.
+
+    Kfx: this rank's n x n int64 fixed-point partial.  fold=True first forms A + A^T in
+    place (exact), so the reduced rows are already those of the symmetrised fourfold K.
+    The leaf-tile occupancy is OR-ed over the job, the union's tiles are packed in tile
+    row-major order, the row spans are cut into one contiguous range per rank with about
+    equal packed elements, and each range is sum-reduced to its owner (one reduce per
+    owner: NCCL and gloo both carry it; the bytes are those of a reduce-scatter).  No
+    rank receives rows it does not own and no zero tile travels.  Returns (KRowBlock,
+    KQuadtree, stats)."""
+    import torch
+    import torch.distributed as dist
+    ops = ops or _NativeSpanOps
+    multi = dist.is_initialized() and dist.get_world_size(group) > 1
+    world = dist.get_world_size(group) if multi else 1
+    rank = dist.get_rank(group) if multi else 0
+    n = Kfx.shape[0]
+    flo, fhi = leaf_function_ranges(part)
+    nl = len(flo)
+    flo_d = torch.from_numpy(flo).to(Kfx.device)
+    fhi_d = torch.from_numpy(fhi).to(Kfx.device)
+    if fold:
+        ops.fold(Kfx)
+    m = ops.mask(Kfx, flo_d, fhi_d)
+    if multi:
+        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    nf = (fhi_d - flo_d).to(torch.int64)
+    sizes = (m.view(nl, nl).to(torch.int64) * nf[:, None] * nf[None, :]).reshape(-1)
+    off = torch.zeros(nl * nl + 1, dtype=torch.int64, device=Kfx.device)
+    torch.cumsum(sizes, 0, out=off[1:])
+    row_start = off[::nl][: nl + 1].cpu().numpy() if nl else np.zeros(1, dtype=np.int64)
+    if len(row_start) < nl + 1:
+        row_start = np.append(row_start, int(off[-1]))
+    total = int(row_start[-1])
+    # row-span cuts: rank k owns spans [cut[k], cut[k+1]) holding ~total / world elements
+    cut = [0]
+    for k in range(1, world):
+        cut.append(int(np.searchsorted(row_start, total * k / world, side="left")))
+    cut.append(nl)
+    cut = np.maximum.accumulate(np.minimum(cut, nl))
+    buf = torch.empty(max(total, 1), dtype=torch.int64, device=Kfx.device)
+    if total:
+        ops.move(Kfx, 0, flo_d, fhi_d, 0, nl, m, off, 0, buf, True)
+    mine = None
+    works = []
+    for k in range(world):
+        a, b = int(row_start[cut[k]]), int(row_start[cut[k + 1]])
+        seg = buf[a:b]
+        if multi and b > a:
+            works.append(dist.reduce(seg, dst=dist.get_global_rank(group, k) if group is not None else k,
+                                     group=group, async_op=True))
+        if k == rank:
+            mine = (int(cut[k]), int(cut[k + 1]), a, b)
+    for w in works:
+        w.wait()
+    r0, r1, a, b = mine
+    f0 = int(flo[r0]) if r1 > r0 else 0
+    f1 = int(fhi[r1 - 1]) if r1 > r0 else 0
+    block = KRowBlock(r0, r1, f0, f1, n, flo_d, fhi_d, m, off, a, buf[a:b].clone(), scale, fold, ops)
+    tree = KQuadtree(part, m.cpu().numpy())
+    stats = {"leaf_tiles": nl * nl, "leaf_tiles_nonzero": tree.nnz_tiles, "packed_elements": total,
+             "bytes_packed": total * 8, "bytes_dense": n * n * 8, "bytes_owned": (b - a) * 8,
+             "row_spans": (r0, r1), "rows": (f0, f1)}
+    return block, tree, stats
+
+
 def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, shards=None,
                      sparse_block=None):
     """One rank's share of a sharded build + the all-reduce of K and counters.
@@ -320,3 +509,36 @@ def exchange_sharded(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, sha
         _native.check(_native.lib().hxf_symmetrize(ctypes.c_void_p(K_dev.data_ptr()), K_dev.shape[0],
                                                    1e-10, _native.current_stream()))
     return counters_from_vector(vec.cpu().numpy(), symmetry), shards
+
+
+def exchange_sharded_rows(bra, ket, P, tau_2e, mode, symmetry, K_dev, group=None, shards=None):
+    """One rank's share of a sharded build, reduced with reduce_scatter_quadtree: every rank
+    ends with only its own rows of K (a KRowBlock of leaf tiles) and the K quadtree.
+
+    K_dev (n x n float64, CUDA) is the rank's scratch for its fixed-point partial.  For the
+    fourfold driver the partials are folded (A + A^T, exact) before the reduction, so the
+    owned rows are those of the symmetrised K = (A + A^T) / 2 (exchange_symmetry.py:197-209);
+    the 1e-10 asymmetry check of that epilogue needs both triangles of the reduced matrix and
+    is not made here.  Returns (KRowBlock, KQuadtree, counters, stats)."""
+    import torch
+    import torch.distributed as dist
+
+    if symmetry not in (False, True):
+        raise ValueError("exchange_sharded_rows: naive or fourfold driver")
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if shards is None:
+        shards = plan(bra, ket, P, tau_2e, mode, symmetry, world)
+    level, ranges = shards
+    b, e, stride = ranges[rank]
+    from .exchange import check_device_matrix
+    check_device_matrix(K_dev, bra.row.n_functions, "float64", bra._t.ds.device_index, "K_dev")
+    Kfx = K_dev.view(torch.int64)
+    (_, S), c, _ = run_exchange(bra, ket, P, tau_2e, mode, symmetry, True, None, K_out=Kfx,
+                                shard=(level, b, e, stride), symmetrize=False, K_fixed=True)
+    vec = torch.from_numpy(counters_vector(c)).to(K_dev.device)
+    if dist.is_initialized() and world > 1:
+        dist.all_reduce(vec, group=group)
+    block, tree, stats = reduce_scatter_quadtree(Kfx, bra._t.partition,
+                                                 S, group=group, fold=bool(symmetry))
+    return block, tree, counters_from_vector(vec.cpu().numpy(), symmetry), stats

@@ -319,3 +319,110 @@ def test_gloo_block_sparse_allreduce_equals_dense(tmp_path):
     assert np.array_equal(res["K"], dense)
     assert res["vec"][0] == 3.0
     assert 0 < int(res["nz"]) < int(res["tiles"])        # the band leaves tiles out
+
+
+# ------------------------------- K quadtree + row-owning reduce-scatter (§8(f) f4, second part)
+
+class _TorchSpanOps:
+    """CPU stand-in for the libhxf leaf-span tile kernels (test checker only): the host
+    logic of distributed.reduce_scatter_quadtree runs over gloo with these."""
+
+    @staticmethod
+    def mask(K, flo, fhi):
+        nl = flo.numel()
+        m = torch.zeros(nl, nl, dtype=torch.uint8)
+        for r in range(nl):
+            for c in range(nl):
+                m[r, c] = int((K[flo[r]:fhi[r], flo[c]:fhi[c]] != 0).any())
+        return m.reshape(-1)
+
+    @staticmethod
+    def move(K, row_base, flo, fhi, r0, r1, m, off, off_base, buf, pack):
+        nl = flo.numel()
+        for r in range(r0, r1):
+            for c in range(nl):
+                if not m[r * nl + c]:
+                    continue
+                h, w = int(fhi[r] - flo[r]), int(fhi[c] - flo[c])
+                a = int(off[r * nl + c]) - off_base
+                tile = K[int(flo[r]) - row_base:int(fhi[r]) - row_base, int(flo[c]):int(fhi[c])]
+                if pack:
+                    buf[a:a + h * w] = tile.reshape(-1)
+                else:
+                    tile.copy_(buf[a:a + h * w].view(h, w))
+
+    @staticmethod
+    def fold(K):
+        K.add_(K.t().clone())
+
+
+def _span_partition():
+    """A ragged partition: s and p shells mixed, leaf spans of 3..6 functions."""
+    cfg = configs.cube_cluster(6, 11, "sp")
+    import paper_1401_6961_b200 as hx
+    return hx.build_partition(cfg.system, leaf_size=6), cfg.system.n_functions
+
+
+def _span_partial(rank, n):
+    g = torch.Generator().manual_seed(300 + rank)
+    K = torch.randint(-2**40, 2**40, (n, n), generator=g, dtype=torch.int64)
+    i = torch.arange(n)
+    K[(i[:, None] - i[None, :]).abs() > 9] = 0
+    K[n - 4:, :3] = 11 * (rank + 1)          # a far corner tile, one-sided
+    if rank == 1:
+        K[:5, :] = 0                         # rank 1 holds nothing in the first rows
+    return K
+
+
+def _scatter_worker(rank, world, port, result_path, fold):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    part, n = _span_partition()
+    K = _span_partial(rank, n)
+    block, tree, stats = distributed.reduce_scatter_quadtree(K, part, scale=20, fold=fold, ops=_TorchSpanOps)
+    np.savez(result_path + f".{rank}.npz", rows=block.dense_fixed().numpy(), f0=block.f0, f1=block.f1,
+             dense=block.dense().numpy(), leaf=tree.leaf_mask, top=tree.levels[0], l1=tree.levels[1],
+             packed=stats["packed_elements"], owned=stats["bytes_owned"], nnz=tree.nnz_tiles,
+             stored=tree.stored_elements)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fold", [False, True])
+def test_gloo_quadtree_reduce_scatter_rows(tmp_path, fold):
+    path = str(tmp_path / "rs")
+    mp.spawn(_scatter_worker, args=(2, _free_port(), path, fold), nprocs=2, join=True)
+    part, n = _span_partition()
+    parts = [_span_partial(r, n) for r in range(2)]
+    if fold:
+        parts = [p + p.t() for p in parts]
+    full = (parts[0] + parts[1]).numpy()
+    got = [np.load(path + f".{r}.npz") for r in range(2)]
+    # the two ranks own disjoint, contiguous row ranges that cover every row
+    assert int(got[0]["f0"]) == 0 and int(got[0]["f1"]) == int(got[1]["f0"]) and int(got[1]["f1"]) == n
+    assert 0 < int(got[0]["f1"]) < n
+    for g in got:
+        f0, f1 = int(g["f0"]), int(g["f1"])
+        assert np.array_equal(g["rows"], full[f0:f1])             # exact integer sum of the owner's rows
+        scale = 2.0 ** -(20 + (1 if fold else 0))
+        assert np.array_equal(g["dense"], full[f0:f1].astype(np.float64) * scale)
+    # the quadtree: leaf occupancy = union of the ranks' nonzero leaf tiles, OR-ed upward
+    flo, fhi = distributed.leaf_function_ranges(part)
+    nl = len(flo)
+    union = np.zeros((nl, nl), dtype=np.uint8)
+    for p in parts:
+        for r in range(nl):
+            for c in range(nl):
+                union[r, c] |= int((p[flo[r]:fhi[r], flo[c]:fhi[c]] != 0).any())
+    assert np.array_equal(got[0]["leaf"], union) and np.array_equal(got[1]["leaf"], union)
+    assert bool(got[0]["top"][0, 0]) and got[0]["top"].shape == (1, 1)
+    lv1 = part.levels[1]
+    leaves = part.leaves
+    for a, sa in enumerate(lv1):
+        for b, sb in enumerate(lv1):
+            ra = [k for k, s in enumerate(leaves) if sa.fn_lo <= s.fn_lo and s.fn_hi <= sa.fn_hi]
+            rb = [k for k, s in enumerate(leaves) if sb.fn_lo <= s.fn_lo and s.fn_hi <= sb.fn_hi]
+            assert bool(got[0]["l1"][a, b]) == bool(union[np.ix_(ra, rb)].any())
+    assert 0 < int(got[0]["nnz"]) < nl * nl                        # the band leaves tiles out
+    assert int(got[0]["packed"]) == int(got[0]["stored"])
+    assert int(got[0]["owned"]) + int(got[1]["owned"]) == 8 * int(got[0]["packed"])

@@ -55,6 +55,18 @@ def _worker(rank, world, port, out_path):
                 torch.cuda.synchronize()
                 res[f"{tag}_{strategy}_{sparse}"] = K.cpu().numpy()
                 res[f"{tag}_{strategy}_{sparse}_q"] = np.int64(c.eri_shell_quartets)
+    # row-owning reduce-scatter over the K quadtree (every rank saves its own rows)
+    for sym, tag in ((True, "fourfold"), (False, "naive")):
+        Pt = hx.build_matrix_tree(P, part)
+        K = torch.empty((n, n), dtype=torch.float64, device=dev)
+        shards = distributed.plan(pairs, pairs, Pt, cfg.tau_2e, "schwarz", sym, world,
+                                  min_tasks_per_rank=8, strategy="hashed")
+        block, tree, c, stats = distributed.exchange_sharded_rows(pairs, pairs, Pt, cfg.tau_2e, "schwarz", sym, K,
+                                                                  shards=shards)
+        torch.cuda.synchronize()
+        np.savez(out_path + f".rows_{tag}_{rank}.npz", rows=block.dense().cpu().numpy(), f0=block.f0, f1=block.f1,
+                 q=np.int64(c.eri_shell_quartets), nnz=tree.nnz_tiles, tiles=stats["leaf_tiles"],
+                 packed=stats["bytes_packed"], dense=stats["bytes_dense"])
     if rank == 0:
         np.savez(out_path, **res)
     dist.barrier()
@@ -78,3 +90,13 @@ def test_two_ranks_on_one_device_reproduce_the_single_device_K(tmp_path):
                 key = f"{tag}_{strategy}_{sparse}"
                 assert np.array_equal(res[key], K1), key           # bitwise: exact integer all-reduce
                 assert int(res[key + "_q"]) == c1.eri_shell_quartets, key
+        # reduce-scatter: the two ranks' row blocks tile K; fourfold rows are (A + A^T) / 2 formed
+        # in fixed point (one rounding) against the epilogue's FP64 average of two rounded values
+        got = [np.load(out + f".rows_{tag}_{r}.npz") for r in range(2)]
+        assert int(got[0]["f0"]) == 0 and int(got[0]["f1"]) == int(got[1]["f0"]) and int(got[1]["f1"]) == n
+        Krs = np.concatenate([g["rows"] for g in got], axis=0)
+        tol = 4e-16 * np.abs(K1).max() if sym else 0.0
+        assert np.abs(Krs - K1).max() <= tol, tag
+        assert int(got[0]["q"]) == c1.eri_shell_quartets
+        assert 0 < int(got[0]["nnz"]) <= int(got[0]["tiles"])
+        assert int(got[0]["packed"]) <= int(got[0]["dense"])
