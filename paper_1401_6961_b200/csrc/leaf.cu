@@ -840,8 +840,11 @@ __device__ __forceinline__ void k_add_warp(const EriArgs& e, bool on, int row, i
     if (leader && on && fv) atomicAdd(e.K + key, (unsigned long long)fv);
 }
 
+// (re-tuned after the bra-node-major leaf order, profiles/r02_ab_locality.log: with the memory
+// path relieved the near (ss|ss) kernel prefers 2 blocks / 255 registers, the far-field kernels
+// more resident blocks: c5 ERI kernels 3366 -> 3188 ms)
 #ifndef HXF_ERI_MINB0
-#define HXF_ERI_MINB0 3
+#define HXF_ERI_MINB0 2
 #endif
 
 #ifndef HXF_ERI_MINB1
@@ -858,12 +861,12 @@ __host__ __device__ constexpr int eri_min_blocks(int la, int lb, int lc, int ld)
                                                                                    : HXF_ERI_MINB1;
 }
 // far-field kernels: no Boys table and shorter dependency chains, so more
-// resident blocks ((ss|ss): 4 = <= 128 registers; p classes 2, as measured: 3 spills)
+// resident blocks ((ss|ss): 6 = <= 80 registers; p classes 3; measured 4/5/6/8 and 2/3/4)
 #ifndef HXF_ERI_FAR_MINB0
-#define HXF_ERI_FAR_MINB0 4
+#define HXF_ERI_FAR_MINB0 6
 #endif
 #ifndef HXF_ERI_FAR_MINB1
-#define HXF_ERI_FAR_MINB1 2
+#define HXF_ERI_FAR_MINB1 3
 #endif
 __host__ __device__ constexpr int eri_far_min_blocks(int la, int lb, int lc, int ld) {
     return (la + lb + lc + ld) == 0 ? HXF_ERI_FAR_MINB0 : HXF_ERI_FAR_MINB1;
