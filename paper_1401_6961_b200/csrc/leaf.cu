@@ -1738,8 +1738,11 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     const int sw = flat ? SCREEN_WARPS
                         : (ms8 ? (sym ? screen2_warps<true, 8>() : screen2_warps<false, 8>())
                                : (sym ? screen2_warps<true, 10>() : screen2_warps<false, 10>()));
+    // HXF_SCREEN_BLOCKS=k: k blocks per SM instead (with HXF_PIPE=1: room for co-resident ERI blocks)
+    const char* sbk = getenv("HXF_SCREEN_BLOCKS");
+    const int screen_per_sm = sbk ? std::max(1, atoi(sbk)) : (sym ? 12 : 8);
     const unsigned screen_grid = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * (sym ? 12 : 8)));
+        1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * screen_per_sm));
     auto launch_screen = [&](bool emit) {
         // task runs per warp: up to tblock_max, shorter when the range would leave warps idle
         sa.tblock = (int)std::max<int64_t>(1, std::min<int64_t>(tblock_max, (sa.t1 - sa.t0) / ((int64_t)screen_grid * sw)));
