@@ -1738,9 +1738,11 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     const int sw = flat ? SCREEN_WARPS
                         : (ms8 ? (sym ? screen2_warps<true, 8>() : screen2_warps<false, 8>())
                                : (sym ? screen2_warps<true, 10>() : screen2_warps<false, 10>()));
-    // HXF_SCREEN_BLOCKS=k: k blocks per SM instead (with HXF_PIPE=1: room for co-resident ERI blocks)
+    // 48 blocks per SM (4 are resident): the cost of a warp's task runs varies, and a finer
+    // deal evens the tail of each chunk's launch (c5 screen: 12 -> 1818 ms, 24 -> 1755, 36 -> 1697,
+    // 48 -> 1655, 96 -> 1734).  HXF_SCREEN_BLOCKS=k overrides.
     const char* sbk = getenv("HXF_SCREEN_BLOCKS");
-    const int screen_per_sm = sbk ? std::max(1, atoi(sbk)) : (sym ? 12 : 8);
+    const int screen_per_sm = sbk ? std::max(1, atoi(sbk)) : (sym ? 48 : 32);
     const unsigned screen_grid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((tr.n_leaf + sw - 1) / sw, (int64_t)dev_sms * screen_per_sm));
     auto launch_screen = [&](bool emit) {
@@ -1827,8 +1829,9 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         const char* pv = getenv("HXF_PIPE");
         const bool pipe = pv && pv[0] == '1';
         const int NB = pipe ? 2 : 1;
-        // (a full-size chunk set is 2^29 records x 160 B; cached scratch of other builds yields to it)
-        const size_t freeb = hxf_free_memory((size_t)160 * NB << 29);
+        // (a full-size chunk set is 2^29 records x 160 B; when not even a quarter of that is free,
+        // the cached scratch of other builds is handed back first)
+        const size_t freeb = hxf_free_memory((size_t)160 * NB << 27);
         // survivor chunk capacity: ~40 B of device memory per record and buffer
         // set (two record buffers, two key buffers, radix-sort scratch)
         const int64_t cap = std::min<int64_t>(1ll << 29, std::max<int64_t>(1 << 16, (int64_t)(freeb / (160 * NB))));
@@ -2398,7 +2401,7 @@ int direct_run(hxf_pairs* pairs, hxf_density* dens, const hxf_exchange_opts* o, 
     if (o->evaluate && total) {
         Kfx = lalloc<unsigned long long>(nfn2, st);
         HXF_CUDA(cudaMemsetAsync(Kfx, 0, nfn2 * sizeof(unsigned long long), st));
-        const size_t freeb = hxf_free_memory((size_t)160 << 29);
+        const size_t freeb = hxf_free_memory((size_t)160 << 27);
         const int64_t cap = std::min<int64_t>(1ll << 29, std::max<int64_t>(1 << 16, (int64_t)(freeb / 160)));
         SurvivorBufs sb;
         survivor_bufs_alloc(sb, cap, st);
