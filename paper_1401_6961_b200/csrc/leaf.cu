@@ -94,7 +94,7 @@ struct ScreenArgs {
 // ~170 ms of sort per c5 build and costs 880 ms in the ERI kernels, whose warps then mix
 // bra primitive counts: profiles/r02_ab_eri_memory.log.  13 bits stay.)
 // ERI bin of a survivor (written over the screen's 12-bit class / count key by
-// k_bin_classify): ((far * 16 + class) * 9 + nb-1) * 9 + nk-1, 2592 bins (a pair has at most
+// k_binb_classify): ((far * 16 + class) * 9 + nb-1) * 9 + nk-1, 2592 bins (a pair has at most
 // 3 x 3 primitives); slab padding goes to bin ERI_NBINS.  One ERI kernel per (far, class)
 // reads the 81 bins of its primitive-count combinations as one record range.
 // (Measured and dropped: bra pair id bits appended to the key -- with the leaf tasks in
@@ -1067,27 +1067,28 @@ __global__ void __launch_bounds__(128, FAR ? eri_far_min_blocks(LA, LB, LC, LD) 
 
 // Survivor binning: a stable counting sort by ERI bin in four kernels (no library sort).
 //
-// Every warp owns one contiguous run of the chunk's records (a "column") and walks it in
-// order with private shared-memory counters, so no atomics are needed and the sort is
-// stable: inside a bin the records keep the screen's order, which is the locality the ERI
-// kernels live on (neighbouring records = neighbouring leaf tasks of one bra node).
+// A column is the contiguous record run of one block of BINB_WARPS warps, walked in tiles of
+// BINB_WARPS x 32 x BINB_ITEMS records; warp w owns records [w, w + 1) x 32 x BINB_ITEMS of a
+// tile.
 //
-// k_bin_classify  per-quartet far-field test + final bin id, written over the screen's key,
-//                 and the column's histogram.  The far-field decision is a function of the
-//                 quartet alone (the two pairs' enclosing spheres, k_pair_geo), so every
-//                 driver (naive, fourfold, eightfold, the direct twin) evaluates a given
-//                 quartet with the same arithmetic.
+// k_binb_classify per-quartet far-field test + final bin id, written over the screen's key,
+//                 and the column's histogram (shared-memory atomics: counting needs no order).
+//                 The far-field decision is a function of the quartet alone (the two pairs'
+//                 enclosing spheres, k_pair_geo), so every driver (naive, fourfold, eightfold,
+//                 the direct twin) evaluates a given quartet with the same arithmetic.
 // k_bin_rowscan   per bin: exclusive scan over the columns, in place, and the bin total.
 // k_bin_scan      bin starts from the totals: the ERI kernels' record ranges.
-// k_bin_scatter   every warp re-reads its run and moves the records: slot = bin start +
-//                 column offset + the warp's running count (+ rank among the lanes of the
-//                 same bin, by __match_any_sync).
+// k_binb_scatter  all warps of a block load their records of the tile at once, then take turns
+//                 (warp order, a block barrier per turn) to reserve slots from the block's
+//                 shared running counters: slot = bin start + column offset + running count +
+//                 rank among the lanes of the same bin (__match_any_sync).  The order inside a
+//                 bin is exactly the screen's order (stable), which is the locality the ERI
+//                 kernels live on (neighbouring records = neighbouring leaf tasks of one bra
+//                 node).
 // Traffic: 10 B read + 2 B written, then 10 B read + 8 B written per record.
-#define BIN_WARPS 4
-#ifndef BIN_UNROLL
-#define BIN_UNROLL 8
-#endif
-
+// History (profiles/r02_ab_locality.log): CUB radix sort 448 ms per c5 build; warp columns
+// with private counters 489-504 ms (20 warps per SM bound the loads in flight, 1.5 M slow
+// (column, bin) write cursors lose partial sectors from L2); block columns 334 ms.
 struct BinGeo {
     const float4* bgeo;
     const float* bgip;
@@ -1117,44 +1118,6 @@ __device__ __forceinline__ int eri_bin_of(uint16_t key, uint64_t r, const BinGeo
         }
     }
     return ((far * 16 + cls) * 9 + nb1) * 9 + nk1;
-}
-
-// wseg: records per column, a multiple of 32 * BIN_UNROLL
-__global__ void __launch_bounds__(BIN_WARPS * 32) k_bin_classify(
-    const uint64_t* __restrict__ rec, uint16_t* __restrict__ keys, int64_t n, int64_t wseg, BinGeo g,
-    unsigned* __restrict__ hist) {
-    __shared__ unsigned h_all[BIN_WARPS][ERI_NBINS + 1];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned* h = h_all[wid];
-    for (int i = lane; i <= ERI_NBINS; i += 32) h[i] = 0;
-    __syncwarp();
-    const int64_t col = (int64_t)blockIdx.x * BIN_WARPS + wid, ncol = (int64_t)gridDim.x * BIN_WARPS;
-    const int64_t lo = col * wseg, hi = min(n, lo + wseg);
-    for (int64_t t0 = lo; t0 < hi; t0 += 32 * BIN_UNROLL) {
-        uint16_t key[BIN_UNROLL];
-        uint64_t r[BIN_UNROLL];
-#pragma unroll
-        for (int u = 0; u < BIN_UNROLL; ++u) {
-            const int64_t t = t0 + 32 * u + lane;
-            key[u] = t < hi ? keys[t] : SENTINEL_KEY;
-            r[u] = t < hi ? rec[t] : 0ull;
-        }
-        int bin[BIN_UNROLL];
-#pragma unroll
-        for (int u = 0; u < BIN_UNROLL; ++u) bin[u] = eri_bin_of(key[u], r[u], g);
-#pragma unroll
-        for (int u = 0; u < BIN_UNROLL; ++u) {
-            const int64_t t = t0 + 32 * u + lane;
-            const bool on = t < hi;
-            if (on) keys[t] = (uint16_t)bin[u];
-            const int b = on ? bin[u] : -1 - lane;   // out of range: a group of its own, not counted
-            const unsigned peers = __match_any_sync(0xffffffffu, b);
-            if (on && (__ffs(peers) - 1) == lane) h[b] += (unsigned)__popc(peers);
-            __syncwarp();
-        }
-    }
-    __syncwarp();
-    for (int i = lane; i <= ERI_NBINS; i += 32) hist[(int64_t)i * ncol + col] = h[i];
 }
 
 // per bin (one warp each): exclusive scan of the row of column counts, in place; the row total
@@ -1197,40 +1160,94 @@ __global__ void __launch_bounds__(1024) k_bin_scan(const long long* __restrict__
     for (int b = threadIdx.x; b <= ERI_NBINS + 1; b += 1024) bounds[b] = tot[b];
 }
 
-__global__ void __launch_bounds__(BIN_WARPS * 32) k_bin_scatter(
-    const uint64_t* __restrict__ rec, const uint16_t* __restrict__ keys, int64_t n, int64_t wseg,
+#define BINB_WARPS 8
+// 4 records per thread per tile and 40 registers (6 resident blocks) measured best:
+// 8 / 68 registers 403 ms, 8 / 64 370, 4 / 40 334, 4 / 32 349, 2 / 32 343
+#ifndef BINB_ITEMS
+#define BINB_ITEMS 4
+#endif
+#ifndef BINB_MINB
+#define BINB_MINB 6
+#endif
+#define BINB_TILE (BINB_WARPS * 32 * BINB_ITEMS)
+
+__global__ void __launch_bounds__(BINB_WARPS * 32, BINB_MINB) k_binb_classify(
+    const uint64_t* __restrict__ rec, uint16_t* __restrict__ keys, int64_t n, int64_t seg, BinGeo g,
+    unsigned* __restrict__ hist) {
+    __shared__ unsigned h[ERI_NBINS + 1];
+    for (int i = threadIdx.x; i <= ERI_NBINS; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t lo = blockIdx.x * seg, hi = min(n, lo + seg);
+    for (int64_t tile = lo; tile < hi; tile += BINB_TILE) {
+        const int64_t w0 = tile + (int64_t)wid * 32 * BINB_ITEMS;
+        uint16_t key[BINB_ITEMS];
+        uint64_t r[BINB_ITEMS];
+#pragma unroll
+        for (int u = 0; u < BINB_ITEMS; ++u) {
+            const int64_t t = w0 + 32 * u + lane;
+            key[u] = t < hi ? keys[t] : SENTINEL_KEY;
+            r[u] = t < hi ? rec[t] : 0ull;
+        }
+        int bin[BINB_ITEMS];
+#pragma unroll
+        for (int u = 0; u < BINB_ITEMS; ++u) bin[u] = eri_bin_of(key[u], r[u], g);
+#pragma unroll
+        for (int u = 0; u < BINB_ITEMS; ++u) {
+            const int64_t t = w0 + 32 * u + lane;
+            const bool on = t < hi;
+            if (on) keys[t] = (uint16_t)bin[u];
+            const int b = on ? bin[u] : -1 - lane;   // out of range: a group of its own, not counted
+            const unsigned peers = __match_any_sync(0xffffffffu, b);
+            if (on && (__ffs(peers) - 1) == lane) atomicAdd(&h[b], (unsigned)__popc(peers));   // counting: any order
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i <= ERI_NBINS; i += blockDim.x) hist[(int64_t)i * gridDim.x + blockIdx.x] = h[i];
+}
+
+__global__ void __launch_bounds__(BINB_WARPS * 32, BINB_MINB) k_binb_scatter(
+    const uint64_t* __restrict__ rec, const uint16_t* __restrict__ keys, int64_t n, int64_t seg,
     const unsigned* __restrict__ hist, const int64_t* __restrict__ bounds, uint64_t* __restrict__ out) {
     // next free slot of this column's run in each bin, relative to the bin start (< 2^29 per chunk)
-    __shared__ unsigned pos_all[BIN_WARPS][ERI_NBINS + 1];
+    __shared__ unsigned pos[ERI_NBINS + 1];
+    for (int i = threadIdx.x; i <= ERI_NBINS; i += blockDim.x) pos[i] = hist[(int64_t)i * gridDim.x + blockIdx.x];
+    __syncthreads();
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned* pos = pos_all[wid];
-    const int64_t col = (int64_t)blockIdx.x * BIN_WARPS + wid, ncol = (int64_t)gridDim.x * BIN_WARPS;
-    for (int i = lane; i <= ERI_NBINS; i += 32) pos[i] = hist[(int64_t)i * ncol + col];
-    __syncwarp();
-    const int64_t lo = col * wseg, hi = min(n, lo + wseg);
-    for (int64_t t0 = lo; t0 < hi; t0 += 32 * BIN_UNROLL) {
-        int bin[BIN_UNROLL];
-        uint64_t r[BIN_UNROLL];
+    const int64_t lo = blockIdx.x * seg, hi = min(n, lo + seg);
+    for (int64_t tile = lo; tile < hi; tile += BINB_TILE) {   // block-uniform trip count
+        const int64_t w0 = tile + (int64_t)wid * 32 * BINB_ITEMS;
+        int bin[BINB_ITEMS];
+        uint64_t r[BINB_ITEMS];
 #pragma unroll
-        for (int u = 0; u < BIN_UNROLL; ++u) {
-            const int64_t t = t0 + 32 * u + lane;
+        for (int u = 0; u < BINB_ITEMS; ++u) {
+            const int64_t t = w0 + 32 * u + lane;
             bin[u] = t < hi ? (int)keys[t] : -1 - lane;
             r[u] = t < hi ? rec[t] : 0ull;
         }
+        unsigned dst[BINB_ITEMS];
+        for (int turn = 0; turn < BINB_WARPS; ++turn) {
+            if (turn == wid) {
 #pragma unroll
-        for (int u = 0; u < BIN_UNROLL; ++u) {
-            const int b = bin[u];
-            const unsigned peers = __match_any_sync(0xffffffffu, b);
-            const int leader = __ffs(peers) - 1;
-            unsigned base = 0;
-            if (b >= 0 && leader == lane) {
-                base = pos[b];
-                pos[b] = base + (unsigned)__popc(peers);
+                for (int u = 0; u < BINB_ITEMS; ++u) {
+                    const int b = bin[u];
+                    const unsigned peers = __match_any_sync(0xffffffffu, b);
+                    const int leader = __ffs(peers) - 1;
+                    unsigned base = 0;
+                    if (b >= 0 && leader == lane) {
+                        base = pos[b];
+                        pos[b] = base + (unsigned)__popc(peers);
+                    }
+                    __syncwarp();
+                    base = __shfl_sync(0xffffffffu, base, leader);
+                    dst[u] = base + __popc(peers & ((1u << lane) - 1u));
+                }
             }
-            __syncwarp();
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (b >= 0) out[bounds[b] + base + __popc(peers & ((1u << lane) - 1u))] = r[u];
+            __syncthreads();
         }
+#pragma unroll
+        for (int u = 0; u < BINB_ITEMS; ++u)
+            if (bin[u] >= 0) out[bounds[bin[u]] + dst[u]] = r[u];
     }
 }
 
@@ -1384,7 +1401,7 @@ thread_local double g_timings[8];
 struct SurvivorBufs {
     uint64_t *rec, *rec2;   // screen order; binned
     uint16_t* keys;
-    unsigned* hist;         // (ERI_NBINS + 1) x (bin_blocks * BIN_WARPS columns) counts, then first slots
+    unsigned* hist;         // (ERI_NBINS + 1) x bin_blocks (columns) counts, then first slots
     int bin_blocks;
     int64_t* dbounds;       // ERI_NBINS + 2 bin starts (slab padding last)
     // per-pair spheres for the per-quartet far-field pass (NULL: skip it)
@@ -1421,17 +1438,14 @@ struct Timer {
 // exit at once)
 void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cudaStream_t st,
                             cudaEvent_t after_sort = nullptr) {
-    const int G = b.bin_blocks;
-    const int64_t ncol = (int64_t)G * BIN_WARPS;
-    // contiguous run per column (warp), a multiple of the warp's stride
-    constexpr int64_t WSTEP = 32 * BIN_UNROLL;
-    const int64_t wseg = ((nrec + ncol - 1) / ncol + WSTEP - 1) / WSTEP * WSTEP;
     long long* total = reinterpret_cast<long long*>(b.dbounds + ERI_NBINS + 2);
     const BinGeo geo{b.bgeo, b.bgip, b.kgeo, b.kgip, b.bfcnt, b.kfcnt, (b.bgeo && !HXF_ERI_NOFAR) ? 1 : 0};
-    k_bin_classify<<<G, BIN_WARPS * 32, 0, st>>>(b.rec, b.keys, nrec, wseg, geo, b.hist);
-    k_bin_rowscan<<<(ERI_NBINS + 1 + 7) / 8, 256, 0, st>>>(b.hist, (int)ncol, total);
+    const int G = b.bin_blocks;   // one column per block
+    const int64_t seg = ((nrec + G - 1) / G + BINB_TILE - 1) / BINB_TILE * BINB_TILE;
+    k_binb_classify<<<G, BINB_WARPS * 32, 0, st>>>(b.rec, b.keys, nrec, seg, geo, b.hist);
+    k_bin_rowscan<<<(ERI_NBINS + 1 + 7) / 8, 256, 0, st>>>(b.hist, G, total);
     k_bin_scan<<<1, 1024, 0, st>>>(total, b.dbounds);
-    k_bin_scatter<<<G, BIN_WARPS * 32, 0, st>>>(b.rec, b.keys, nrec, wseg, b.hist, b.dbounds, b.rec2);
+    k_binb_scatter<<<G, BINB_WARPS * 32, 0, st>>>(b.rec, b.keys, nrec, seg, b.hist, b.dbounds, b.rec2);
     for (int k = 0; k < 4; ++k) note_launch();
     if (after_sort) cudaEventRecord(after_sort, st);
     e.rec = b.rec2;
@@ -1450,11 +1464,11 @@ void survivor_bufs_alloc(SurvivorBufs& sb, int64_t cap, cudaStream_t st) {
     sb.rec = lalloc<uint64_t>(cap, st);
     sb.rec2 = lalloc<uint64_t>(cap, st);
     sb.keys = lalloc<uint16_t>(cap, st);
-    // up to 5 blocks of BIN_WARPS warps x 41.5 KB of counters per SM; fewer columns = fewer
-    // concurrent (column, bin) write cursors for L2 to merge into full sectors
+    // 48 columns (blocks) per SM, 6 resident: a finer deal and more loads in flight measured
+    // better up to here (8: 403 ms, 24: 346, 48: 334 per c5 build); HXF_BIN_BLOCKS=k overrides
     const char* bb = getenv("HXF_BIN_BLOCKS");
-    sb.bin_blocks = sms * std::max(1, std::min(5, bb ? atoi(bb) : 5));
-    sb.hist = lalloc<unsigned>((size_t)(ERI_NBINS + 1) * sb.bin_blocks * BIN_WARPS, st);
+    sb.bin_blocks = sms * std::max(1, std::min(64, bb ? atoi(bb) : 48));
+    sb.hist = lalloc<unsigned>((size_t)(ERI_NBINS + 1) * sb.bin_blocks, st);
     sb.dbounds = lalloc<int64_t>(2 * (ERI_NBINS + 2), st);   // bin starts, then the bin totals
 }
 
