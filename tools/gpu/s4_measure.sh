@@ -9,7 +9,7 @@ tail -c 600 gpurun_out/${tag}_bench_c5_fourfold.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/${tag}_launches_c5.csv python tools/one_build.py c5 fourfold - 1 > gpurun_out/${tag}_ncu_launches.log 2>&1; echo launches_rc=$?
 python tools/launch_stats.py gpurun_out/${tag}_launches_c5.csv 40 > gpurun_out/${tag}_launches_c5_summary.txt; head -12 gpurun_out/${tag}_launches_c5_summary.txt
 # DRAM bytes per kernel family of one build
-timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_eri|k_screen2|k_expand|k_bin_|DeviceRadixSort" --csv --log-file gpurun_out/${tag}_dram_launches_c5.csv python tools/one_build.py c5 fourfold - 1 > gpurun_out/${tag}_ncu_dram.log 2>&1; echo dram_rc=$?
+timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_eri|k_screen2|k_expand|k_bin|DeviceRadixSort" --csv --log-file gpurun_out/${tag}_dram_launches_c5.csv python tools/one_build.py c5 fourfold - 1 > gpurun_out/${tag}_ncu_dram.log 2>&1; echo dram_rc=$?
 python tools/ncu_dram.py gpurun_out/${tag}_dram_launches_c5.csv c5 fourfold 1 > gpurun_out/${tag}_ncu_c5_dram.json; head -c 1200 gpurun_out/${tag}_ncu_c5_dram.json
 # full captures: leaf screen, (ss|ss) far and near
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_screen2" -s 8 -c 1 -o gpurun_out/${tag}_full_screen_c5 python tools/one_build.py c5 fourfold - 1 > gpurun_out/${tag}_full_screen.log 2>&1; echo rc=$?

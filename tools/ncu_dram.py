@@ -4,7 +4,7 @@ usage: python tools/ncu_dram.py launches.csv workload mode builds > profiles/rNN
 
 The csv comes from
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
-      --clock-control none -k regex:"k_eri|k_screen2|k_expand|k_bin_|DeviceRadixSort" --csv --log-file launches.csv \
+      --clock-control none -k regex:"k_eri|k_screen2|k_expand|k_bin|DeviceRadixSort" --csv --log-file launches.csv \
       python tools/one_build.py <workload> <mode> - <builds>
 bench.py quotes k_eri's bytes per build as roofline.traffic (ncu replays are
 cold-cache and serialised: bytes are meaningful, times only as shares).
@@ -17,8 +17,8 @@ from tools.tau_sweep import _UNIT  # noqa: E402
 import csv  # noqa: E402
 
 path, workload, mode, builds = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
-# k_bin_classify / k_bin_scatter: survivor binning; DeviceRadixSort: the leaf-task order (cub, keys only)
-fam = {"k_eri": {}, "k_screen2": {}, "k_expand": {}, "k_bin_classify": {}, "k_bin_scatter": {}, "DeviceRadixSort": {}}
+# k_binb_classify / k_binb_scatter: survivor binning; DeviceRadixSort: the leaf-task order (cub, keys only)
+fam = {"k_eri": {}, "k_screen2": {}, "k_expand": {}, "k_binb_classify": {}, "k_binb_scatter": {}, "DeviceRadixSort": {}}
 hdr = None
 launches = {k: set() for k in fam}
 for r in csv.reader(open(path)):
