@@ -1462,7 +1462,8 @@ void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cuda
                             cudaEvent_t after_sort = nullptr) {
     long long* total = reinterpret_cast<long long*>(b.dbounds + ERI_NBINS + 2);
     const BinGeo geo{b.bgeo, b.bgip, b.kgeo, b.kgip, b.bfcnt, b.kfcnt, (b.bgeo && !HXF_ERI_NOFAR) ? 1 : 0};
-    const int G = b.bin_blocks;   // one column per block
+    // one column per block; small chunks (c1 / c2: a few tiles) take only the blocks they fill
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(b.bin_blocks, (nrec + BINB_TILE - 1) / BINB_TILE));
     const int64_t seg = ((nrec + G - 1) / G + BINB_TILE - 1) / BINB_TILE * BINB_TILE;
     k_binb_classify<<<G, BINB_WARPS * 32, 0, st>>>(b.rec, b.keys, nrec, seg, geo, b.hist);
     k_bin_rowscan<<<(ERI_NBINS + 1 + 7) / 8, 256, 0, st>>>(b.hist, G, total);
@@ -1484,7 +1485,8 @@ void eri_sorted_stage_async(EriArgs e, const SurvivorBufs& b, int64_t nrec, cuda
         const char* v = getenv("HXF_ERI_STREAMS");
         return v ? std::max(1, std::min(4, atoi(v))) : 0;
     }();
-    const int n_streams = env_streams ? env_streams : ((int64_t)e.nfn * e.nfn * 8 <= (128ll << 20) ? 4 : 1);
+    const int n_streams = env_streams ? env_streams
+                          : ((int64_t)e.nfn * e.nfn * 8 <= (128ll << 20) && nrec >= (1 << 20) ? 4 : 1);
     EriStreams& xs = eri_streams();
     cudaStream_t lanes[4] = {st, st, st, st};
     if (n_streams > 1) {
