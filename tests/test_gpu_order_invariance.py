@@ -72,7 +72,8 @@ def test_work_order_does_not_change_K(sym):
     K0, c0, d0 = _run(hx, cfg, part, P, pairs, sym)
     assert c0.eri_shell_quartets > 10 ** 6
     for env in ({"HXF_LEAF_SORT": 0}, {"HXF_LEAF_SORT": 0, "HXF_TASK_BLOCK": 1}, {"HXF_TASK_BLOCK": 5},
-                {"HXF_SCREEN_BLOCKS": 3, "HXF_TASK_BLOCK": 64}, {"HXF_BIN_BLOCKS": 1}):
+                {"HXF_SCREEN_BLOCKS": 3, "HXF_TASK_BLOCK": 64}, {"HXF_BIN_BLOCKS": 1},
+                {"HXF_BIN_BLOCKS": 64, "HXF_SCREEN_BLOCKS": 12}):
         with _env(**env):
             K1, c1, d1 = _run(hx, cfg, part, P, pairs, sym)
         assert torch.equal(K0, K1), env
