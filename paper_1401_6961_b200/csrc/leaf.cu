@@ -44,6 +44,7 @@ struct ScreenArgs {
     const uint64_t* tasks;
     int64_t t0, t1;
     int tblock;               // k_screen2: a warp takes runs of tblock consecutive tasks (block-cyclic)
+    unsigned* next_run;       // k_screen2: non-NULL = runs are handed out dynamically (zeroed per launch)
     const int* lslo;
     const int* lshi;
     int nleaf;
@@ -331,7 +332,9 @@ __device__ __forceinline__ int fdiv(int a, int n, float inv) {
 
 // EIGHT (with SYM): the eightfold driver's bra pair <= ket pair rule on bra == ket tasks
 template <bool SYM, bool EMIT, int MS, bool EIGHT = false>
-__global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(ScreenArgs a) {
+// (MS <= 8: 24 resident warps per SM = at most 80 registers, the measured sweet spot,
+// profiles/r02_ab_eri_memory.log; the MS = 10 instances are bound by their shared memory)
+__global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32, MS <= 8 ? 24 / screen2_warps<SYM, MS>() : 1) k_screen2(ScreenArgs a) {
     constexpr int NW = screen2_warps<SYM, MS>();
     __shared__ Smem2<SYM, MS> sm_all[NW];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -352,12 +355,31 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
 #else
 #define PROF_MARK(v)
 #endif
-    // block-cyclic: runs of tblock consecutive leaf tasks per warp, so a warp's survivor slab
-    // (and after the stable key sort every ERI warp) holds neighbouring tasks of one bra node
+    // Runs of tblock consecutive leaf tasks per warp, so a warp's survivor slab (and after the
+    // stable binning every ERI warp) holds neighbouring tasks of one bra node.  The runs are
+    // dealt block-cyclically (next_run == NULL) or handed out by a device counter as warps
+    // finish (the next run is requested while the current one is processed).  Either way a
+    // run's ledger contribution is rounded to fixed point once per run, in a fixed shuffle
+    // tree, so the ledger words do not depend on which warp took which run.
+    // (32-bit run and task indices relative to t0: a chunk holds far fewer than 2^31 tasks)
     const int TB = a.tblock;
-    const int64_t tskip = (Wt - 1) * (int64_t)TB + 1;
-    int trun = 0;
-    for (int64_t t = a.t0 + gw * TB; t < a.t1; t += (++trun == TB ? (trun = 0, tskip) : 1)) {
+    const int ntask = (int)(a.t1 - a.t0);
+    const bool dyn = a.next_run != nullptr;
+    __shared__ unsigned long long s_led[NW][LEDGER_LIMBS];
+    if (lane < LEDGER_LIMBS) s_led[wid][lane] = 0ull;
+    __syncwarp();
+    unsigned run = (unsigned)gw;
+    if (dyn) {
+        unsigned r0 = 0;
+        if (lane == 0) r0 = atomicAdd(a.next_run, 1u);
+        run = __shfl_sync(0xffffffffu, r0, 0);
+    }
+    while ((int64_t)run * TB < ntask) {
+    unsigned pend = 0;
+    if (dyn && lane == 0) pend = atomicAdd(a.next_run, 1u);
+    const int tend = min(ntask, (int)(run * TB) + TB);
+    for (int tl = (int)(run * TB); tl < tend; ++tl) {
+        const int64_t t = a.t0 + tl;
         PROF_MARK(c_start);
         const uint64_t task = a.tasks[t];
         const int mu = task & 0x7fff, nu = (task >> 15) & 0x7fff, lam = (task >> 30) & 0x7fff,
@@ -734,11 +756,27 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
 #endif
         }
     }
+    {   // the run's ledger, rounded once, into the warp's 256-bit partial
+        const double lr = warp_sum(ledger);
+        ledger = 0.0;
+        if (lane == 0 && lr != 0.0) {
+            unsigned long long limb[LEDGER_LIMBS];
+            fx_from_double<LEDGER_LIMBS>(0.5 * lr, LEDGER_SCALE, limb);
+            unsigned long long carry = 0;
+#pragma unroll
+            for (int k = 0; k < LEDGER_LIMBS; ++k) {
+                const unsigned long long x = s_led[wid][k], y = x + limb[k], z = y + carry;
+                carry = (unsigned long long)(y < x) + (unsigned long long)(z < y);
+                s_led[wid][k] = z;
+            }
+        }
+    }
+    run = dyn ? __shfl_sync(0xffffffffu, pend, 0) : run + (unsigned)Wt;
+    }
     if (EMIT) slab_pad(slab, a, lane);
     n_eri = warp_sum_ll(n_eri);
     n_cull = warp_sum_ll(n_cull);
     n_tie = warp_sum_ll(n_tie);
-    ledger = warp_sum(ledger);
     if (lane == 0) {
 #ifdef HXF_PROF_SCREEN
         for (int k = 0; k < 4; ++k) atomic_add_ll(&a.counters[C_DBG0 + k], cyc[k]);
@@ -747,11 +785,14 @@ __global__ void __launch_bounds__(screen2_warps<SYM, MS>() * 32) k_screen2(Scree
         if (n_eri) atomic_add_ll(&a.counters[C_ERIQ], n_eri);
         if (n_cull) atomic_add_ll(&a.counters[C_CULL_LEAF], n_cull);
         if (n_tie) atomic_add_ll(&a.counters[C_TIE_LEAF], n_tie);
-        if (ledger != 0.0) {
-            unsigned long long limb[LEDGER_LIMBS];
-            fx_from_double<LEDGER_LIMBS>(0.5 * ledger, LEDGER_SCALE, limb);
-            fx_atomic_add<LEDGER_LIMBS>(a.ledger, limb);
+        unsigned long long limb[LEDGER_LIMBS];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < LEDGER_LIMBS; ++k) {
+            limb[k] = s_led[wid][k];
+            any |= limb[k] != 0ull;
         }
+        if (any) fx_atomic_add<LEDGER_LIMBS>(a.ledger, limb);
     }
 }
 
@@ -1744,8 +1785,14 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     ScreenArgs sa;
     sa.tasks = tr.leaf;
     const char* tb_env = getenv("HXF_TASK_BLOCK");
-    const int tblock_max = std::max(1, tb_env ? atoi(tb_env) : 16);
+    const int tblock_max = std::max(1, tb_env ? atoi(tb_env) : 32);
     sa.tblock = 1;
+    // HXF_SCREEN_DYN=0: the screen's task runs are dealt block-cyclically instead of handed out
+    // by a device counter
+    const char* dyn_env = getenv("HXF_SCREEN_DYN");
+    const bool screen_dyn = dyn_env ? atoi(dyn_env) != 0 : true;
+    unsigned* drun = lalloc<unsigned>(1, st);
+    sa.next_run = nullptr;
     std::vector<int> lslo(s->n_leaves), lshi(s->n_leaves);
     {
         const int D = s->n_levels - 1;
@@ -1818,6 +1865,11 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
     auto launch_screen = [&](bool emit) {
         // task runs per warp: up to tblock_max, shorter when the range would leave warps idle
         sa.tblock = (int)std::max<int64_t>(1, std::min<int64_t>(tblock_max, (sa.t1 - sa.t0) / ((int64_t)screen_grid * sw)));
+        sa.next_run = nullptr;
+        if (screen_dyn && !flat) {
+            cudaMemsetAsync(drun, 0, sizeof(unsigned), st);
+            sa.next_run = drun;
+        }
         if (flat) {
             if (eight) { if (emit) k_screen<true, true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false, true><<<screen_grid, sw * 32, 0, st>>>(sa); }
             else if (sym) { if (emit) k_screen<true, true><<<screen_grid, sw * 32, 0, st>>>(sa); else k_screen<true, false><<<screen_grid, sw * 32, 0, st>>>(sa); }
@@ -2192,7 +2244,7 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
         for (int k = 0; k < 3; ++k) o->digest[k] = hd[k];
     }
     for (void* p : {(void*)Kfx, (void*)scount, (void*)sledger, (void*)dfill, (void*)dcount,
-                    (void*)dledger, (void*)d_lslo, (void*)d_lshi, (void*)tr.leaf})
+                    (void*)dledger, (void*)d_lslo, (void*)d_lshi, (void*)tr.leaf, (void*)drun})
         if (p) hxf_cache_free(p, st);
     free_tables(etb, st);
     free_tables(etk, st);
