@@ -1857,7 +1857,8 @@ int exchange_run(hxf_pairs* bra, hxf_pairs* ket, hxf_density* dens, const hxf_ex
                                : (sym ? screen2_warps<true, 10>() : screen2_warps<false, 10>()));
     // 48 blocks per SM (4 are resident): the cost of a warp's task runs varies, and a finer
     // deal evens the tail of each chunk's launch (c5 screen: 12 -> 1818 ms, 24 -> 1755, 36 -> 1697,
-    // 48 -> 1655, 96 -> 1734).  HXF_SCREEN_BLOCKS=k overrides.
+    // 48 -> 1655, 96 -> 1734).  With the runs handed out dynamically (HXF_SCREEN_DYN, default) the
+    // grid no longer matters (4 / 8 / 48: 1595 ms).  HXF_SCREEN_BLOCKS=k overrides.
     const char* sbk = getenv("HXF_SCREEN_BLOCKS");
     const int screen_per_sm = sbk ? std::max(1, atoi(sbk)) : (sym ? 48 : 32);
     const unsigned screen_grid = (unsigned)std::max<int64_t>(
